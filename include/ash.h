@@ -1,0 +1,161 @@
+/*
+ * ash.h — C ABI of the B200-native spatial hash map (libash.so).
+ *
+ * This is the drop-in boundary below the reference's Python map API
+ * (/root/reference/pkg/src/spatialhash/hashmap.py:153-515).  The reference has
+ * no FFI of its own — it is pure numpy — so each entry point below names the
+ * reference method whose semantics it implements; INTEGRATION.md shows the
+ * ctypes binding a maintainer would add on the reference side.
+ *
+ * Rules of the ABI
+ *   - Stateless launchers.  All memory (table, buffers, heap, counters, scan
+ *     workspace) is allocated by the caller and described by ash_map_t; no
+ *     ownership crosses the boundary.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*).
+ *     Results that the host needs (sizes, counts, error flags) are written to
+ *     device counters; the caller reads them when it must.
+ *   - Return codes: ASH_OK, or an ASH_ERR_* code with a message retrievable
+ *     through ash_last_error() (thread-local).
+ *   - Plain pointers and sizes only: no torch or CUDA types in signatures.
+ */
+#ifndef ASH_H
+#define ASH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASH_ABI_VERSION 1
+
+#define ASH_OK 0
+#define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
+#define ASH_ERR_CAPACITY 2  /* batch needs more free indices -> CapacityError */
+#define ASH_ERR_CUDA 3      /* launch / runtime failure -> RuntimeError       */
+
+#define ASH_MAX_VALUE_BUFFERS 8
+
+/* device counter slots (int32 each, ASH_N_COUNTERS of them) */
+#define ASH_CTR_TOP 0      /* index-heap top; equals the map size          */
+#define ASH_CTR_USED 1     /* non-EMPTY table slots (live+pending+tomb)    */
+#define ASH_CTR_WINNERS 2  /* new keys of the last insert/activate         */
+#define ASH_CTR_ERASED 3   /* keys removed by the last erase               */
+#define ASH_CTR_FLAGS 4    /* sticky error bits, see ASH_FLAG_*            */
+#define ASH_CTR_COUNT 5    /* result count of the last compaction/voxelize */
+#define ASH_N_COUNTERS 8
+
+#define ASH_FLAG_TABLE_FULL 1  /* a probe wrapped the whole table */
+#define ASH_FLAG_RANGE 2       /* quantized coordinate outside int32 */
+
+/*
+ * Map state.  Table slots are 16 bytes {w0, w1, w2, state}: the first three
+ * key words inline (zero-padded for arity < 3) and
+ *   state = 0xFFFFFFFF EMPTY | 0xFFFFFFFE TOMBSTONE | [0, 2^31) buffer index
+ *         | 0x80000000|pos  (PENDING, only inside one insert batch).
+ * Slots are probed in 32-byte buckets (two slots, one DRAM sector).
+ */
+typedef struct ash_map {
+  void* slots;              /* n_slots x 16 B                                  */
+  int64_t n_slots;          /* power of two, 64 <= n_slots <= 2^30             */
+  int32_t* key_buf;         /* capacity x arity int32  (hashmap.py:203)        */
+  int32_t arity;            /* >= 1                                            */
+  int32_t n_values;         /* number of value buffers, <= 8                   */
+  void* value_bufs[ASH_MAX_VALUE_BUFFERS];          /* capacity x row bytes    */
+  int64_t value_row_bytes[ASH_MAX_VALUE_BUFFERS];   /* hashmap.py:204-206      */
+  int32_t* heap;            /* capacity, index free list (index_heap.py:17-20) */
+  uint8_t* active;          /* capacity, 0/1 (hashmap.py:207)                  */
+  int32_t* erase_claim;     /* capacity, INT32_MAX between calls               */
+  uint8_t* freed;           /* capacity, 0 between calls                       */
+  int32_t* counters;        /* ASH_N_COUNTERS                                  */
+  uint64_t* scan_status;    /* single-pass scan tile status, zeroed once       */
+  int64_t scan_status_len;  /* >= ash_scan_tiles(max(n, capacity))             */
+  int64_t capacity;         /* <= 2^31 - 1                                     */
+  uint32_t epoch;           /* scan epoch; the library bumps it per launch     */
+  uint32_t reserved;
+} ash_map_t;
+
+int ash_abi_version(void);
+const char* ash_last_error(void);
+
+/* Scan-status words needed for a single-pass scan over n items. */
+int64_t ash_scan_tiles(int64_t n);
+
+/* HashMap.__init__/_init_state (hashmap.py:200-210): all slots EMPTY,
+ * heap = arange(capacity), counters 0, active 0; key/value rows zeroed when
+ * zero_rows != 0. */
+int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream);
+
+/* HashMap.find (hashmap.py:415-429): out_idx = buffer index or -1,
+ * out_mask = 1 where present.  One fused hash+probe kernel. */
+int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx,
+             uint8_t* out_mask, void* stream);
+
+/* HashMap.insert / activate (hashmap.py:336-413), generic-backend semantics:
+ * winners are first occurrences of absent keys, winner of rank r gets
+ * heap[top + r].  `values` holds n_values device pointers (rows of
+ * value_row_bytes each, batch order) or is NULL for activate/HashSet.
+ * association != 0 gives activate masks (found OR winner).
+ * Precondition: capacity - size >= n (the caller checks; otherwise use the
+ * claim/count/commit|rollback sequence below). */
+int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n,
+               const void* const* values, int32_t association,
+               int32_t* out_idx, uint8_t* out_mask, void* stream);
+
+/* Split form of ash_insert for the capacity-uncertain path
+ * (hashmap.py:389-396 re-plan on growth, :317-324 CapacityError):
+ *   claim -> count (counters[WINNERS]) -> host reads the count ->
+ *   commit when it fits, else rollback (map unchanged). */
+int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n,
+                     int32_t* out_idx, uint8_t* out_mask, void* stream);
+int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx,
+                     const uint8_t* out_mask, void* stream);
+int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n,
+                      const void* const* values, int32_t association,
+                      int32_t* out_idx, uint8_t* out_mask, void* stream);
+int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx,
+                        void* stream);
+
+/* HashMap.erase (hashmap.py:431-456): first found occurrence per key is
+ * removed; freed indices return to the heap sorted (index_heap.py:38-47).
+ * scratch: 2*n int32 device words. */
+int ash_erase(ash_map_t* m, const int32_t* keys, int64_t n, uint8_t* out_mask,
+              int32_t* scratch, void* stream);
+
+/* HashMap.active_indices (hashmap.py:458-460): ascending; `out` must hold
+ * size entries; the count is also written to counters[COUNT]. */
+int ash_active_indices(ash_map_t* m, int32_t* out, void* stream);
+
+/* HashMap._rehash_into (hashmap.py:326-332): dst is freshly reset; rows
+ * act[0..n_act) of src (ascending) become rows 0..n_act-1 of dst. */
+int ash_rehash_from(ash_map_t* dst, const ash_map_t* src, const int32_t* act,
+                    int64_t n_act, void* stream);
+
+/* Tombstone cleanup: rebuild the table into new_slots (same indices, no API
+ * visible change).  The caller swaps m->slots afterwards. */
+int ash_rebuild_table(ash_map_t* m, void* new_slots, int64_t new_n_slots,
+                      void* stream);
+
+/* Fill a table with EMPTY slots (workspace initialisation). */
+int ash_table_clear(void* slots, int64_t n_slots, void* stream);
+
+/* geometry.quantize (geometry.py:49-56): floor(p / cell) in float64;
+ * out of int32 range sets ASH_FLAG_RANGE in flags[0]. */
+int ash_quantize(const void* points, int32_t points_are_f64, int64_t n,
+                 double cell, int32_t* out_coords, int32_t* flags, void* stream);
+
+/* geometry.voxel_downsample (geometry.py:59-76), fused quantize + set insert
+ * + first-occurrence select.  `ws` supplies an all-EMPTY workspace table
+ * (slots, n_slots >= 2n), counters and scan status; the table is left EMPTY
+ * again.  Writes count voxels to out_coords (count x 3) / out_sel (int64)
+ * in ascending point order; count in ws->counters[COUNT].
+ * scratch_idx: n int32, scratch_mask: n bytes. */
+int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64,
+                 int64_t n, double voxel, int32_t* out_coords, int64_t* out_sel,
+                 int32_t* scratch_idx, uint8_t* scratch_mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ASH_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of libash.so (include/ash.h).
+
+There is no CPU fallback: importing this module without the built library
+raises, and every launcher error surfaces as a Python exception.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_uint32, c_void_p
+
+from .build import LIB_PATH
+
+ASH_OK, ASH_ERR_INVALID, ASH_ERR_CAPACITY, ASH_ERR_CUDA = 0, 1, 2, 3
+MAX_VALUE_BUFFERS = 8
+CTR_TOP, CTR_USED, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT = 0, 1, 2, 3, 4, 5
+N_COUNTERS = 8
+FLAG_TABLE_FULL, FLAG_RANGE = 1, 2
+TILE = 2048  # positions per scan tile (csrc kTile)
+
+
+class AshMap(ctypes.Structure):
+    """Mirror of ``ash_map_t``."""
+    _fields_ = [
+        ("slots", c_void_p), ("n_slots", c_int64),
+        ("key_buf", c_void_p), ("arity", c_int32), ("n_values", c_int32),
+        ("value_bufs", c_void_p * MAX_VALUE_BUFFERS),
+        ("value_row_bytes", c_int64 * MAX_VALUE_BUFFERS),
+        ("heap", c_void_p), ("active", c_void_p), ("erase_claim", c_void_p),
+        ("freed", c_void_p), ("counters", c_void_p), ("scan_status", c_void_p),
+        ("scan_status_len", c_int64), ("capacity", c_int64),
+        ("epoch", c_uint32), ("reserved", c_uint32),
+    ]
+
+
+_M = POINTER(AshMap)
+_SIGNATURES = {
+    "ash_abi_version": (c_int32, []),
+    "ash_last_error": (c_char_p, []),
+    "ash_scan_tiles": (c_int64, [c_int64]),
+    "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
+    "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_insert": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_claim": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_count": (c_int32, [_M, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_commit": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_rollback": (c_int32, [_M, c_int64, c_void_p, c_void_p]),
+    "ash_erase": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_active_indices": (c_int32, [_M, c_void_p, c_void_p]),
+    "ash_rehash_from": (c_int32, [_M, _M, c_void_p, c_int64, c_void_p]),
+    "ash_rebuild_table": (c_int32, [_M, c_void_p, c_int64, c_void_p]),
+    "ash_table_clear": (c_int32, [c_void_p, c_int64, c_void_p]),
+    "ash_quantize": (c_int32, [c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p, c_void_p]),
+    "ash_voxelize": (c_int32, [_M, c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA library must be built first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ash_abi_version() != 1:
+        raise ImportError("libash.so ABI version mismatch; rebuild")
+    return lib
+
+
+lib = _load()
+
+
+class AshError(RuntimeError):
+    pass
+
+
+def call(name: str, *args) -> None:
+    """Invoke an ABI entry point and map its status code to an exception."""
+    rc = getattr(lib, name)(*args)
+    if rc == ASH_OK:
+        return
+    msg = (lib.ash_last_error() or b"").decode(errors="replace")
+    if rc == ASH_ERR_INVALID:
+        raise ValueError(f"{name}: {msg}")
+    raise AshError(f"{name} failed ({rc}): {msg}")
+
+
+def scan_tiles(n: int) -> int:
+    return int(lib.ash_scan_tiles(int(n)))

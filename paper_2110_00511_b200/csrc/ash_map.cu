@@ -1,0 +1,1104 @@
+// ash_map.cu — sm_100a kernels for the batch spatial hash map + C ABI.
+//
+// Replaces the reference's numpy hot path (pkg/src/spatialhash):
+//   hashing.py:28-43 hash_keys + backends.py:107-133 ChainTable.walk  -> k_find / probe loops
+//   backends.py:59-96 first_occurrence_unique + hashmap.py:125-131    -> k_claim (atomicMin winner)
+//   index_heap.py:26-36 allocate + hashmap.py:397-413 commit          -> k_commit (single-pass scan)
+//   hashmap.py:431-456 erase + index_heap.py:38-47 sorted free        -> k_erase_* + k_free_compact
+//   hashmap.py:458-460 active_indices                                 -> k_active_compact
+//   hashmap.py:326-332 _rehash_into                                   -> k_rehash_build
+//   geometry.py:49-76 quantize / voxel_downsample                     -> k_quantize / k_voxel_*
+//
+// Table: open addressing over 16-byte slots {w0,w1,w2,state}, probed as
+// 32-byte buckets (two slots = one DRAM sector; one 256-bit load each).
+// Keys are int32 rows; arity <= 3 is compared inline, larger arities compare
+// the first three words inline and the rest against the key rows.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/ash.h"
+
+namespace {
+
+constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr uint32_t TOMB = 0xFFFFFFFEu;
+constexpr uint32_t PEND = 0x80000000u;
+// per-position scratch encoding after the claim pass (stored in out_idx):
+//   >= 0                       key already present, value = buffer index
+//   PEND | [CLAIMER] | slot    key absent; slot holds the batch's pending entry
+constexpr uint32_t CLAIMER = 0x40000000u;
+constexpr uint32_t SLOT_MASK = 0x3FFFFFFFu;
+constexpr uint8_t DEMOTED = 2;  // out_mask scratch: this position lost the slot
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kItems = 8;
+constexpr int kTile = kBlock * kItems;  // positions per scan tile
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return ASH_ERR_CUDA;
+  }
+  return ASH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// memory helpers
+
+__device__ __forceinline__ void ld256_nc(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ void ld256_relaxed(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p)
+               : "memory");
+}
+
+__device__ __forceinline__ bool cas128(uint4* addr, uint4 cmp, uint4 val) {
+  unsigned long long clo = ((unsigned long long)cmp.y << 32) | cmp.x;
+  unsigned long long chi = ((unsigned long long)cmp.w << 32) | cmp.z;
+  unsigned long long vlo = ((unsigned long long)val.y << 32) | val.x;
+  unsigned long long vhi = ((unsigned long long)val.w << 32) | val.z;
+  unsigned long long olo, ohi;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(olo), "=l"(ohi)
+      : "l"(clo), "l"(chi), "l"(vlo), "l"(vhi), "l"(addr)
+      : "memory");
+  return olo == clo && ohi == chi;
+}
+
+__device__ __forceinline__ uint4 ld128_relaxed(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int32_t ld_volatile_i32(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Bitwise row copy, widest aligned word first (hashmap.py:134-150 dispatches
+// 4/8/12/16-byte rows to word copies and the rest to bytes; here every row
+// takes the widest word its alignment allows).
+__device__ __forceinline__ void copy_row(uint8_t* dst, const uint8_t* src, int64_t rb) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) |
+                static_cast<uintptr_t>(rb);
+  if ((a & 15) == 0) {
+    for (int64_t i = 0; i < rb; i += 16)
+      *reinterpret_cast<uint4*>(dst + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+  } else if ((a & 7) == 0) {
+    for (int64_t i = 0; i < rb; i += 8)
+      *reinterpret_cast<uint2*>(dst + i) = __ldg(reinterpret_cast<const uint2*>(src + i));
+  } else if ((a & 3) == 0) {
+    for (int64_t i = 0; i < rb; i += 4)
+      *reinterpret_cast<uint32_t*>(dst + i) = __ldg(reinterpret_cast<const uint32_t*>(src + i));
+  } else {
+    for (int64_t i = 0; i < rb; ++i) dst[i] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// hashing: murmur3-style word mix; only bucket_count is observable in the
+// reference (tests/test_hashmap.py:26-28), so the table uses its own hash.
+
+__device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+
+__device__ __forceinline__ uint32_t mix_word(uint32_t h, uint32_t k) {
+  k *= 0xcc9e2d51u;
+  k = rotl32(k, 15);
+  k *= 0x1b873593u;
+  h ^= k;
+  h = rotl32(h, 13);
+  return h * 5u + 0xe6546b64u;
+}
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
+// A = arity when 1..3 (key fully inline), A = 0 for arity > 3.
+template <int A>
+struct Key {
+  uint32_t w[3];
+  const int32_t* row;  // full key row (A == 0 only)
+};
+
+template <int A>
+__device__ __forceinline__ Key<A> load_key(const int32_t* keys, int64_t p, int arity) {
+  Key<A> k;
+  const int32_t* r = keys + p * (A ? A : arity);
+  k.row = r;
+  k.w[0] = static_cast<uint32_t>(r[0]);
+  k.w[1] = (A == 0 || A >= 2) ? static_cast<uint32_t>(r[1]) : 0u;
+  k.w[2] = (A == 0 || A >= 3) ? static_cast<uint32_t>(r[2]) : 0u;
+  return k;
+}
+
+template <int A>
+__device__ __forceinline__ uint32_t hash_key(const Key<A>& k, int arity) {
+  uint32_t h = 0x9747b28cu;
+  if (A == 0) {
+    for (int d = 0; d < arity; ++d) h = mix_word(h, static_cast<uint32_t>(k.row[d]));
+    h ^= static_cast<uint32_t>(arity) * 4u;
+  } else {
+#pragma unroll
+    for (int d = 0; d < A; ++d) h = mix_word(h, k.w[d]);
+    h ^= static_cast<uint32_t>(A) * 4u;
+  }
+  return fmix32(h);
+}
+
+struct Table {
+  uint4* slots;
+  uint32_t bucket_mask;  // n_buckets - 1 (bucket = 2 slots)
+  uint32_t slot_mask;    // n_slots - 1
+  const int32_t* key_buf;
+  int arity;
+};
+
+Table make_table(const ash_map_t* m) {
+  Table t;
+  t.slots = static_cast<uint4*>(m->slots);
+  t.bucket_mask = static_cast<uint32_t>(m->n_slots / 2 - 1);
+  t.slot_mask = static_cast<uint32_t>(m->n_slots - 1);
+  t.key_buf = m->key_buf;
+  t.arity = m->arity;
+  return t;
+}
+
+// Does slot words w[0..2] (+ state st, which is committed or pending) hold key k?
+// Pending states carry a batch position whose row in `batch` equals the
+// pending key (any position of the group: all hold the same key).
+template <int A>
+__device__ __forceinline__ bool slot_matches(const uint32_t* w, uint32_t st, const Key<A>& k,
+                                             const Table& t, const int32_t* batch) {
+  if (w[0] != k.w[0]) return false;
+  if ((A == 0 || A >= 2) && w[1] != k.w[1]) return false;
+  if ((A == 0 || A >= 3) && w[2] != k.w[2]) return false;
+  if (A == 0) {
+    const int32_t* other = (st < PEND) ? t.key_buf + static_cast<int64_t>(st) * t.arity
+                                       : batch + static_cast<int64_t>(st & ~PEND) * t.arity;
+    for (int d = 3; d < t.arity; ++d)
+      if (other[d] != k.row[d]) return false;
+  }
+  return true;
+}
+
+template <int A>
+__device__ __forceinline__ uint4 slot_value(const Key<A>& k, uint32_t state) {
+  return make_uint4(k.w[0], k.w[1], k.w[2], state);
+}
+
+// Read-only probe (find / erase): returns the buffer index or -1; slot out.
+template <int A>
+__device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, uint32_t h,
+                                              uint32_t* slot_out) {
+  uint32_t b = h & t.bucket_mask;
+  for (uint32_t step = 0; step <= t.bucket_mask; ++step) {
+    uint32_t w[8];
+    ld256_nc(t.slots + 2 * static_cast<size_t>(b), w);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      uint32_t st = w[4 * s + 3];
+      if (st == EMPTY) return -1;
+      if (st < PEND && slot_matches<A>(w + 4 * s, st, k, t, nullptr)) {
+        if (slot_out) *slot_out = 2 * b + s;
+        return static_cast<int32_t>(st);
+      }
+    }
+    b = (b + 1) & t.bucket_mask;
+  }
+  return -1;
+}
+
+// Claim pass for one (group-leader) position j.  Returns the scratch
+// encoding; writes DEMOTED into mask[] for the position that lost the slot.
+template <int A>
+__device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k, uint32_t h,
+                                                uint32_t j, const int32_t* batch, uint8_t* mask,
+                                                int32_t* counters, bool* claimed_empty) {
+  const uint32_t me = PEND | j;
+  uint32_t b = h & t.bucket_mask;
+  int first = 0;
+  uint32_t free_slot = EMPTY;
+  uint4 free_val = make_uint4(0, 0, 0, 0);
+  uint32_t scanned = 0;
+  while (true) {
+    uint32_t w[8];
+    ld256_relaxed(t.slots + 2 * static_cast<size_t>(b), w);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s < first) continue;
+      const uint32_t slot = 2 * b + s;
+      const uint32_t st = w[4 * s + 3];
+      if (st >= TOMB) {  // EMPTY or TOMB: a free slot
+        if (free_slot == EMPTY) {
+          free_slot = slot;
+          free_val = make_uint4(w[4 * s], w[4 * s + 1], w[4 * s + 2], st);
+        }
+        if (st == EMPTY) goto claim;
+      } else if (slot_matches<A>(w + 4 * s, st, k, t, batch)) {
+        if (st < PEND) return st;  // already present
+        const uint32_t old = atomicMin(&t.slots[slot].w, me);
+        if (old < me) {
+          mask[j] = DEMOTED;  // a lower position holds the key
+        } else {
+          mask[old & ~PEND] = DEMOTED;  // we displaced a higher position
+        }
+        return PEND | slot;
+      }
+    }
+    first = 0;
+    b = (b + 1) & t.bucket_mask;
+    if (++scanned > t.bucket_mask) {
+      if (free_slot != EMPTY) goto claim;
+      atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_TABLE_FULL);
+      mask[j] = DEMOTED;
+      return PEND;
+    }
+    continue;
+  claim:
+    if (cas128(t.slots + free_slot, free_val, slot_value<A>(k, me))) {
+      *claimed_empty = (free_val.w == EMPTY);
+      return PEND | CLAIMER | free_slot;
+    }
+    // lost the race for free_slot: everything before it is unchanged, so
+    // rescan from there (it now holds some batch key, maybe ours)
+    b = free_slot >> 1;
+    first = free_slot & 1;
+    free_slot = EMPTY;
+    scanned = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernels: reset
+
+__global__ void k_reset(uint4* slots, int64_t n_slots, int32_t* heap, uint8_t* active,
+                        int32_t* claim, uint8_t* freed, int64_t capacity, int32_t* counters) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t s = i; s < n_slots; s += stride) slots[s] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+  for (int64_t c = i; c < capacity; c += stride) {
+    heap[c] = static_cast<int32_t>(c);
+    active[c] = 0;
+    claim[c] = INT32_MAX;
+    freed[c] = 0;
+  }
+  if (i < ASH_N_COUNTERS) counters[i] = 0;
+}
+
+__global__ void k_fill_empty(uint4* slots, int64_t n_slots) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t s = i; s < n_slots; s += stride) slots[s] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+}
+
+// ---------------------------------------------------------------------------
+// kernels: find
+
+template <int A>
+__global__ void __launch_bounds__(kBlock) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
+                                                 int32_t* __restrict__ out_idx,
+                                                 uint8_t* __restrict__ out_mask) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p >= n) return;
+  Key<A> k = load_key<A>(keys, p, t.arity);
+  int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), nullptr);
+  out_idx[p] = idx;
+  out_mask[p] = idx >= 0;
+}
+
+// ---------------------------------------------------------------------------
+// kernels: insert / activate claim pass
+
+template <int A>
+__device__ __forceinline__ bool same_key_in_warp(const Key<A>& k, unsigned live, unsigned* grp) {
+  unsigned g = __match_any_sync(live, k.w[0]);
+  if (A == 0 || A >= 2) g &= __match_any_sync(live, k.w[1]);
+  if (A == 0 || A >= 3) g &= __match_any_sync(live, k.w[2]);
+  *grp = g;
+  return true;
+}
+
+template <int A>
+__global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
+                                                  int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
+                                                  int32_t* counters) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if (p == 0) counters[ASH_CTR_WINNERS] = 0;
+  const bool valid = p < n;
+  const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
+  if (!valid) return;
+  Key<A> k = load_key<A>(keys, p, t.arity);
+  // warp pre-aggregation: equal keys in a warp resolve through their lowest
+  // lane (= lowest batch position); the rest are duplicate losers or share
+  // the leader's found index (hashmap.py:125-131 first-occurrence rule)
+  unsigned grp = 1u << lane;
+  if (A != 0) same_key_in_warp<A>(k, live, &grp);
+  const int leader = __ffs(grp) - 1;
+  uint32_t res = 0;
+  bool claimed_empty = false;
+  if (lane == leader)
+    res = probe_claim<A>(t, k, hash_key<A>(k, t.arity), static_cast<uint32_t>(p), keys, mask, counters,
+                         &claimed_empty);
+  __syncwarp(live);
+  const uint32_t lres = __shfl_sync(live, res, leader);
+  if (lane == leader) {
+    tmp[p] = static_cast<int32_t>(res);
+  } else if (lres < PEND) {
+    tmp[p] = static_cast<int32_t>(lres);
+  } else {
+    tmp[p] = static_cast<int32_t>(PEND);
+    mask[p] = DEMOTED;
+  }
+  const unsigned ce = __ballot_sync(live, claimed_empty);
+  if (ce && lane == __ffs(live) - 1) atomicAdd(&counters[ASH_CTR_USED], __popc(ce));
+}
+
+// ---------------------------------------------------------------------------
+// single-pass (decoupled look-back) tile scan over a 0/1 predicate
+
+constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
+
+__device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, uint32_t v) {
+  return (static_cast<uint64_t>(epoch) << 34) | (flag << 32) | v;
+}
+
+// Warp 0 only.  Returns the exclusive prefix of tile `tile`.
+__device__ uint32_t lookback(uint64_t* status, int64_t tile, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0;
+  int64_t pred = tile - 1;
+  while (true) {
+    const int64_t t = pred - lane;
+    uint64_t flag = kFlagIncl;
+    uint32_t val = 0;
+    while (true) {
+      bool ready = true;
+      if (t >= 0) {
+        uint64_t s = ld_relaxed_u64(status + t);
+        flag = (s >> 32) & 3;
+        val = static_cast<uint32_t>(s);
+        ready = (static_cast<uint32_t>(s >> 34) == epoch) && flag != 0;
+      }
+      if (__all_sync(0xFFFFFFFFu, ready)) break;
+      __nanosleep(20);
+    }
+    const unsigned incl = __ballot_sync(0xFFFFFFFFu, flag == kFlagIncl);
+    if (incl) {
+      const int first = __ffs(incl) - 1;
+      uint32_t c = lane <= first ? val : 0;
+      prefix += __reduce_add_sync(0xFFFFFFFFu, c);
+      break;
+    }
+    prefix += __reduce_add_sync(0xFFFFFFFFu, val);
+    pred -= 32;
+  }
+  __threadfence();
+  return prefix;
+}
+
+struct TileScan {
+  uint32_t prefix;  // exclusive prefix of this tile
+  uint32_t total;   // this tile's count
+  uint32_t base;    // value read by thread 0 before publishing (e.g. heap top)
+};
+
+// Block-wide: ballots per item, per-(item, warp) offsets in smem, tile
+// prefix through look-back.  `base_src` (may be null) is read by thread 0
+// before the tile publishes, so a later tile may overwrite it safely.
+struct ScanSmem {
+  uint32_t cnt[kItems * kWarps];
+  uint32_t pre[kItems * kWarps];
+  uint32_t prefix, total, base;
+};
+
+__device__ __forceinline__ TileScan tile_scan(const bool (&flag)[kItems], uint32_t (&bal)[kItems],
+                                              ScanSmem& sm, uint64_t* status, int64_t tile,
+                                              uint32_t epoch, const int32_t* base_src) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) sm.base = base_src ? static_cast<uint32_t>(ld_volatile_i32(base_src)) : 0u;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    bal[it] = __ballot_sync(0xFFFFFFFFu, flag[it]);
+    if (lane == 0) sm.cnt[it * kWarps + warp] = __popc(bal[it]);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    static_assert(kItems * kWarps == 64, "two entries per lane");
+    const uint32_t e0 = sm.cnt[2 * lane], e1 = sm.cnt[2 * lane + 1];
+    uint32_t incl = e0 + e1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - e0 - e1;
+    sm.pre[2 * lane] = excl;
+    sm.pre[2 * lane + 1] = excl + e0;
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_release_u64(status, pack_status(epoch, kFlagIncl, total));
+    } else {
+      if (lane == 0) st_release_u64(status + tile, pack_status(epoch, kFlagAgg, total));
+      prefix = lookback(status, tile, epoch);
+      if (lane == 0) st_release_u64(status + tile, pack_status(epoch, kFlagIncl, prefix + total));
+    }
+    if (lane == 0) {
+      sm.prefix = prefix;
+      sm.total = total;
+    }
+  }
+  __syncthreads();
+  return TileScan{sm.prefix, sm.total, sm.base};
+}
+
+__device__ __forceinline__ uint32_t item_rank(const ScanSmem& sm, const uint32_t (&bal)[kItems], int it) {
+  const int warp = threadIdx.x >> 5;
+  return sm.prefix + sm.pre[it * kWarps + warp] + __popc(bal[it] & lanemask_lt());
+}
+
+// ---------------------------------------------------------------------------
+// kernels: insert / activate commit (winner rank -> heap index -> rows)
+
+struct ValueArgs {
+  int n;
+  const uint8_t* src[ASH_MAX_VALUE_BUFFERS];
+  uint8_t* dst[ASH_MAX_VALUE_BUFFERS];
+  int64_t rb[ASH_MAX_VALUE_BUFFERS];
+};
+
+template <int A>
+__global__ void __launch_bounds__(kBlock)
+    k_commit(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
+             int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
+             uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
+             uint64_t* status, uint32_t epoch) {
+  __shared__ ScanSmem sm;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kTile;
+  int32_t v[kItems];
+  bool win[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    v[it] = 0;
+    win[it] = false;
+    if (p < n) {
+      v[it] = tmp[p];
+      win[it] = v[it] < 0 && !(mask[p] & DEMOTED);
+    }
+  }
+  uint32_t bal[kItems];
+  TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, counters + ASH_CTR_TOP);
+  const int arity = A ? A : t.arity;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p >= n) continue;
+    if (win[it]) {
+      const uint32_t rank = item_rank(sm, bal, it);
+      const int32_t idx = heap[ts.base + rank];
+      const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
+      t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+      const int32_t* kr = keys + p * arity;
+      int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
+      for (int d = 0; d < arity; ++d) dr[d] = kr[d];
+#pragma unroll
+      for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
+        if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
+      active[idx] = 1;
+      tmp[p] = idx;
+      mask[p] = 1;
+    } else if (v[it] >= 0) {
+      tmp[p] = assoc ? v[it] : -1;
+      mask[p] = assoc ? 1 : 0;
+    } else {
+      tmp[p] = -1;
+      mask[p] = 0;
+    }
+  }
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+    const uint32_t total = ts.prefix + ts.total;
+    counters[ASH_CTR_TOP] = static_cast<int32_t>(ts.base + total);
+    counters[ASH_CTR_WINNERS] = static_cast<int32_t>(total);
+  }
+}
+
+__global__ void k_count_winners(const int32_t* __restrict__ tmp, const uint8_t* __restrict__ mask, int64_t n,
+                                int32_t* counters) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  bool w = p < n && tmp[p] < 0 && !(mask[p] & DEMOTED);
+  unsigned b = __ballot_sync(0xFFFFFFFFu, w);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[ASH_CTR_WINNERS], __popc(b));
+}
+
+__global__ void k_rollback(uint4* slots, const int32_t* __restrict__ tmp, int64_t n) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t v = static_cast<uint32_t>(tmp[p]);
+  // a claimed slot reverts to TOMBSTONE: probe chains through it stay intact
+  if ((v & PEND) && (v & CLAIMER)) slots[v & SLOT_MASK].w = TOMB;
+}
+
+// ---------------------------------------------------------------------------
+// kernels: erase
+
+template <int A>
+__global__ void __launch_bounds__(kBlock) k_erase_probe(Table t, const int32_t* __restrict__ keys, int64_t n,
+                                                        int32_t* __restrict__ scratch, int32_t* claim,
+                                                        int32_t* counters) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p == 0) counters[ASH_CTR_ERASED] = 0;
+  if (p >= n) return;
+  Key<A> k = load_key<A>(keys, p, t.arity);
+  uint32_t slot = 0;
+  int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), &slot);
+  scratch[2 * p] = static_cast<int32_t>(slot);
+  scratch[2 * p + 1] = idx;
+  // first found occurrence wins (hashmap.py:448-449)
+  if (idx >= 0) atomicMin(&claim[idx], static_cast<int32_t>(p));
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_erase_commit(uint4* slots, int64_t n, const int32_t* __restrict__ scratch, int32_t* claim,
+                   uint8_t* active, uint8_t* freed, uint8_t* __restrict__ out_mask, int32_t* counters) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  bool hit = false;
+  if (p < n) {
+    const int32_t idx = scratch[2 * p + 1];
+    if (idx >= 0 && claim[idx] == static_cast<int32_t>(p)) {
+      hit = true;
+      claim[idx] = INT32_MAX;
+      slots[scratch[2 * p]].w = TOMB;
+      active[idx] = 0;  // rows are not cleared (hashmap.py:451-455)
+      freed[idx] = 1;
+    }
+    out_mask[p] = hit;
+  }
+  unsigned b = __ballot_sync(0xFFFFFFFFu, hit);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[ASH_CTR_ERASED], __popc(b));
+}
+
+// freed flags over [0, capacity) -> heap[top - E + rank], ascending
+// (index_heap.py:38-47: the freed indices are written sorted below top)
+__global__ void __launch_bounds__(kBlock) k_free_compact(uint8_t* freed, int64_t capacity, int32_t* heap,
+                                                         int32_t* counters, uint64_t* status,
+                                                         uint32_t epoch) {
+  __shared__ ScanSmem sm;
+  const int32_t erased = ld_volatile_i32(counters + ASH_CTR_ERASED);
+  if (erased == 0) return;
+  const int64_t tile = blockIdx.x, base = tile * kTile;
+  bool f[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t i = base + it * kBlock + threadIdx.x;
+    f[it] = i < capacity && freed[i];
+  }
+  uint32_t bal[kItems];
+  TileScan ts = tile_scan(f, bal, sm, status, tile, epoch, counters + ASH_CTR_TOP);
+  const uint32_t start = ts.base - static_cast<uint32_t>(erased);
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    if (!f[it]) continue;
+    const int64_t i = base + it * kBlock + threadIdx.x;
+    heap[start + item_rank(sm, bal, it)] = static_cast<int32_t>(i);
+    freed[i] = 0;
+  }
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) counters[ASH_CTR_TOP] = static_cast<int32_t>(start);
+}
+
+// ascending select of active flags (hashmap.py:458-460)
+__global__ void __launch_bounds__(kBlock) k_active_compact(const uint8_t* __restrict__ active, int64_t capacity,
+                                                           int32_t* __restrict__ out, int32_t* counters,
+                                                           uint64_t* status, uint32_t epoch) {
+  __shared__ ScanSmem sm;
+  const int64_t tile = blockIdx.x, base = tile * kTile;
+  bool f[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t i = base + it * kBlock + threadIdx.x;
+    f[it] = i < capacity && active[i];
+  }
+  uint32_t bal[kItems];
+  TileScan ts = tile_scan(f, bal, sm, status, tile, epoch, nullptr);
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    if (!f[it]) continue;
+    out[item_rank(sm, bal, it)] = static_cast<int32_t>(base + it * kBlock + threadIdx.x);
+  }
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) counters[ASH_CTR_COUNT] = static_cast<int32_t>(ts.prefix + ts.total);
+}
+
+// ---------------------------------------------------------------------------
+// kernels: rehash / table rebuild (unique keys: claim the first EMPTY slot)
+
+template <int A>
+__device__ __forceinline__ void insert_unique(const Table& t, const Key<A>& k, uint32_t h, uint32_t state) {
+  uint32_t s = (h & t.bucket_mask) * 2;
+  while (true) {
+    uint4 cur = ld128_relaxed(t.slots + s);
+    if (cur.w == EMPTY && cas128(t.slots + s, cur, slot_value<A>(k, state))) return;
+    if (cur.w == EMPTY) continue;  // lost the race on this slot: re-read it
+    s = (s + 1) & t.slot_mask;
+  }
+}
+
+template <int A>
+__global__ void __launch_bounds__(kBlock)
+    k_rehash_build(Table dst, const int32_t* __restrict__ src_keys, const int32_t* __restrict__ act,
+                   int64_t n_act, ValueArgs va, int32_t* __restrict__ dst_keys, uint8_t* dst_active,
+                   int32_t* dst_counters) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (i == 0) {
+    dst_counters[ASH_CTR_TOP] = static_cast<int32_t>(n_act);
+    dst_counters[ASH_CTR_USED] = static_cast<int32_t>(n_act);
+  }
+  if (i >= n_act) return;
+  const int64_t src = act[i];
+  const int arity = A ? A : dst.arity;
+  for (int d = 0; d < arity; ++d) dst_keys[i * arity + d] = src_keys[src * arity + d];
+#pragma unroll
+  for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
+    if (b < va.n) copy_row(va.dst[b] + i * va.rb[b], va.src[b] + src * va.rb[b], va.rb[b]);
+  dst_active[i] = 1;
+  Key<A> k = load_key<A>(src_keys, src, arity);
+  insert_unique<A>(dst, k, hash_key<A>(k, arity), static_cast<uint32_t>(i));
+}
+
+template <int A>
+__global__ void __launch_bounds__(kBlock)
+    k_rebuild_table(const uint4* __restrict__ old_slots, int64_t old_n, Table dst, int32_t* counters) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (s == 0) counters[ASH_CTR_USED] = ld_volatile_i32(counters + ASH_CTR_TOP);
+  if (s >= old_n) return;
+  const uint4 v = old_slots[s];
+  if (v.w >= PEND) return;
+  Key<A> k;
+  k.w[0] = v.x;
+  k.w[1] = v.y;
+  k.w[2] = v.z;
+  k.row = dst.key_buf + static_cast<int64_t>(v.w) * dst.arity;
+  insert_unique<A>(dst, k, hash_key<A>(k, dst.arity), v.w);
+}
+
+// ---------------------------------------------------------------------------
+// kernels: quantize / voxelize (geometry.py:49-76)
+
+template <typename T>
+__device__ __forceinline__ int32_t quantize_one(T x, double cell, bool* bad) {
+  // float64 true division then floor, exactly as numpy (geometry.py:53)
+  const double q = floor(__ddiv_rn(static_cast<double>(x), cell));
+  if (q < -2147483648.0 || q >= 2147483648.0) *bad = true;
+  if (q != q) return INT32_MIN;  // numpy's NaN -> int32 conversion result on x86
+  if (*bad) return 0;
+  return static_cast<int32_t>(q);
+}
+
+template <typename T>
+__global__ void k_quantize(const T* __restrict__ pts, int64_t n, double cell, int32_t* __restrict__ out,
+                           int32_t* flags) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p >= n) return;
+  bool bad = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[3 * p + d] = quantize_one<T>(pts[3 * p + d], cell, &bad);
+  if (bad) atomicOr(flags, ASH_FLAG_RANGE);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __restrict__ pts, int64_t n,
+                                                        double cell, int32_t* __restrict__ tmp,
+                                                        uint8_t* __restrict__ mask, int32_t* counters) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = p < n;
+  const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
+  if (!valid) return;
+  bool bad = false;
+  Key<3> k;
+  k.row = nullptr;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(pts[3 * p + d], cell, &bad));
+  if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
+  unsigned grp;
+  same_key_in_warp<3>(k, live, &grp);
+  // out-of-range points never claim; the host raises before using results
+  const unsigned bad_lanes = __ballot_sync(live, bad);
+  grp &= ~bad_lanes;
+  if (bad) grp = 1u << lane;
+  const int leader = __ffs(grp) - 1;
+  uint32_t res = PEND;
+  bool claimed_empty = false;
+  if (lane == leader && !bad)
+    res = probe_claim<3>(t, k, hash_key<3>(k, 3), static_cast<uint32_t>(p), nullptr, mask, counters,
+                         &claimed_empty);
+  __syncwarp(live);
+  if (lane == leader && !bad) {
+    tmp[p] = static_cast<int32_t>(res);
+  } else {
+    tmp[p] = static_cast<int32_t>(PEND);
+    mask[p] = DEMOTED;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    k_voxel_select(uint4* slots, const T* __restrict__ pts, int64_t n, double cell,
+                   const int32_t* __restrict__ tmp, const uint8_t* __restrict__ mask,
+                   int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel, int32_t* counters,
+                   uint64_t* status, uint32_t epoch) {
+  __shared__ ScanSmem sm;
+  const int64_t tile = blockIdx.x, base = tile * kTile;
+  int32_t v[kItems];
+  bool win[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    v[it] = 0;
+    win[it] = false;
+    if (p < n) {
+      v[it] = tmp[p];
+      win[it] = v[it] < 0 && !(mask[p] & DEMOTED);
+    }
+  }
+  uint32_t bal[kItems];
+  TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, nullptr);
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    if (!win[it]) continue;
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    const uint32_t r = item_rank(sm, bal, it);
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) out_coords[3 * static_cast<int64_t>(r) + d] = quantize_one<T>(pts[3 * p + d], cell, &bad);
+    out_sel[r] = p;
+    // leave the workspace table EMPTY for the next call
+    slots[static_cast<uint32_t>(v[it]) & SLOT_MASK] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+  }
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) counters[ASH_CTR_COUNT] = static_cast<int32_t>(ts.prefix + ts.total);
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned grid_for(int64_t n, int per_block) {
+  int64_t g = (n + per_block - 1) / per_block;
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+inline int64_t tiles_for(int64_t n) { return (n + kTile - 1) / kTile; }
+
+int check_map(const ash_map_t* m) {
+  if (!m) return fail(ASH_ERR_INVALID, "null map");
+  if (!m->slots || !m->key_buf || !m->heap || !m->active || !m->counters || !m->erase_claim || !m->freed)
+    return fail(ASH_ERR_INVALID, "map has a null buffer");
+  if (m->n_slots < 64 || (m->n_slots & (m->n_slots - 1)) || m->n_slots > (int64_t(1) << 30))
+    return fail(ASH_ERR_INVALID, "n_slots must be a power of two in [64, 2^30]");
+  if (m->arity < 1) return fail(ASH_ERR_INVALID, "arity must be >= 1");
+  if (m->capacity < 1 || m->capacity > INT32_MAX) return fail(ASH_ERR_INVALID, "capacity out of range");
+  if (m->n_values < 0 || m->n_values > ASH_MAX_VALUE_BUFFERS) return fail(ASH_ERR_INVALID, "too many value buffers");
+  return ASH_OK;
+}
+
+int check_batch(int64_t n) {
+  if (n < 0) return fail(ASH_ERR_INVALID, "negative batch length");
+  if (n >= int64_t(SLOT_MASK)) return fail(ASH_ERR_INVALID, "batch too long (>= 2^30 - 1)");
+  return ASH_OK;
+}
+
+int check_scan(const ash_map_t* m, int64_t n) {
+  if (!m->scan_status || m->scan_status_len < tiles_for(n))
+    return fail(ASH_ERR_INVALID, "scan workspace too small");
+  return ASH_OK;
+}
+
+inline uint32_t next_epoch(ash_map_t* m) {
+  m->epoch = (m->epoch + 1) & 0x3FFFFFFFu;
+  if (m->epoch == 0) m->epoch = 1;
+  return m->epoch;
+}
+
+ValueArgs value_args(const ash_map_t* m, const void* const* values) {
+  ValueArgs va;
+  memset(&va, 0, sizeof(va));
+  if (!values) return va;
+  va.n = m->n_values;
+  for (int b = 0; b < m->n_values; ++b) {
+    va.src[b] = static_cast<const uint8_t*>(values[b]);
+    va.dst[b] = static_cast<uint8_t*>(m->value_bufs[b]);
+    va.rb[b] = m->value_row_bytes[b];
+  }
+  return va;
+}
+
+int arity_class(int arity) { return arity <= 3 ? arity : 0; }
+
+#define ASH_DISPATCH_ARITY(arity, KERNEL_CALL) \
+  switch (arity_class(arity)) {                \
+    case 1: { constexpr int A = 1; KERNEL_CALL; break; } \
+    case 2: { constexpr int A = 2; KERNEL_CALL; break; } \
+    case 3: { constexpr int A = 3; KERNEL_CALL; break; } \
+    default: { constexpr int A = 0; KERNEL_CALL; break; } \
+  }
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+int ash_abi_version(void) { return ASH_ABI_VERSION; }
+
+const char* ash_last_error(void) { return g_err; }
+
+int64_t ash_scan_tiles(int64_t n) { return tiles_for(n < 1 ? 1 : n); }
+
+int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  cudaStream_t s = as_stream(stream);
+  int64_t work = m->n_slots > m->capacity ? m->n_slots : m->capacity;
+  unsigned g = grid_for(work, kBlock);
+  if (g > 148 * 16) g = 148 * 16;
+  k_reset<<<g, kBlock, 0, s>>>(static_cast<uint4*>(m->slots), m->n_slots, m->heap, m->active,
+                               m->erase_claim, m->freed, m->capacity, m->counters);
+  if (zero_rows) {
+    cudaMemsetAsync(m->key_buf, 0, sizeof(int32_t) * m->capacity * m->arity, s);
+    for (int b = 0; b < m->n_values; ++b)
+      if (m->value_row_bytes[b]) cudaMemsetAsync(m->value_bufs[b], 0, m->capacity * m->value_row_bytes[b], s);
+  }
+  return check_launch("ash_map_reset");
+}
+
+int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  if (!keys || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
+  Table t = make_table(m);
+  cudaStream_t s = as_stream(stream);
+  ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask)));
+  return check_launch("ash_find");
+}
+
+int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
+                     void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  if (!keys || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
+  Table t = make_table(m);
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(out_mask, 0, n, s);
+  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
+                                                                                 m->counters)));
+  return check_launch("ash_insert_claim");
+}
+
+int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint8_t* out_mask, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(m->counters + ASH_CTR_WINNERS, 0, sizeof(int32_t), s);
+  if (n > 0) k_count_winners<<<grid_for(n, kBlock), kBlock, 0, s>>>(out_idx, out_mask, n, m->counters);
+  return check_launch("ash_insert_count");
+}
+
+int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
+                      int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  if (int rc = check_scan(m, n)) return rc;
+  Table t = make_table(m);
+  ValueArgs va = value_args(m, values);
+  uint32_t ep = next_epoch(m);
+  cudaStream_t s = as_stream(stream);
+  ASH_DISPATCH_ARITY(m->arity, (k_commit<A><<<grid_for(n, kTile), kBlock, 0, s>>>(
+                                   t, keys, n, va, association, out_idx, out_mask, m->heap, m->active,
+                                   m->key_buf, m->counters, m->scan_status, ep)));
+  return check_launch("ash_insert_commit");
+}
+
+int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values, int32_t association,
+               int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (int rc = ash_insert_claim(m, keys, n, out_idx, out_mask, stream)) return rc;
+  return ash_insert_commit(m, keys, n, values, association, out_idx, out_mask, stream);
+}
+
+int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n);
+  return check_launch("ash_insert_rollback");
+}
+
+int ash_erase(ash_map_t* m, const int32_t* keys, int64_t n, uint8_t* out_mask, int32_t* scratch, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  if (!keys || !out_mask || !scratch) return fail(ASH_ERR_INVALID, "null batch pointer");
+  if (int rc = check_scan(m, m->capacity)) return rc;
+  Table t = make_table(m);
+  cudaStream_t s = as_stream(stream);
+  ASH_DISPATCH_ARITY(m->arity, (k_erase_probe<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(
+                                   t, keys, n, scratch, m->erase_claim, m->counters)));
+  k_erase_commit<<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<uint4*>(m->slots), n, scratch, m->erase_claim,
+                                                         m->active, m->freed, out_mask, m->counters);
+  uint32_t ep = next_epoch(m);
+  k_free_compact<<<grid_for(m->capacity, kTile), kBlock, 0, s>>>(m->freed, m->capacity, m->heap, m->counters,
+                                                                  m->scan_status, ep);
+  return check_launch("ash_erase");
+}
+
+int ash_active_indices(ash_map_t* m, int32_t* out, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_scan(m, m->capacity)) return rc;
+  uint32_t ep = next_epoch(m);
+  k_active_compact<<<grid_for(m->capacity, kTile), kBlock, 0, as_stream(stream)>>>(
+      m->active, m->capacity, out, m->counters, m->scan_status, ep);
+  return check_launch("ash_active_indices");
+}
+
+int ash_rehash_from(ash_map_t* dst, const ash_map_t* src, const int32_t* act, int64_t n_act, void* stream) {
+  if (int rc = check_map(dst)) return rc;
+  if (int rc = check_map(src)) return rc;
+  if (dst->arity != src->arity || dst->n_values != src->n_values)
+    return fail(ASH_ERR_INVALID, "rehash between maps of different layout");
+  if (n_act < 0 || n_act > dst->capacity) return fail(ASH_ERR_INVALID, "rehash source larger than destination");
+  ValueArgs va;
+  memset(&va, 0, sizeof(va));
+  va.n = src->n_values;
+  for (int b = 0; b < va.n; ++b) {
+    if (dst->value_row_bytes[b] != src->value_row_bytes[b]) return fail(ASH_ERR_INVALID, "value row size mismatch");
+    va.src[b] = static_cast<const uint8_t*>(src->value_bufs[b]);
+    va.dst[b] = static_cast<uint8_t*>(dst->value_bufs[b]);
+    va.rb[b] = src->value_row_bytes[b];
+  }
+  Table t = make_table(dst);
+  cudaStream_t s = as_stream(stream);
+  ASH_DISPATCH_ARITY(dst->arity, (k_rehash_build<A><<<grid_for(n_act, kBlock), kBlock, 0, s>>>(
+                                     t, src->key_buf, act, n_act, va, dst->key_buf, dst->active, dst->counters)));
+  return check_launch("ash_rehash_from");
+}
+
+int ash_rebuild_table(ash_map_t* m, void* new_slots, int64_t new_n_slots, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (!new_slots || new_n_slots < 64 || (new_n_slots & (new_n_slots - 1)) || new_n_slots > (int64_t(1) << 30))
+    return fail(ASH_ERR_INVALID, "bad new table");
+  cudaStream_t s = as_stream(stream);
+  unsigned g = grid_for(new_n_slots, kBlock);
+  if (g > 148 * 16) g = 148 * 16;
+  k_fill_empty<<<g, kBlock, 0, s>>>(static_cast<uint4*>(new_slots), new_n_slots);
+  ash_map_t nm = *m;
+  nm.slots = new_slots;
+  nm.n_slots = new_n_slots;
+  Table t = make_table(&nm);
+  ASH_DISPATCH_ARITY(m->arity, (k_rebuild_table<A><<<grid_for(m->n_slots, kBlock), kBlock, 0, s>>>(
+                                   static_cast<const uint4*>(m->slots), m->n_slots, t, m->counters)));
+  return check_launch("ash_rebuild_table");
+}
+
+int ash_table_clear(void* slots, int64_t n_slots, void* stream) {
+  if (!slots || n_slots < 0) return fail(ASH_ERR_INVALID, "bad table");
+  if (n_slots == 0) return ASH_OK;
+  unsigned g = grid_for(n_slots, kBlock);
+  if (g > 148 * 16) g = 148 * 16;
+  k_fill_empty<<<g, kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(slots), n_slots);
+  return check_launch("ash_table_clear");
+}
+
+int ash_quantize(const void* points, int32_t points_are_f64, int64_t n, double cell, int32_t* out_coords,
+                 int32_t* flags, void* stream) {
+  if (n < 0) return fail(ASH_ERR_INVALID, "negative point count");
+  if (!(cell > 0)) return fail(ASH_ERR_INVALID, "cell size must be > 0");
+  if (n == 0) return ASH_OK;
+  cudaStream_t s = as_stream(stream);
+  if (points_are_f64)
+    k_quantize<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const double*>(points), n, cell, out_coords, flags);
+  else
+    k_quantize<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const float*>(points), n, cell, out_coords, flags);
+  return check_launch("ash_quantize");
+}
+
+int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int64_t n, double voxel,
+                 int32_t* out_coords, int64_t* out_sel, int32_t* scratch_idx, uint8_t* scratch_mask, void* stream) {
+  if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
+  if (int rc = check_batch(n)) return rc;
+  if (!(voxel > 0)) return fail(ASH_ERR_INVALID, "voxel size must be > 0");
+  if (ws->n_slots < 2 * n || (ws->n_slots & (ws->n_slots - 1))) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (int rc = check_scan(ws, n)) return rc;
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
+  if (n == 0) return check_launch("ash_voxelize");
+  cudaMemsetAsync(scratch_mask, 0, n, s);
+  Table t = make_table(ws);
+  uint32_t ep = next_epoch(ws);
+  if (points_are_f64) {
+    const double* p = static_cast<const double*>(points);
+    k_voxel_claim<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask, ws->counters);
+    k_voxel_select<double><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
+                                                                 out_coords, out_sel, ws->counters, ws->scan_status, ep);
+  } else {
+    const float* p = static_cast<const float*>(points);
+    k_voxel_claim<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask, ws->counters);
+    k_voxel_select<float><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
+                                                                out_coords, out_sel, ws->counters, ws->scan_status, ep);
+  }
+  return check_launch("ash_voxelize");
+}
+
+}  // extern "C"

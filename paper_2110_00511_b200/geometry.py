@@ -1,0 +1,172 @@
+"""Batch geometry on the device map: quantize and voxel_downsample.
+
+Mirrors /root/reference/pkg/src/spatialhash/geometry.py:49-76.  Quantization
+is float64 true division then floor (geometry.py:53), so float32 clouds are
+widened exactly on the device and match the reference bit-for-bit.
+voxel_downsample is one fused pass: quantize + set insert with the
+first-occurrence winner + ascending select (libash ``ash_voxelize``).
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import AshMap, call
+from .hashmap import BatchResult, HashMap, HashSet, _stream_handle, _table_slots
+
+__all__ = ["quantize", "voxel_downsample", "lattice_offsets", "radius_neighbors",
+           "set_intersection"]
+
+
+def _points_tensor(points, device) -> torch.Tensor:
+    """(n, 3) float32/float64 on the device; other dtypes widen to float64
+    (PointCloud stores float64, geometry.py:25)."""
+    pos = getattr(points, "positions", points)
+    if isinstance(pos, torch.Tensor):
+        t = pos if pos.dtype in (torch.float32, torch.float64) else pos.to(torch.float64)
+    else:
+        a = np.asarray(pos)
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    t = t.reshape(-1, 3)
+    return t.to(device, non_blocking=True).contiguous()
+
+
+def _device(device) -> torch.device:
+    return torch.device(device) if device is not None else \
+        torch.device("cuda", torch.cuda.current_device())
+
+
+def quantize(positions, cell: float, device=None) -> torch.Tensor:
+    """floor(p / cell) as int32 voxel coordinates (geometry.py:49-56)."""
+    if cell <= 0:
+        raise ValueError("cell size must be > 0")
+    dev = _device(device)
+    pts = _points_tensor(positions, dev)
+    n = pts.shape[0]
+    out = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    if n == 0:
+        return out
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    call("ash_quantize", pts.data_ptr(), int(pts.dtype == torch.float64), n, float(cell),
+         out.data_ptr(), flags.data_ptr(), _stream_handle(dev))
+    if int(flags.item()) & _lib.FLAG_RANGE:
+        raise ValueError("quantized coordinates exceed int32 range")
+    return out
+
+
+class _VoxelWorkspace:
+    """Per-device all-EMPTY table reused across voxelize calls; the select
+    kernel restores every slot it claimed, so no per-call clear is needed."""
+
+    _lock = threading.Lock()
+    _by_device: dict = {}
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.slots = torch.empty(0, dtype=torch.int32, device=device)
+        self.n_slots = 0
+        self.counters = torch.zeros(_lib.N_COUNTERS, dtype=torch.int32, device=device)
+        self.scan = torch.zeros(0, dtype=torch.int64, device=device)
+        self.struct = AshMap()
+        self.struct.arity = 3
+        self.struct.counters = self.counters.data_ptr()
+
+    @classmethod
+    def get(cls, device: torch.device) -> "_VoxelWorkspace":
+        with cls._lock:
+            ws = cls._by_device.get(device)
+            if ws is None:
+                ws = cls._by_device[device] = cls(device)
+            return ws
+
+    def reserve(self, n: int) -> None:
+        need = _table_slots(max(n, 1))
+        if need > self.n_slots:
+            self.slots = torch.empty(need * 4, dtype=torch.int32, device=self.device)
+            self.n_slots = need
+            call("ash_table_clear", self.slots.data_ptr(), need, _stream_handle(self.device))
+            self.struct.slots = self.slots.data_ptr()
+            self.struct.n_slots = need
+        tiles = _lib.scan_tiles(max(n, 1))
+        if self.scan.numel() < tiles:
+            self.scan = torch.zeros(tiles, dtype=torch.int64, device=self.device)
+            self.struct.scan_status = self.scan.data_ptr()
+            self.struct.scan_status_len = tiles
+
+
+def voxel_downsample(points, voxel_size: float, backend: str = "generic", threads: int = 1,
+                     device=None):
+    """One representative point per occupied voxel (geometry.py:59-76).
+
+    Returns ``(voxel_coords int32 (k,3), selected int64 (k,))`` in
+    first-occurrence (ascending point index) order, exactly the reference's
+    ``coords[flatnonzero(HashSet.insert(coords).masks)]`` and index list.
+    """
+    if backend not in ("generic", "delegate", "integer_delegate"):
+        raise ValueError(f"unknown backend {backend!r}")
+    if voxel_size <= 0:
+        raise ValueError("cell size must be > 0")
+    dev = _device(device)
+    pts = _points_tensor(points, dev)
+    n = pts.shape[0]
+    if n == 0:
+        return (torch.zeros((0, 3), dtype=torch.int32, device=dev),
+                torch.zeros(0, dtype=torch.int64, device=dev))
+    ws = _VoxelWorkspace.get(dev)
+    with _VoxelWorkspace._lock:
+        ws.reserve(n)
+        coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
+        sel = torch.empty(n, dtype=torch.int64, device=dev)
+        scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
+        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        call("ash_voxelize", _lib.ctypes.byref(ws.struct), pts.data_ptr(),
+             int(pts.dtype == torch.float64), n, float(voxel_size), coords.data_ptr(),
+             sel.data_ptr(), scratch_idx.data_ptr(), scratch_mask.data_ptr(),
+             _stream_handle(dev))
+        count, flags = ws.counters[[_lib.CTR_COUNT, _lib.CTR_FLAGS]].tolist()
+    if flags & _lib.FLAG_RANGE:
+        raise ValueError("quantized coordinates exceed int32 range")
+    return coords[:count], sel[:count]
+
+
+def lattice_offsets(r: int) -> torch.Tensor:
+    """(2r+1)^3 offsets in [-r, r]^3, lexicographic (geometry.py:79-84)."""
+    if r < 0:
+        raise ValueError("radius must be >= 0")
+    ax = torch.arange(-r, r + 1, dtype=torch.int32)
+    g = torch.stack(torch.meshgrid(ax, ax, ax, indexing="ij"), dim=-1)
+    return g.reshape(-1, 3)
+
+
+def radius_neighbors(hashmap: HashMap, coords, r: int = 1) -> BatchResult:
+    """find() of every lattice offset around each coordinate
+    (geometry.py:87-99); results shaped (n, (2r+1)^3)."""
+    c = hashmap._check_keys(coords)
+    offs = lattice_offsets(r).to(c.device)
+    n, k = c.shape[0], offs.shape[0]
+    q = (c[:, None, :] + offs[None, :, :]).reshape(n * k, 3)
+    res = hashmap.find(q)
+    return BatchResult(res.indices.reshape(n, k), res.masks.reshape(n, k))
+
+
+def set_intersection(keys_a, keys_b, backend: str = "generic", threads: int = 1,
+                     device=None) -> torch.Tensor:
+    """Rows of keys_b present in keys_a, duplicates kept (geometry.py:129-143)."""
+    dev = _device(device)
+    a = torch.as_tensor(np.atleast_2d(np.asarray(keys_a, dtype=np.int32))) \
+        if not isinstance(keys_a, torch.Tensor) else keys_a.to(torch.int32)
+    b = torch.as_tensor(np.atleast_2d(np.asarray(keys_b, dtype=np.int32))) \
+        if not isinstance(keys_b, torch.Tensor) else keys_b.to(torch.int32)
+    a, b = a.to(dev), b.to(dev)
+    if a.shape[0] == 0 or b.shape[0] == 0:
+        return b[:0]
+    if a.shape[1] != b.shape[1]:
+        raise ValueError("key arity mismatch between the two sets")
+    probe = HashSet(a.shape[0], a.shape[1], backend=backend, device=dev)
+    probe.insert(a)
+    return b[probe.find(b).masks]

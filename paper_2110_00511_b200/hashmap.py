@@ -1,0 +1,602 @@
+"""Index-first spatial hash map on B200 — host side of the drop-in.
+
+Mirrors the reference ``spatialhash.HashMap`` / ``HashSet`` API
+(/root/reference/pkg/src/spatialhash/hashmap.py:33-515): same constructor,
+same batch operations, same error types and messages, same generic-backend
+index semantics.  Storage is CUDA memory owned by torch tensors; every batch
+operation is a hand-written sm_100a kernel sequence behind the C ABI in
+``include/ash.h`` (libash.so).  There is no CPU path.
+
+Host policy kept from the reference:
+  * validation (hashmap.py:246-286) and the reader/writer guard (:91-122);
+  * growth by doubling and the re-plan after a rehash (:311-332, :389-396);
+  * CapacityError leaves the map unchanged (:317-324).
+
+Differences in mechanism (not in results):
+  * ``size`` is tracked lazily: a mutating batch does not synchronise with the
+    device unless the host cannot prove the batch fits (capacity - an upper
+    bound on size >= batch length).  Reading ``size`` synchronises.
+  * Results are CUDA tensors (indices int32, masks bool).
+  * ``threads`` is accepted and ignored (the device is the parallelism).
+"""
+from __future__ import annotations
+
+import threading
+from contextlib import contextmanager
+from dataclasses import dataclass
+from typing import Iterator, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import AshMap, call
+
+__all__ = ["HashMap", "HashSet", "ValueSpec", "BatchResult", "CapacityError",
+           "ConcurrentAccessError"]
+
+
+class CapacityError(RuntimeError):
+    """Batch does not fit and automatic rehashing is disabled (hashmap.py:33)."""
+
+
+class ConcurrentAccessError(RuntimeError):
+    """A mutating batch overlapped another operation (hashmap.py:37)."""
+
+
+def _np_dtype(dt) -> np.dtype:
+    if isinstance(dt, torch.dtype):
+        return torch.empty(0, dtype=dt).numpy().dtype
+    return np.dtype(dt)
+
+
+def _torch_dtype(dt: np.dtype) -> torch.dtype:
+    return torch.from_numpy(np.empty(0, dtype=dt)).dtype
+
+
+@dataclass(frozen=True)
+class ValueSpec:
+    """Shape and dtype of one value buffer entry (hashmap.py:41-70)."""
+
+    shape: tuple
+    dtype: np.dtype
+
+    @classmethod
+    def coerce(cls, spec) -> "ValueSpec":
+        if isinstance(spec, ValueSpec):
+            return spec
+        if isinstance(spec, tuple) and len(spec) == 2 and isinstance(spec[0], (tuple, list)):
+            return cls(tuple(int(s) for s in spec[0]), spec[1])
+        return cls((1,), spec)
+
+    def __post_init__(self):
+        object.__setattr__(self, "shape", tuple(int(s) for s in self.shape))
+        object.__setattr__(self, "dtype", _np_dtype(self.dtype))
+        if any(s < 0 for s in self.shape):
+            raise ValueError("value shape dimensions must be >= 0")
+
+    @property
+    def count(self) -> int:
+        return int(np.prod(self.shape, dtype=np.int64)) if self.shape else 1
+
+    @property
+    def nbytes(self) -> int:
+        return self.count * self.dtype.itemsize
+
+
+@dataclass
+class BatchResult:
+    """Buffer indices (int32) and masks (bool), parallel to the batch
+    (hashmap.py:73-88).  Where ``masks`` is False the index is -1."""
+
+    indices: torch.Tensor
+    masks: torch.Tensor
+
+    def __iter__(self) -> Iterator[torch.Tensor]:
+        return iter((self.indices, self.masks))
+
+    def __len__(self) -> int:
+        return len(self.indices)
+
+
+class _AccessGuard:
+    """N readers or one writer; violations raise (hashmap.py:91-122)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._readers = 0
+        self._writing = False
+
+    @contextmanager
+    def reading(self):
+        with self._lock:
+            if self._writing:
+                raise ConcurrentAccessError("read overlapped a mutating batch")
+            self._readers += 1
+        try:
+            yield
+        finally:
+            with self._lock:
+                self._readers -= 1
+
+    @contextmanager
+    def writing(self):
+        with self._lock:
+            if self._writing or self._readers:
+                raise ConcurrentAccessError("mutating batch requires exclusive map access")
+            self._writing = True
+        try:
+            yield
+        finally:
+            with self._lock:
+                self._writing = False
+
+
+class ReadOnlyBuffer(torch.Tensor):
+    """Tensor view whose item assignment and in-place ops raise ValueError,
+    like the reference's non-writeable ``key_buffer`` (hashmap.py:227-233)."""
+
+    def __setitem__(self, key, value):
+        raise ValueError("assignment destination is read-only")
+
+    @classmethod
+    def __torch_function__(cls, func, types, args=(), kwargs=None):
+        name = getattr(func, "__name__", "")
+        inplace = (name.endswith("_") and not name.endswith("__")) or (
+            name.startswith("__i") and name.endswith("__")
+            and name not in ("__index__", "__int__", "__init__", "__iter__"))
+        if inplace and args and isinstance(args[0], cls):
+            raise ValueError("assignment destination is read-only")
+        with torch._C.DisableTorchFunctionSubclass():
+            return func(*args, **(kwargs or {}))
+
+
+class _HeapView:
+    """Read access matching ``IndexHeap`` (index_heap.py:14-55) for tests
+    that inspect ``m._heap``."""
+
+    def __init__(self, owner: "HashMap"):
+        self._m = owner
+
+    @property
+    def capacity(self) -> int:
+        return self._m.capacity
+
+    @property
+    def top(self) -> int:
+        return self._m.size
+
+    @property
+    def free_count(self) -> int:
+        return self._m.capacity - self._m.size
+
+    @property
+    def heap(self) -> torch.Tensor:
+        return self._m._heap_buf
+
+    def free_set(self) -> torch.Tensor:
+        return self._m._heap_buf[self.top:].clone()
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _table_slots(capacity: int) -> int:
+    """Power-of-two slot count with live load factor <= 0.5."""
+    n = 64
+    while n < 2 * capacity:
+        n *= 2
+    if n > 1 << 30:
+        raise ValueError(f"capacity {capacity} exceeds the single-map limit (2^29)")
+    return n
+
+
+_SLOT_LIMIT = 0.75  # rebuild the table when non-EMPTY slots would pass this
+
+
+class HashMap:
+    """Batch-parallel map from fixed-arity int32 keys to value buffers, on a
+    CUDA device.  Signature of hashmap.py:178-196 plus ``device``."""
+
+    def __init__(self, capacity: int, key_arity: int, value_specs: Sequence = (),
+                 backend: str = "generic", threads: int = 1, auto_rehash: bool = True,
+                 device=None):
+        if capacity < 1:
+            raise ValueError("capacity must be >= 1")
+        if key_arity < 1:
+            raise ValueError("key arity must be >= 1")
+        if backend not in ("generic", "delegate", "integer_delegate"):
+            raise ValueError(f"unknown backend {backend!r}")
+        self.key_arity = int(key_arity)
+        self.value_specs = tuple(ValueSpec.coerce(s) for s in value_specs)
+        if len(self.value_specs) > _lib.MAX_VALUE_BUFFERS:
+            raise ValueError(f"at most {_lib.MAX_VALUE_BUFFERS} value buffers are supported")
+        self.backend_name = "delegate" if backend in ("delegate", "integer_delegate") else "generic"
+        self.threads = max(1, int(threads))
+        self.auto_rehash = bool(auto_rehash)
+        self._device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        if self._device.type != "cuda":
+            raise ValueError("HashMap storage must be a CUDA device")
+        self._torch_dtypes = tuple(_torch_dtype(s.dtype) for s in self.value_specs)
+        self._guard = _AccessGuard()
+        self._debug_checksum = False
+        self._heap = _HeapView(self)
+        self._init_state(int(capacity))
+
+    # -- state ---------------------------------------------------------
+
+    def _init_state(self, capacity: int, zero_rows: bool = True) -> None:
+        """hashmap.py:200-210: fresh table, heap = arange, zeroed buffers."""
+        dev = self._device
+        self._capacity = capacity
+        self._n_slots = _table_slots(capacity)
+        self._slots = torch.empty(self._n_slots * 4, dtype=torch.int32, device=dev)
+        self._key_buf = torch.empty((capacity, self.key_arity), dtype=torch.int32, device=dev)
+        self._value_bufs = tuple(torch.empty((capacity, *s.shape), dtype=td, device=dev)
+                                 for s, td in zip(self.value_specs, self._torch_dtypes))
+        self._heap_buf = torch.empty(capacity, dtype=torch.int32, device=dev)
+        self._active = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        self._erase_claim = torch.empty(capacity, dtype=torch.int32, device=dev)
+        self._freed = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        self._counters = torch.zeros(_lib.N_COUNTERS, dtype=torch.int32, device=dev)
+        self._scan = torch.zeros(0, dtype=torch.int64, device=dev)
+        self._struct = AshMap()
+        self._fill_struct()
+        self._ensure_scan(capacity)
+        call("ash_map_reset", self._ptr(), 1 if zero_rows else 0, self._stream())
+        self._size = 0
+        self._size_known = True
+        self._top_ub = 0
+        self._used_ub = 0
+
+    def _fill_struct(self) -> None:
+        s = self._struct
+        s.slots = self._slots.data_ptr()
+        s.n_slots = self._n_slots
+        s.key_buf = self._key_buf.data_ptr()
+        s.arity = self.key_arity
+        s.n_values = len(self._value_bufs)
+        for i, (buf, spec) in enumerate(zip(self._value_bufs, self.value_specs)):
+            s.value_bufs[i] = buf.data_ptr()
+            s.value_row_bytes[i] = spec.nbytes
+        s.heap = self._heap_buf.data_ptr()
+        s.active = self._active.data_ptr()
+        s.erase_claim = self._erase_claim.data_ptr()
+        s.freed = self._freed.data_ptr()
+        s.counters = self._counters.data_ptr()
+        s.capacity = self._capacity
+
+    def _ensure_scan(self, n: int) -> None:
+        need = _lib.scan_tiles(max(n, self._capacity))
+        if self._scan.numel() < need:
+            # zeroed once; the library tags every launch with a fresh epoch
+            self._scan = torch.zeros(max(need, 2 * self._scan.numel()), dtype=torch.int64,
+                                     device=self._device)
+            self._struct.scan_status = self._scan.data_ptr()
+            self._struct.scan_status_len = self._scan.numel()
+
+    def _ptr(self):
+        return _lib.ctypes.byref(self._struct)
+
+    def _stream(self) -> int:
+        return _stream_handle(self._device)
+
+    def _sync_size(self) -> int:
+        if not self._size_known:
+            self._size = int(self._counters[_lib.CTR_TOP].item())
+            self._size_known = True
+            self._top_ub = self._size
+        return self._size
+
+    @property
+    def device(self) -> torch.device:
+        return self._device
+
+    @property
+    def capacity(self) -> int:
+        return self._capacity
+
+    @property
+    def bucket_count(self) -> int:
+        """The reference's bucket count: capacity (generic) or 2x capacity
+        (delegate), backends.py:187,233."""
+        return self._capacity * (2 if self.backend_name == "delegate" else 1)
+
+    @property
+    def slot_count(self) -> int:
+        """Open-addressing slots actually allocated on the device."""
+        return self._n_slots
+
+    @property
+    def size(self) -> int:
+        return self._sync_size()
+
+    def __len__(self) -> int:
+        return self._sync_size()
+
+    @property
+    def key_buffer(self) -> torch.Tensor:
+        """Read-only (capacity, arity) int32 view (hashmap.py:227-233)."""
+        return torch.Tensor._make_subclass(ReadOnlyBuffer, self._key_buf, False)
+
+    @property
+    def value_buffers(self) -> tuple:
+        """Writable value buffers (hashmap.py:235-239)."""
+        return self._value_bufs
+
+    def value_buffer(self, i: int = 0) -> torch.Tensor:
+        return self._value_bufs[i]
+
+    # Open3D-style names used by north_star
+    @property
+    def key_tensor(self) -> torch.Tensor:
+        return self.key_buffer
+
+    def value_tensor(self, i: int = 0) -> torch.Tensor:
+        return self.value_buffer(i)
+
+    def active_buf_indices(self) -> torch.Tensor:
+        return self.active_indices()
+
+    def reserve(self, capacity: int) -> None:
+        """Grow to at least ``capacity`` (no-op when already large enough)."""
+        if int(capacity) > self._capacity:
+            self.rehash(int(capacity))
+
+    # -- validation (hashmap.py:246-286) --------------------------------
+
+    def _check_keys(self, keys) -> torch.Tensor:
+        if isinstance(keys, torch.Tensor):
+            k = keys
+            if k.is_floating_point() or k.is_complex():
+                raise ValueError("floating-point keys are not accepted; quantize to int32 first")
+        else:
+            arr = np.asarray(keys)
+            if arr.dtype.kind == "f":
+                raise ValueError("floating-point keys are not accepted; quantize to int32 first")
+            if arr.dtype.kind not in "iub" and arr.size:
+                raise ValueError(f"keys must be integers, got {arr.dtype}")
+            if arr.size == 0 and arr.dtype.kind not in "iub":
+                arr = arr.astype(np.int32)
+            if arr.dtype != np.int32:
+                cast = arr.astype(np.int32)
+                if np.any(cast != arr):
+                    raise ValueError("key values do not fit in int32")
+                arr = cast
+            k = torch.from_numpy(np.ascontiguousarray(arr))
+        if k.dim() == 1:
+            if self.key_arity == 1:
+                k = k.reshape(-1, 1)
+            elif k.numel() == self.key_arity:
+                k = k.reshape(1, -1)
+        if k.dim() != 2 or k.shape[1] != self.key_arity:
+            raise ValueError(f"keys must have shape (n, {self.key_arity}), got {tuple(k.shape)}")
+        if k.dtype != torch.int32:
+            cast = k.to(torch.int32)
+            if bool((cast.to(k.dtype) != k).any()):
+                raise ValueError("key values do not fit in int32")
+            k = cast
+        return k.to(self._device, non_blocking=True).contiguous()
+
+    def _check_values(self, m: int, values) -> list:
+        if len(values) != len(self.value_specs):
+            raise ValueError(f"expected {len(self.value_specs)} value batches, got {len(values)}")
+        out = []
+        for pos, (spec, td, batch) in enumerate(zip(self.value_specs, self._torch_dtypes, values)):
+            if isinstance(batch, torch.Tensor):
+                t = batch.to(dtype=td)
+            else:
+                a = np.asarray(batch)
+                if a.dtype != spec.dtype:
+                    a = a.astype(spec.dtype)
+                t = torch.from_numpy(np.ascontiguousarray(a))
+            if t.dim() == 0 or (t.shape[0] != m and not (m == 0 and t.numel() == 0)):
+                length = t.shape[0] if t.dim() else 1
+                raise ValueError(f"value batch {pos} has length {length}, expected {m}")
+            try:
+                t = t.reshape((m, *spec.shape))
+            except RuntimeError:
+                raise ValueError(
+                    f"value batch {pos} has shape {tuple(t.shape)}, expected "
+                    f"(n, {', '.join(map(str, spec.shape))})") from None
+            out.append(t.to(self._device, non_blocking=True).contiguous())
+        return out
+
+    # -- growth (hashmap.py:311-332) --------------------------------------
+
+    def _grown_capacity(self, extra: int) -> int:
+        size = self._sync_size()
+        cap = self._capacity
+        while cap - size < extra:
+            cap *= 2
+        return cap
+
+    def _rehash_into(self, new_capacity: int) -> None:
+        """Rebuild: active rows in ascending index order become rows
+        0..size-1 of fresh zeroed buffers (hashmap.py:326-332)."""
+        size = self._sync_size()
+        act = torch.empty(size, dtype=torch.int32, device=self._device)
+        if size:
+            call("ash_active_indices", self._ptr(), act.data_ptr(), self._stream())
+        old = AshMap.from_buffer_copy(self._struct)
+        keep = (self._slots, self._key_buf, self._value_bufs, self._heap_buf, self._active,
+                self._erase_claim, self._freed, self._counters)
+        self._init_state(new_capacity)
+        if size:
+            call("ash_rehash_from", self._ptr(), _lib.ctypes.byref(old), act.data_ptr(), size,
+                 self._stream())
+        del keep  # stream-ordered frees: the allocator reuses them only after these kernels
+        self._size = size
+        self._size_known = True
+        self._top_ub = size
+        self._used_ub = size
+
+    def _reserve_slots(self, m: int) -> None:
+        """Keep non-EMPTY slots (live + tombstones) under the probe limit;
+        rebuilds the table in place when erases left too many tombstones."""
+        limit = int(_SLOT_LIMIT * self._n_slots)
+        if self._used_ub + m <= limit:
+            return
+        used = int(self._counters[_lib.CTR_USED].item())
+        size = self._sync_size()
+        self._used_ub = used
+        if used + min(m, self._capacity - size) <= limit:
+            return
+        new_slots = torch.empty_like(self._slots)
+        call("ash_rebuild_table", self._ptr(), new_slots.data_ptr(), self._n_slots, self._stream())
+        self._slots = new_slots
+        self._struct.slots = new_slots.data_ptr()
+        self._used_ub = size
+
+    # -- operations (hashmap.py:336-456) ---------------------------------
+
+    def insert(self, keys, *values) -> BatchResult:
+        """Insert keys with one value batch per value buffer: the first
+        occurrence of each absent key wins a fresh index; existing values are
+        never overwritten (hashmap.py:336-347)."""
+        keys = self._check_keys(keys)
+        vals = self._check_values(keys.shape[0], values)
+        with self._guard.writing():
+            return self._insert_like(keys, vals, association=False)
+
+    def activate(self, keys) -> BatchResult:
+        """Ensure keys are present; values untouched; masks = found OR
+        winner (hashmap.py:349-360)."""
+        keys = self._check_keys(keys)
+        with self._guard.writing():
+            return self._insert_like(keys, None, association=True)
+
+    def _insert_like(self, keys: torch.Tensor, vals, association: bool) -> BatchResult:
+        m = keys.shape[0]
+        dev = self._device
+        idx = torch.empty(m, dtype=torch.int32, device=dev)
+        msk = torch.empty(m, dtype=torch.uint8, device=dev)
+        if m == 0:
+            return BatchResult(idx, msk.view(torch.bool))
+        vptr = None
+        if vals is not None and len(vals):
+            vptr = (_lib.c_void_p * len(vals))(*[v.data_ptr() for v in vals])
+        assoc = 1 if association else 0
+        while True:
+            self._reserve_slots(m)
+            self._ensure_scan(m)
+            if m > self._capacity - self._top_ub:
+                self._sync_size()
+            free = self._capacity - self._top_ub
+            if m <= free:
+                # the whole batch fits: fused path, no host synchronisation
+                call("ash_insert", self._ptr(), keys.data_ptr(), m, vptr, assoc,
+                     idx.data_ptr(), msk.data_ptr(), self._stream())
+                self._top_ub = min(self._capacity, self._top_ub + m)
+                break
+            call("ash_insert_claim", self._ptr(), keys.data_ptr(), m, idx.data_ptr(),
+                 msk.data_ptr(), self._stream())
+            call("ash_insert_count", self._ptr(), m, idx.data_ptr(), msk.data_ptr(),
+                 self._stream())
+            winners = int(self._counters[_lib.CTR_WINNERS].item())
+            if winners <= free:
+                call("ash_insert_commit", self._ptr(), keys.data_ptr(), m, vptr, assoc,
+                     idx.data_ptr(), msk.data_ptr(), self._stream())
+                self._top_ub = min(self._capacity, self._top_ub + winners)
+                break
+            call("ash_insert_rollback", self._ptr(), m, idx.data_ptr(), self._stream())
+            self._used_ub += m
+            if not self.auto_rehash:
+                raise CapacityError(
+                    f"batch needs {winners} free slots, {free} available at capacity "
+                    f"{self._capacity}")
+            # rehash moves every slot, so plan again afterwards (hashmap.py:393-396)
+            self._rehash_into(self._grown_capacity(winners))
+        self._used_ub += m
+        self._size_known = False
+        return BatchResult(idx, msk.view(torch.bool))
+
+    def find(self, keys) -> BatchResult:
+        """Look up keys; the map is not modified (hashmap.py:415-429)."""
+        keys = self._check_keys(keys)
+        with self._guard.reading():
+            m = keys.shape[0]
+            idx = torch.empty(m, dtype=torch.int32, device=self._device)
+            msk = torch.empty(m, dtype=torch.uint8, device=self._device)
+            if m:
+                call("ash_find", self._ptr(), keys.data_ptr(), m, idx.data_ptr(),
+                     msk.data_ptr(), self._stream())
+            return BatchResult(idx, msk.view(torch.bool))
+
+    def erase(self, keys) -> torch.Tensor:
+        """Remove keys; exactly one True per removed key, at its first batch
+        position (hashmap.py:431-456)."""
+        keys = self._check_keys(keys)
+        with self._guard.writing():
+            m = keys.shape[0]
+            out = torch.empty(m, dtype=torch.uint8, device=self._device)
+            if m:
+                scratch = torch.empty(2 * m, dtype=torch.int32, device=self._device)
+                call("ash_erase", self._ptr(), keys.data_ptr(), m, out.data_ptr(),
+                     scratch.data_ptr(), self._stream())
+                self._size_known = False
+            return out.view(torch.bool)
+
+    def active_indices(self) -> torch.Tensor:
+        """All buffer indices holding an entry, ascending (hashmap.py:458-460)."""
+        with self._guard.reading():
+            size = self._sync_size()
+            out = torch.empty(size, dtype=torch.int32, device=self._device)
+            if size:
+                call("ash_active_indices", self._ptr(), out.data_ptr(), self._stream())
+            return out
+
+    def rehash(self, new_capacity: int) -> None:
+        """Rebuild at the given capacity; content preserved, indices become
+        0..size-1 in ascending old-index order (hashmap.py:462-472)."""
+        new_capacity = int(new_capacity)
+        if new_capacity < 1:
+            raise ValueError("capacity must be >= 1")
+        size = self._sync_size()
+        if new_capacity < size:
+            raise ValueError(f"new capacity {new_capacity} is below current size {size}")
+        with self._guard.writing():
+            self._rehash_into(new_capacity)
+
+    # -- content helpers (hashmap.py:476-496) ----------------------------
+
+    def items_arrays(self) -> tuple:
+        act = self.active_indices().long()
+        return (self._key_buf[act].clone(), *(b[act].clone() for b in self._value_bufs))
+
+    def validate(self) -> None:
+        """Structural invariants (hashmap.py:483-496); raises AssertionError."""
+        size = self._sync_size()
+        act = self.active_indices().long()
+        free = self._heap_buf[size:].long()
+        assert act.numel() == size, "size counter vs active flags"
+        assert int(self._active.sum().item()) == size, "size counter vs active flags"
+        assert free.numel() + act.numel() == self._capacity, "heap conservation"
+        both = torch.sort(torch.cat([act, free])).values
+        assert torch.equal(both, torch.arange(self._capacity, device=self._device)), \
+            "active/free sets must partition the index range"
+        if size:
+            res = self.find(self._key_buf[act])
+            assert bool(res.masks.all()), "stored key failed lookup"
+            assert torch.equal(torch.sort(res.indices.long()).values, act), \
+                "lookup resolved to foreign indices"
+        flags = int(self._counters[_lib.CTR_FLAGS].item())
+        assert flags & _lib.FLAG_TABLE_FULL == 0, "a probe wrapped the whole table"
+
+    def save(self, path, metadata=None) -> None:
+        raise NotImplementedError("ASHL snapshots (serialize.py) are not on the device path yet")
+
+    @classmethod
+    def load(cls, path, backend=None, threads=1):
+        raise NotImplementedError("ASHL snapshots (serialize.py) are not on the device path yet")
+
+
+class HashSet(HashMap):
+    """Hash map without value buffers (hashmap.py:508-515)."""
+
+    def __init__(self, capacity: int, key_arity: int, backend: str = "generic",
+                 threads: int = 1, auto_rehash: bool = True, device=None):
+        super().__init__(capacity, key_arity, value_specs=(), backend=backend,
+                         threads=threads, auto_rehash=auto_rehash, device=device)
