@@ -1,0 +1,414 @@
+"""Benchmark: insert & find Mops/s on int3 keys (BASELINE.json metric).
+
+Workload at N=1 (BASELINE.json configs[1], the config the metric is quoted
+on): a fresh map of capacity 10M, one insert of 10M int3 keys (uniqueness
+0.5, one float32 value each), then one find of the same 10M keys.  A step =
+that insert + find; value = (insert ops + find ops) / step time.  Map
+construction (HashMap.clear) is excluded from the step as in the reference
+timing loop (pkg/src/spatialhash/bench.py:110,123).  The working set (keys
+120 MB + values 40 MB + table 512 MB) exceeds the 126 MB L2, and L2 is also
+flushed between steps.
+
+Arms:
+  default            this repo's CUDA path; one JSON line on rank 0.
+  --impl reference   the reference algorithm on the host CPU (the numpy
+                     oracle port, oracle/ash_oracle.py, since the reference is
+                     pure Python and cannot travel to the GPU box).
+Multi-GPU (torchrun, N>1): hash-partitioned map, NCCL all-to-all routing,
+10M insert + 10M find keys per rank per step (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_KEYS = 10_000_000
+RHO = 0.5
+CAPACITY = 10_000_000
+CPU_SAMPLE_KEYS = 2_000_000
+METRIC = "insert & find Mops/s (int3 keys)"
+UNIT = "Mops/s"
+
+
+def algorithmic_bytes(op: str, rho_new: float, value_bytes: int, key_bytes: int = 12) -> float:
+    """K + 5 + S [+ rho_new (K + 2V + S)], S = 32 B sector."""
+    base = key_bytes + 5 + 32
+    if op == "find":
+        return base
+    return base + rho_new * (key_bytes + 2 * value_bytes + 32)
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling while the GPU is busy."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        return False
+
+    def summary(self):
+        rows = []
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                rows.append((float(f[0]), float(f[1]), f[4:8]))
+            except (ValueError, IndexError):
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        load = [r for r in rows if r[0] > 0.5 * r[1]] or rows
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in load for n, v in zip(names, r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm (numpy oracle port) on host cores
+
+def cpu_reference_step(keys: np.ndarray, vals: np.ndarray):
+    from oracle.ash_oracle import OracleMap
+    m = OracleMap(len(keys), 3, [np.float32])
+    t0 = time.perf_counter()
+    m.insert(keys, vals)
+    r = m.find(keys)
+    dt = time.perf_counter() - t0
+    assert bool(r.masks.all())
+    return dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    from paper_2110_00511_b200.workloads import int3_batch
+    keys = int3_batch(CPU_SAMPLE_KEYS, RHO, seed=0)
+    vals = np.random.default_rng(1).random((len(keys), 1), dtype=np.float32)
+    for _ in range(args.warmup):
+        cpu_reference_step(keys, vals)
+    times = [cpu_reference_step(keys, vals) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = 2 * CPU_SAMPLE_KEYS / t / 1e6
+    sample = (f"per step: insert+find of {CPU_SAMPLE_KEYS:,} int3 keys (rho={RHO}, f32[1]) into a "
+              f"fresh map of capacity {CPU_SAMPLE_KEYS:,}, the reference generic-backend algorithm "
+              f"(numpy oracle port, single thread)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"C2 sample: {CPU_SAMPLE_KEYS:,} int3 keys rho={RHO} f32[1] insert+find",
+                   "capacity": CPU_SAMPLE_KEYS},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+class Events:
+    def __init__(self, torch, stream):
+        self.torch = torch
+        self.stream = stream
+        self.pairs = []
+
+    def start(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def stop(self, s):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        self.pairs.append((s, e))
+
+    def total_ms(self):
+        self.torch.cuda.synchronize()
+        return sum(s.elapsed_time(e) for s, e in self.pairs)
+
+
+def l2_flush(torch, buf):
+    buf.add_(1)  # 256 MB read+write > 126 MB L2
+
+
+def gpu_single(args, torch, dev):
+    """N=1: the plain map (no routing)."""
+    import paper_2110_00511_b200 as ash
+    from paper_2110_00511_b200 import _lib
+    from paper_2110_00511_b200.workloads import int3_batch
+
+    stream = torch.cuda.current_stream(dev)
+    keys_np = int3_batch(N_KEYS, RHO, seed=0)
+    vals_np = np.random.default_rng(1).random((N_KEYS, 1), dtype=np.float32)
+    keys_h = torch.from_numpy(keys_np).pin_memory()
+    vals_h = torch.from_numpy(vals_np).pin_memory()
+    keys = keys_h.to(dev)
+    vals = vals_h.to(dev)
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    m = ash.HashMap(CAPACITY, 3, [np.float32], device=dev)
+
+    def step(ev):
+        m.clear()
+        l2_flush(torch, flush)
+        s = ev.start()
+        m.insert(keys, vals)
+        m.find(keys)
+        ev.stop(s)
+
+    # correctness backstop (reference bench.py:134-150)
+    m.clear()
+    r = m.insert(keys, vals)
+    f = m.find(keys)
+    n_unique = int(np.ceil(RHO * N_KEYS))
+    assert m.size == n_unique and int(r.masks.sum()) == n_unique and bool(f.masks.all())
+
+    warm = Events(torch, stream)
+    for _ in range(args.warmup):
+        step(warm)
+    torch.cuda.synchronize()
+    timed = Events(torch, stream)
+    with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            step(timed)
+        torch.cuda.synchronize()
+        # keep the GPU busy for the clock sampler: extra untimed steps
+        extra = Events(torch, stream)
+        t_end = time.time() + (0.0 if args.profile else 1.0)
+        while time.time() < t_end:
+            step(extra)
+        torch.cuda.synchronize()
+    ms = timed.total_ms() / args.steps
+    value = 2 * N_KEYS / (ms / 1e3) / 1e6
+    if args.profile:
+        print(json.dumps({"profile_ms_per_step": ms, "value": value}), flush=True)
+        sys.exit(0)
+
+    # per-kernel split (same workload): claim / commit / find, CUDA events on
+    # the launching stream
+    kern = {"claim": [], "commit": [], "find": []}
+    for _ in range(5):
+        m.clear()
+        l2_flush(torch, flush)
+        idx = torch.empty(N_KEYS, dtype=torch.int32, device=dev)
+        msk = torch.empty(N_KEYS, dtype=torch.uint8, device=dev)
+        vptr = (_lib.c_void_p * 1)(vals.data_ptr())
+        m._ensure_scan(N_KEYS)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        _lib.call("ash_insert_claim", m._ptr(), keys.data_ptr(), N_KEYS, idx.data_ptr(), msk.data_ptr(), m._stream())
+        e[1].record(stream)
+        _lib.call("ash_insert_commit", m._ptr(), keys.data_ptr(), N_KEYS, vptr, 0, idx.data_ptr(), msk.data_ptr(), m._stream())
+        e[2].record(stream)
+        m._size_known = False
+        l2_flush(torch, flush)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e3.record(stream)
+        m.find(keys)
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        kern["claim"].append(e[0].elapsed_time(e[1]))
+        kern["commit"].append(e[1].elapsed_time(e[2]))
+        kern["find"].append(e3.elapsed_time(e[3]))
+    kms = {k: statistics.median(v) for k, v in kern.items()}
+
+    # e2e: public API with pinned host buffers; H2D of inputs and D2H of the
+    # results inside the timed region
+    idx_h = torch.empty(N_KEYS, dtype=torch.int32).pin_memory()
+    msk_h = torch.empty(N_KEYS, dtype=torch.bool).pin_memory()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        m.clear()
+        torch.cuda.synchronize()
+        s = torch.cuda.Event(enable_timing=True)
+        t = torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        r = m.insert(keys_h, vals_h)
+        idx_h.copy_(r.indices, non_blocking=True)
+        msk_h.copy_(r.masks, non_blocking=True)
+        f = m.find(keys_h)
+        idx_h.copy_(f.indices, non_blocking=True)
+        msk_h.copy_(f.masks, non_blocking=True)
+        t.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e.append(s.elapsed_time(t))
+    e2e_ms = sum(e2e) / len(e2e)
+    h2d = 2 * keys_np.nbytes + vals_np.nbytes
+    d2h = 2 * (idx_h.numel() * 4 + msk_h.numel())
+
+    sweep = run_sweep(torch, dev, ash, flush)
+    return dict(ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
+                sweep=sweep, launches_per_step=3)
+
+
+def run_sweep(torch, dev, ash, flush):
+    """configs[1] sweep: rho in {0.1, 0.5, 1.0} x value f32[1] / f32[8];
+    insert-only and find-only Mops/s (fresh map per trial)."""
+    from paper_2110_00511_b200.workloads import int3_batch
+    out = []
+    stream = torch.cuda.current_stream(dev)
+    for rho in (0.1, 0.5, 1.0):
+        keys = torch.from_numpy(int3_batch(N_KEYS, rho, seed=0)).to(dev)
+        for width in (1, 8):
+            vals = torch.rand((N_KEYS, width), dtype=torch.float32, device=dev)
+            m = ash.HashMap(CAPACITY, 3, [((width,), np.float32)], device=dev)
+            ti, tf = [], []
+            for trial in range(6):
+                m.clear()
+                l2_flush(torch, flush)
+                a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a.record(stream)
+                m.insert(keys, vals)
+                b.record(stream)
+                l2_flush(torch, flush)
+                b2 = torch.cuda.Event(enable_timing=True)
+                b2.record(stream)
+                m.find(keys)
+                c.record(stream)
+                torch.cuda.synchronize()
+                if trial:
+                    ti.append(a.elapsed_time(b))
+                    tf.append(b2.elapsed_time(c))
+            ims, fms = statistics.median(ti), statistics.median(tf)
+            bw, _ = _peaks()
+            ib = algorithmic_bytes("insert", rho, 4 * width) * N_KEYS
+            fb = algorithmic_bytes("find", rho, 4 * width) * N_KEYS
+            out.append({"rho": rho, "value": f"f32[{width}]",
+                        "insert_mops": round(N_KEYS / ims / 1e3, 1),
+                        "find_mops": round(N_KEYS / fms / 1e3, 1),
+                        "insert_frac": round(ib / (ims / 1e3) / 1e9 / bw, 4),
+                        "find_frac": round(fb / (fms / 1e3) / 1e9 / bw, 4)})
+            del m
+    return out
+
+
+def cpu_baseline_sample():
+    from paper_2110_00511_b200.workloads import int3_batch
+    keys = int3_batch(CPU_SAMPLE_KEYS, RHO, seed=0)
+    vals = np.random.default_rng(1).random((len(keys), 1), dtype=np.float32)
+    times = [cpu_reference_step(keys, vals) for _ in range(3)]
+    t = min(times)
+    return {"value": round(2 * CPU_SAMPLE_KEYS / t / 1e6, 4), "unit": UNIT, "cores": 1,
+            "kind": "port",
+            "sample": f"insert+find of {CPU_SAMPLE_KEYS:,} int3 keys (rho={RHO}, f32[1]), fresh map; "
+                      f"reference generic-backend algorithm via the numpy oracle port, single thread, "
+                      f"best of 3"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    if world > 1:
+        from paper_2110_00511_b200 import partitioned
+        partitioned.bench_main(args, rank, world)
+        return
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    if args.profile:
+        args.no_cpu_baseline = True
+    res = gpu_single(args, torch, dev)
+    bw, peak_kind = _peaks()
+    kms = res["kms"]
+    # dominant kernel and its roofline (algorithmic bytes per launch)
+    per_kernel_bytes = {
+        "claim": (12 + 32 + 5) * N_KEYS,                    # key, table sector, scratch idx+mask
+        "commit": (5 + 5) * N_KEYS + RHO * (12 + 2 * 4 + 32) * N_KEYS,  # scratch in, out; winner rows + slot
+        "find": algorithmic_bytes("find", RHO, 4) * N_KEYS,
+    }
+    dom = max(kms, key=kms.get)
+    achieved = per_kernel_bytes[dom] / (kms[dom] / 1e3) / 1e9
+    cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
+    line = {
+        "metric": METRIC, "value": round(res["value"], 2), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": "configs[1]: 10M int3 keys, uniqueness 0.5, value f32[1]; "
+                               "insert into a fresh capacity-10M map, then find the same keys",
+                   "keys": N_KEYS, "uniqueness": RHO, "capacity": CAPACITY, "value": "f32[1]",
+                   "l2": "flushed between steps (256 MB write); working set > L2",
+                   "construction": "excluded (HashMap.clear before each step)"},
+        "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": round(achieved, 1),
+                     "peak": bw, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / bw, 4), "traffic": None,
+                     "kernel_ms": {k: round(v, 4) for k, v in kms.items()}},
+        "op_roofline": {
+            "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS /
+                                 ((kms["claim"] + kms["commit"]) / 1e3) / 1e9 / bw, 4),
+            "find_frac": round(per_kernel_bytes["find"] / (kms["find"] / 1e3) / 1e9 / bw, 4)},
+        "e2e": {"value": round(2 * N_KEYS / (res["e2e_ms"] / 1e3) / 1e6, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
+        "gpu_launches": res["launches_per_step"] * args.steps,
+        "clocks": res["clocks"],
+        "sweep": res["sweep"],
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -560,6 +560,16 @@ class HashMap:
         with self._guard.writing():
             self._rehash_into(new_capacity)
 
+    def clear(self) -> None:
+        """Remove every entry, keep the capacity (Open3D ``clear``); the map
+        is then indistinguishable from a freshly constructed one."""
+        with self._guard.writing():
+            call("ash_map_reset", self._ptr(), 1, self._stream())
+            self._size = 0
+            self._size_known = True
+            self._top_ub = 0
+            self._used_ub = 0
+
     # -- content helpers (hashmap.py:476-496) ----------------------------
 
     def items_arrays(self) -> tuple:
