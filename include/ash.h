@@ -38,7 +38,7 @@ extern "C" {
 
 /* device counter slots (int32 each, ASH_N_COUNTERS of them) */
 #define ASH_CTR_TOP 0      /* index-heap top; equals the map size          */
-#define ASH_CTR_USED 1     /* non-EMPTY table slots (live+pending+tomb)    */
+#define ASH_CTR_TOMBS 1    /* tombstone slots (erased / rolled-back claims) */
 #define ASH_CTR_WINNERS 2  /* new keys of the last insert/activate         */
 #define ASH_CTR_ERASED 3   /* keys removed by the last erase               */
 #define ASH_CTR_FLAGS 4    /* sticky error bits, see ASH_FLAG_*            */
@@ -77,6 +77,11 @@ typedef struct ash_map {
 
 int ash_abi_version(void);
 const char* ash_last_error(void);
+
+/* Per-device setup for the random-access workload: caps the L2 fetch
+ * granularity at `l2_fetch_bytes` (32 = one sector per random probe) on the
+ * current device.  Call once per process and device. */
+int ash_device_setup(int32_t l2_fetch_bytes);
 
 /* Scan-status words needed for a single-pass scan over n items. */
 int64_t ash_scan_tiles(int64_t n);

@@ -12,7 +12,7 @@ from .build import LIB_PATH
 
 ASH_OK, ASH_ERR_INVALID, ASH_ERR_CAPACITY, ASH_ERR_CUDA = 0, 1, 2, 3
 MAX_VALUE_BUFFERS = 8
-CTR_TOP, CTR_USED, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT = 0, 1, 2, 3, 4, 5
+CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT = 0, 1, 2, 3, 4, 5
 N_COUNTERS = 8
 FLAG_TABLE_FULL, FLAG_RANGE = 1, 2
 TILE = 2048  # positions per scan tile (csrc kTile)
@@ -36,6 +36,7 @@ _M = POINTER(AshMap)
 _SIGNATURES = {
     "ash_abi_version": (c_int32, []),
     "ash_last_error": (c_char_p, []),
+    "ash_device_setup": (c_int32, [c_int32]),
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -88,6 +89,24 @@ def call(name: str, *args) -> None:
     if rc == ASH_ERR_INVALID:
         raise ValueError(f"{name}: {msg}")
     raise AshError(f"{name} failed ({rc}): {msg}")
+
+
+_setup_done = set()
+# one DRAM sector per random probe (profiles/ r01 showed 64+ B over-fetch);
+# ASH_L2_FETCH=0 leaves the driver default (for A/B measurements)
+import os as _os
+L2_FETCH_BYTES = int(_os.environ.get("ASH_L2_FETCH", "32"))
+
+
+def device_setup(device) -> None:
+    """Once per process and device: cap the L2 fetch granularity."""
+    import torch
+    key = (device.type, device.index)
+    if key in _setup_done:
+        return
+    with torch.cuda.device(device):
+        call("ash_device_setup", L2_FETCH_BYTES)
+    _setup_done.add(key)
 
 
 def scan_tiles(n: int) -> int:

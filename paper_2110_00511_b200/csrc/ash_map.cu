@@ -180,6 +180,36 @@ __device__ __forceinline__ Key<A> load_key(const int32_t* keys, int64_t p, int a
   return k;
 }
 
+// Coalesced key load for arity 3: the warp reads its 32 rows (384 B) as
+// three fully used 128-byte transactions into shared memory, then each lane
+// picks its row (stride-3 words: bank-conflict free).  Every lane of the warp
+// must call this (before any early exit).
+template <int A>
+__device__ __forceinline__ Key<A> load_key_warp(const int32_t* __restrict__ keys, int64_t p, int64_t n,
+                                                int arity, uint32_t* stage) {
+  if (A != 3) {
+    Key<A> k;
+    if (p < n) k = load_key<A>(keys, p, arity);
+    return k;
+  }
+  const int lane = threadIdx.x & 31;
+  uint32_t* st = stage + (threadIdx.x >> 5) * 96;
+  const int64_t base = p - lane;
+  const int64_t words = (n - base < 32 ? n - base : 32) * 3;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int w = lane + 32 * r;
+    if (w < words) st[w] = __ldg(reinterpret_cast<const uint32_t*>(keys) + base * 3 + w);
+  }
+  __syncwarp();
+  Key<A> k;
+  k.row = keys + p * 3;
+  k.w[0] = st[lane * 3];
+  k.w[1] = st[lane * 3 + 1];
+  k.w[2] = st[lane * 3 + 2];
+  return k;
+}
+
 template <int A>
 __device__ __forceinline__ uint32_t hash_key(const Key<A>& k, int arity) {
   uint32_t h = 0x9747b28cu;
@@ -262,7 +292,7 @@ __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, u
 template <int A>
 __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k, uint32_t h,
                                                 uint32_t j, const int32_t* batch, uint8_t* mask,
-                                                int32_t* counters, bool* claimed_empty) {
+                                                int32_t* counters, bool* claimed_tomb) {
   const uint32_t me = PEND | j;
   uint32_t b = h & t.bucket_mask;
   int first = 0;
@@ -305,7 +335,7 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
     continue;
   claim:
     if (cas128(t.slots + free_slot, free_val, slot_value<A>(k, me))) {
-      *claimed_empty = (free_val.w == EMPTY);
+      *claimed_tomb = (free_val.w == TOMB);
       return PEND | CLAIMER | free_slot;
     }
     // lost the race for free_slot: everything before it is unchanged, so
@@ -347,9 +377,10 @@ template <int A>
 __global__ void __launch_bounds__(kBlock) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                  int32_t* __restrict__ out_idx,
                                                  uint8_t* __restrict__ out_mask) {
+  __shared__ uint32_t stage[kBlock * 3];
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage);
   if (p >= n) return;
-  Key<A> k = load_key<A>(keys, p, t.arity);
   int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), nullptr);
   out_idx[p] = idx;
   out_mask[p] = idx >= 0;
@@ -371,13 +402,14 @@ template <int A>
 __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
                                                   int32_t* counters) {
+  __shared__ uint32_t stage[kBlock * 3];
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (p == 0) counters[ASH_CTR_WINNERS] = 0;
   const bool valid = p < n;
   const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
+  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage);
   if (!valid) return;
-  Key<A> k = load_key<A>(keys, p, t.arity);
   // warp pre-aggregation: equal keys in a warp resolve through their lowest
   // lane (= lowest batch position); the rest are duplicate losers or share
   // the leader's found index (hashmap.py:125-131 first-occurrence rule)
@@ -385,10 +417,10 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
   if (A != 0) same_key_in_warp<A>(k, live, &grp);
   const int leader = __ffs(grp) - 1;
   uint32_t res = 0;
-  bool claimed_empty = false;
+  bool claimed_tomb = false;
   if (lane == leader)
     res = probe_claim<A>(t, k, hash_key<A>(k, t.arity), static_cast<uint32_t>(p), keys, mask, counters,
-                         &claimed_empty);
+                         &claimed_tomb);
   __syncwarp(live);
   const uint32_t lres = __shfl_sync(live, res, leader);
   if (lane == leader) {
@@ -399,8 +431,9 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
     tmp[p] = static_cast<int32_t>(PEND);
     mask[p] = DEMOTED;
   }
-  const unsigned ce = __ballot_sync(live, claimed_empty);
-  if (ce && lane == __ffs(live) - 1) atomicAdd(&counters[ASH_CTR_USED], __popc(ce));
+  // tombstones reused by this batch (rare: only after erases)
+  const unsigned ct = __ballot_sync(live, claimed_tomb);
+  if (ct && lane == __ffs(live) - 1) atomicSub(&counters[ASH_CTR_TOMBS], __popc(ct));
 }
 
 // ---------------------------------------------------------------------------
@@ -541,18 +574,23 @@ __global__ void __launch_bounds__(kBlock)
   uint32_t bal[kItems];
   TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, counters + ASH_CTR_TOP);
   const int arity = A ? A : t.arity;
+  // issue every winner's heap load before any store (they are independent;
+  // stores to the table would otherwise serialise them)
+  int32_t hidx[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it)
+    hidx[it] = win[it] ? __ldg(heap + ts.base + item_rank(sm, bal, it)) : 0;
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
     if (p >= n) continue;
     if (win[it]) {
-      const uint32_t rank = item_rank(sm, bal, it);
-      const int32_t idx = heap[ts.base + rank];
+      const int32_t idx = hidx[it];
       const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
       t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
       const int32_t* kr = keys + p * arity;
       int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
-      for (int d = 0; d < arity; ++d) dr[d] = kr[d];
+      for (int d = 0; d < arity; ++d) dr[d] = __ldg(kr + d);
 #pragma unroll
       for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
         if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
@@ -574,20 +612,53 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-__global__ void k_count_winners(const int32_t* __restrict__ tmp, const uint8_t* __restrict__ mask, int64_t n,
-                                int32_t* counters) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
-  bool w = p < n && tmp[p] < 0 && !(mask[p] & DEMOTED);
-  unsigned b = __ballot_sync(0xFFFFFFFFu, w);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[ASH_CTR_WINNERS], __popc(b));
+// Block-wide count of a predicate accumulated into *ctr with one atomic per
+// block (a warp-level atomic on one address serialises in its L2 slice).
+// Every thread of the block must call it.
+__device__ __forceinline__ void block_count_add(bool pred, int32_t* ctr) {
+  __shared__ int32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const unsigned b = __ballot_sync(0xFFFFFFFFu, pred);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_cnt, __popc(b));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(ctr, s_cnt);
 }
 
-__global__ void k_rollback(uint4* slots, const int32_t* __restrict__ tmp, int64_t n) {
+constexpr int kCountItems = 16;  // positions per thread in the counting kernels
+
+__global__ void __launch_bounds__(kBlock) k_count_winners(const int32_t* __restrict__ tmp,
+                                                          const uint8_t* __restrict__ mask, int64_t n,
+                                                          int32_t* counters) {
+  int cnt = 0;
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kBlock) * kCountItems + threadIdx.x;
+#pragma unroll 4
+  for (int it = 0; it < kCountItems; ++it) {
+    const int64_t p = base + it * kBlock;
+    cnt += (p < n && tmp[p] < 0 && !(mask[p] & DEMOTED));
+  }
+  __shared__ int32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int w = __reduce_add_sync(0xFFFFFFFFu, cnt);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_cnt, w);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(&counters[ASH_CTR_WINNERS], s_cnt);
+}
+
+__global__ void __launch_bounds__(kBlock) k_rollback(uint4* slots, const int32_t* __restrict__ tmp, int64_t n,
+                                                     int32_t* counters) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
-  if (p >= n) return;
-  const uint32_t v = static_cast<uint32_t>(tmp[p]);
-  // a claimed slot reverts to TOMBSTONE: probe chains through it stay intact
-  if ((v & PEND) && (v & CLAIMER)) slots[v & SLOT_MASK].w = TOMB;
+  bool claimed = false;
+  if (p < n) {
+    const uint32_t v = static_cast<uint32_t>(tmp[p]);
+    // a claimed slot reverts to TOMBSTONE: probe chains through it stay intact
+    if ((v & PEND) && (v & CLAIMER)) {
+      slots[v & SLOT_MASK].w = TOMB;
+      claimed = true;
+    }
+  }
+  block_count_add(claimed, &counters[ASH_CTR_TOMBS]);
 }
 
 // ---------------------------------------------------------------------------
@@ -625,8 +696,7 @@ __global__ void __launch_bounds__(kBlock)
     }
     out_mask[p] = hit;
   }
-  unsigned b = __ballot_sync(0xFFFFFFFFu, hit);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&counters[ASH_CTR_ERASED], __popc(b));
+  block_count_add(hit, &counters[ASH_CTR_ERASED]);
 }
 
 // freed flags over [0, capacity) -> heap[top - E + rank], ascending
@@ -654,7 +724,10 @@ __global__ void __launch_bounds__(kBlock) k_free_compact(uint8_t* freed, int64_t
     heap[start + item_rank(sm, bal, it)] = static_cast<int32_t>(i);
     freed[i] = 0;
   }
-  if (tile == gridDim.x - 1 && threadIdx.x == 0) counters[ASH_CTR_TOP] = static_cast<int32_t>(start);
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+    counters[ASH_CTR_TOP] = static_cast<int32_t>(start);
+    counters[ASH_CTR_TOMBS] += erased;
+  }
 }
 
 // ascending select of active flags (hashmap.py:458-460)
@@ -701,7 +774,7 @@ __global__ void __launch_bounds__(kBlock)
   const int64_t i = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   if (i == 0) {
     dst_counters[ASH_CTR_TOP] = static_cast<int32_t>(n_act);
-    dst_counters[ASH_CTR_USED] = static_cast<int32_t>(n_act);
+    dst_counters[ASH_CTR_TOMBS] = 0;
   }
   if (i >= n_act) return;
   const int64_t src = act[i];
@@ -719,7 +792,7 @@ template <int A>
 __global__ void __launch_bounds__(kBlock)
     k_rebuild_table(const uint4* __restrict__ old_slots, int64_t old_n, Table dst, int32_t* counters) {
   const int64_t s = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
-  if (s == 0) counters[ASH_CTR_USED] = ld_volatile_i32(counters + ASH_CTR_TOP);
+  if (s == 0) counters[ASH_CTR_TOMBS] = 0;
   if (s >= old_n) return;
   const uint4 v = old_slots[s];
   if (v.w >= PEND) return;
@@ -778,10 +851,10 @@ __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __rest
   if (bad) grp = 1u << lane;
   const int leader = __ffs(grp) - 1;
   uint32_t res = PEND;
-  bool claimed_empty = false;
+  bool claimed_tomb = false;
   if (lane == leader && !bad)
     res = probe_claim<3>(t, k, hash_key<3>(k, 3), static_cast<uint32_t>(p), nullptr, mask, counters,
-                         &claimed_empty);
+                         &claimed_tomb);
   __syncwarp(live);
   if (lane == leader && !bad) {
     tmp[p] = static_cast<int32_t>(res);
@@ -902,6 +975,18 @@ extern "C" {
 
 int ash_abi_version(void) { return ASH_ABI_VERSION; }
 
+int ash_device_setup(int32_t l2_fetch_bytes) {
+  if (l2_fetch_bytes < 0 || l2_fetch_bytes > 128 || (l2_fetch_bytes & (l2_fetch_bytes - 1)))
+    return fail(ASH_ERR_INVALID, "l2 fetch granularity must be a power of two <= 128");
+  if (l2_fetch_bytes == 0) return ASH_OK;
+  cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(l2_fetch_bytes));
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "cudaDeviceSetLimit(MaxL2FetchGranularity): %s", cudaGetErrorString(e));
+    return ASH_ERR_CUDA;
+  }
+  return ASH_OK;
+}
+
 const char* ash_last_error(void) { return g_err; }
 
 int64_t ash_scan_tiles(int64_t n) { return tiles_for(n < 1 ? 1 : n); }
@@ -952,7 +1037,8 @@ int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint
   if (int rc = check_batch(n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(m->counters + ASH_CTR_WINNERS, 0, sizeof(int32_t), s);
-  if (n > 0) k_count_winners<<<grid_for(n, kBlock), kBlock, 0, s>>>(out_idx, out_mask, n, m->counters);
+  if (n > 0)
+    k_count_winners<<<grid_for(n, kBlock * kCountItems), kBlock, 0, s>>>(out_idx, out_mask, n, m->counters);
   return check_launch("ash_insert_count");
 }
 
@@ -982,7 +1068,8 @@ int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* s
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
-  k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n);
+  k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n,
+                                                                    m->counters);
   return check_launch("ash_insert_rollback");
 }
 

@@ -37,8 +37,12 @@ def _points_tensor(points, device) -> torch.Tensor:
 
 
 def _device(device) -> torch.device:
-    return torch.device(device) if device is not None else \
+    dev = torch.device(device) if device is not None else \
         torch.device("cuda", torch.cuda.current_device())
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    _lib.device_setup(dev)
+    return dev
 
 
 def quantize(positions, cell: float, device=None) -> torch.Tensor:

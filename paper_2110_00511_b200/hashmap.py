@@ -219,10 +219,13 @@ class HashMap:
             torch.device("cuda", torch.cuda.current_device())
         if self._device.type != "cuda":
             raise ValueError("HashMap storage must be a CUDA device")
+        if self._device.index is None:
+            self._device = torch.device("cuda", torch.cuda.current_device())
         self._torch_dtypes = tuple(_torch_dtype(s.dtype) for s in self.value_specs)
         self._guard = _AccessGuard()
         self._debug_checksum = False
         self._heap = _HeapView(self)
+        _lib.device_setup(self._device)
         self._init_state(int(capacity))
 
     # -- state ---------------------------------------------------------
@@ -249,7 +252,7 @@ class HashMap:
         self._size = 0
         self._size_known = True
         self._top_ub = 0
-        self._used_ub = 0
+        self._tombs_ub = 0
 
     def _fill_struct(self) -> None:
         s = self._struct
@@ -431,24 +434,25 @@ class HashMap:
         self._size = size
         self._size_known = True
         self._top_ub = size
-        self._used_ub = size
+        self._tombs_ub = 0
 
     def _reserve_slots(self, m: int) -> None:
-        """Keep non-EMPTY slots (live + tombstones) under the probe limit;
-        rebuilds the table in place when erases left too many tombstones."""
+        """Keep non-EMPTY slots (live + tombstones + this batch's claims)
+        under the probe limit; rebuilds the table in place (same indices)
+        when erases left too many tombstones."""
         limit = int(_SLOT_LIMIT * self._n_slots)
-        if self._used_ub + m <= limit:
+        if self._top_ub + self._tombs_ub + m <= limit:
             return
-        used = int(self._counters[_lib.CTR_USED].item())
+        tombs = int(self._counters[_lib.CTR_TOMBS].item())
         size = self._sync_size()
-        self._used_ub = used
-        if used + min(m, self._capacity - size) <= limit:
+        self._tombs_ub = tombs
+        if size + tombs + min(m, self._capacity - size) <= limit:
             return
         new_slots = torch.empty_like(self._slots)
         call("ash_rebuild_table", self._ptr(), new_slots.data_ptr(), self._n_slots, self._stream())
         self._slots = new_slots
         self._struct.slots = new_slots.data_ptr()
-        self._used_ub = size
+        self._tombs_ub = 0
 
     # -- operations (hashmap.py:336-456) ---------------------------------
 
@@ -502,14 +506,13 @@ class HashMap:
                 self._top_ub = min(self._capacity, self._top_ub + winners)
                 break
             call("ash_insert_rollback", self._ptr(), m, idx.data_ptr(), self._stream())
-            self._used_ub += m
+            self._tombs_ub += m
             if not self.auto_rehash:
                 raise CapacityError(
                     f"batch needs {winners} free slots, {free} available at capacity "
                     f"{self._capacity}")
             # rehash moves every slot, so plan again afterwards (hashmap.py:393-396)
             self._rehash_into(self._grown_capacity(winners))
-        self._used_ub += m
         self._size_known = False
         return BatchResult(idx, msk.view(torch.bool))
 
@@ -537,6 +540,7 @@ class HashMap:
                 call("ash_erase", self._ptr(), keys.data_ptr(), m, out.data_ptr(),
                      scratch.data_ptr(), self._stream())
                 self._size_known = False
+                self._tombs_ub += m
             return out.view(torch.bool)
 
     def active_indices(self) -> torch.Tensor:
@@ -568,7 +572,7 @@ class HashMap:
             self._size = 0
             self._size_known = True
             self._top_ub = 0
-            self._used_ub = 0
+            self._tombs_ub = 0
 
     # -- content helpers (hashmap.py:476-496) ----------------------------
 
