@@ -83,6 +83,10 @@ const char* ash_last_error(void);
  * current device.  Call once per process and device. */
 int ash_device_setup(int32_t l2_fetch_bytes);
 
+/* Mark batch streams (keys, values, scratch, outputs) L2 evict-first so the
+ * table keeps the L2 (default on; process-wide). */
+int ash_set_stream_hints(int32_t on);
+
 /* Scan-status words needed for a single-pass scan over n items. */
 int64_t ash_scan_tiles(int64_t n);
 

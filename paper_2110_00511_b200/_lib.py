@@ -6,6 +6,7 @@ raises, and every launcher error surfaces as a Python exception.
 from __future__ import annotations
 
 import ctypes
+import os as _os
 from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_uint32, c_void_p
 
 from .build import LIB_PATH
@@ -37,6 +38,7 @@ _SIGNATURES = {
     "ash_abi_version": (c_int32, []),
     "ash_last_error": (c_char_p, []),
     "ash_device_setup": (c_int32, [c_int32]),
+    "ash_set_stream_hints": (c_int32, [c_int32]),
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -74,6 +76,7 @@ def _load():
 
 
 lib = _load()
+lib.ash_set_stream_hints(int(_os.environ.get("ASH_STREAM_HINTS", "1")))
 
 
 class AshError(RuntimeError):
@@ -94,7 +97,6 @@ def call(name: str, *args) -> None:
 _setup_done = set()
 # one DRAM sector per random probe (profiles/ r01 showed 64+ B over-fetch);
 # ASH_L2_FETCH=0 leaves the driver default (for A/B measurements)
-import os as _os
 L2_FETCH_BYTES = int(_os.environ.get("ASH_L2_FETCH", "32"))
 
 

@@ -38,6 +38,7 @@ constexpr int kItems = 8;
 constexpr int kTile = kBlock * kItems;  // positions per scan tile
 
 thread_local char g_err[512] = "";
+uint32_t g_stream_hints = 1;
 
 int fail(int code, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -110,6 +111,39 @@ __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
 
 __device__ __forceinline__ int32_t ld_volatile_i32(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+// L2 cache policies: batch streams (keys, values, scratch, outputs) are read
+// or written once, so they are marked evict-first to leave L2 to the table.
+__device__ __forceinline__ uint64_t stream_policy(uint32_t hints) {
+  uint64_t pol;
+  if (hints)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint32_t ld_stream(const void* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ uint8_t ld_stream_u8(const void* p, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return static_cast<uint8_t>(v);
+}
+
+__device__ __forceinline__ void st_stream(void* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void st_stream_u8(void* p, uint8_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(p), "h"(static_cast<uint16_t>(v)),
+               "l"(pol)
+               : "memory");
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -186,7 +220,7 @@ __device__ __forceinline__ Key<A> load_key(const int32_t* keys, int64_t p, int a
 // must call this (before any early exit).
 template <int A>
 __device__ __forceinline__ Key<A> load_key_warp(const int32_t* __restrict__ keys, int64_t p, int64_t n,
-                                                int arity, uint32_t* stage) {
+                                                int arity, uint32_t* stage, uint64_t pol) {
   if (A != 3) {
     Key<A> k;
     if (p < n) k = load_key<A>(keys, p, arity);
@@ -199,7 +233,7 @@ __device__ __forceinline__ Key<A> load_key_warp(const int32_t* __restrict__ keys
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const int w = lane + 32 * r;
-    if (w < words) st[w] = __ldg(reinterpret_cast<const uint32_t*>(keys) + base * 3 + w);
+    if (w < words) st[w] = ld_stream(reinterpret_cast<const uint32_t*>(keys) + base * 3 + w, pol);
   }
   __syncwarp();
   Key<A> k;
@@ -224,10 +258,15 @@ __device__ __forceinline__ uint32_t hash_key(const Key<A>& k, int arity) {
   return fmix32(h);
 }
 
+// home bucket by multiply-shift range reduction (any table size)
+__device__ __forceinline__ uint32_t home_bucket(uint32_t h, uint32_t n_buckets) { return __umulhi(h, n_buckets); }
+__device__ __forceinline__ uint32_t next_bucket(uint32_t b, uint32_t n_buckets) { return b + 1 == n_buckets ? 0 : b + 1; }
+
 struct Table {
   uint4* slots;
-  uint32_t bucket_mask;  // n_buckets - 1 (bucket = 2 slots)
-  uint32_t slot_mask;    // n_slots - 1
+  uint32_t n_buckets;    // n_slots / 2 (bucket = 2 slots = one 32-byte sector)
+  uint32_t n_slots;
+  uint32_t hints;        // 1: streaming traffic marked L2 evict-first
   const int32_t* key_buf;
   int arity;
 };
@@ -235,8 +274,9 @@ struct Table {
 Table make_table(const ash_map_t* m) {
   Table t;
   t.slots = static_cast<uint4*>(m->slots);
-  t.bucket_mask = static_cast<uint32_t>(m->n_slots / 2 - 1);
-  t.slot_mask = static_cast<uint32_t>(m->n_slots - 1);
+  t.n_buckets = static_cast<uint32_t>(m->n_slots / 2);
+  t.n_slots = static_cast<uint32_t>(m->n_slots);
+  t.hints = g_stream_hints;
   t.key_buf = m->key_buf;
   t.arity = m->arity;
   return t;
@@ -269,8 +309,8 @@ __device__ __forceinline__ uint4 slot_value(const Key<A>& k, uint32_t state) {
 template <int A>
 __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, uint32_t h,
                                               uint32_t* slot_out) {
-  uint32_t b = h & t.bucket_mask;
-  for (uint32_t step = 0; step <= t.bucket_mask; ++step) {
+  uint32_t b = home_bucket(h, t.n_buckets);
+  for (uint32_t step = 0; step < t.n_buckets; ++step) {
     uint32_t w[8];
     ld256_nc(t.slots + 2 * static_cast<size_t>(b), w);
 #pragma unroll
@@ -282,7 +322,7 @@ __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, u
         return static_cast<int32_t>(st);
       }
     }
-    b = (b + 1) & t.bucket_mask;
+    b = next_bucket(b, t.n_buckets);
   }
   return -1;
 }
@@ -294,7 +334,7 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
                                                 uint32_t j, const int32_t* batch, uint8_t* mask,
                                                 int32_t* counters, bool* claimed_tomb) {
   const uint32_t me = PEND | j;
-  uint32_t b = h & t.bucket_mask;
+  uint32_t b = home_bucket(h, t.n_buckets);
   int first = 0;
   uint32_t free_slot = EMPTY;
   uint4 free_val = make_uint4(0, 0, 0, 0);
@@ -325,8 +365,8 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
       }
     }
     first = 0;
-    b = (b + 1) & t.bucket_mask;
-    if (++scanned > t.bucket_mask) {
+    b = next_bucket(b, t.n_buckets);
+    if (++scanned >= t.n_buckets) {
       if (free_slot != EMPTY) goto claim;
       atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_TABLE_FULL);
       mask[j] = DEMOTED;
@@ -379,11 +419,12 @@ __global__ void __launch_bounds__(kBlock) k_find(Table t, const int32_t* __restr
                                                  uint8_t* __restrict__ out_mask) {
   __shared__ uint32_t stage[kBlock * 3];
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
-  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage);
+  const uint64_t pol = stream_policy(t.hints);
+  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, pol);
   if (p >= n) return;
   int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), nullptr);
-  out_idx[p] = idx;
-  out_mask[p] = idx >= 0;
+  st_stream(out_idx + p, static_cast<uint32_t>(idx), pol);
+  st_stream_u8(out_mask + p, idx >= 0, pol);
 }
 
 // ---------------------------------------------------------------------------
@@ -408,7 +449,7 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
   if (p == 0) counters[ASH_CTR_WINNERS] = 0;
   const bool valid = p < n;
   const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
-  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage);
+  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, stream_policy(t.hints));
   if (!valid) return;
   // warp pre-aggregation: equal keys in a warp resolve through their lowest
   // lane (= lowest batch position); the rest are duplicate losers or share
@@ -559,6 +600,7 @@ __global__ void __launch_bounds__(kBlock)
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * kTile;
+  const uint64_t pol = stream_policy(t.hints);
   int32_t v[kItems];
   bool win[kItems];
 #pragma unroll
@@ -567,8 +609,8 @@ __global__ void __launch_bounds__(kBlock)
     v[it] = 0;
     win[it] = false;
     if (p < n) {
-      v[it] = tmp[p];
-      win[it] = v[it] < 0 && !(mask[p] & DEMOTED);
+      v[it] = static_cast<int32_t>(ld_stream(tmp + p, pol));
+      win[it] = v[it] < 0 && !(ld_stream_u8(mask + p, pol) & DEMOTED);
     }
   }
   uint32_t bal[kItems];
@@ -579,7 +621,7 @@ __global__ void __launch_bounds__(kBlock)
   int32_t hidx[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it)
-    hidx[it] = win[it] ? __ldg(heap + ts.base + item_rank(sm, bal, it)) : 0;
+    hidx[it] = win[it] ? static_cast<int32_t>(ld_stream(heap + ts.base + item_rank(sm, bal, it), pol)) : 0;
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
@@ -590,19 +632,19 @@ __global__ void __launch_bounds__(kBlock)
       t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
       const int32_t* kr = keys + p * arity;
       int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
-      for (int d = 0; d < arity; ++d) dr[d] = __ldg(kr + d);
+      for (int d = 0; d < arity; ++d) st_stream(dr + d, ld_stream(kr + d, pol), pol);
 #pragma unroll
       for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
         if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
       active[idx] = 1;
-      tmp[p] = idx;
-      mask[p] = 1;
+      st_stream(tmp + p, static_cast<uint32_t>(idx), pol);
+      st_stream_u8(mask + p, 1, pol);
     } else if (v[it] >= 0) {
-      tmp[p] = assoc ? v[it] : -1;
-      mask[p] = assoc ? 1 : 0;
+      st_stream(tmp + p, static_cast<uint32_t>(assoc ? v[it] : -1), pol);
+      st_stream_u8(mask + p, assoc ? 1 : 0, pol);
     } else {
-      tmp[p] = -1;
-      mask[p] = 0;
+      st_stream(tmp + p, 0xFFFFFFFFu, pol);
+      st_stream_u8(mask + p, 0, pol);
     }
   }
   if (tile == gridDim.x - 1 && threadIdx.x == 0) {
@@ -757,12 +799,12 @@ __global__ void __launch_bounds__(kBlock) k_active_compact(const uint8_t* __rest
 
 template <int A>
 __device__ __forceinline__ void insert_unique(const Table& t, const Key<A>& k, uint32_t h, uint32_t state) {
-  uint32_t s = (h & t.bucket_mask) * 2;
+  uint32_t s = home_bucket(h, t.n_buckets) * 2;
   while (true) {
     uint4 cur = ld128_relaxed(t.slots + s);
     if (cur.w == EMPTY && cas128(t.slots + s, cur, slot_value<A>(k, state))) return;
     if (cur.w == EMPTY) continue;  // lost the race on this slot: re-read it
-    s = (s + 1) & t.slot_mask;
+    s = s + 1 == t.n_slots ? 0 : s + 1;
   }
 }
 
@@ -917,8 +959,8 @@ int check_map(const ash_map_t* m) {
   if (!m) return fail(ASH_ERR_INVALID, "null map");
   if (!m->slots || !m->key_buf || !m->heap || !m->active || !m->counters || !m->erase_claim || !m->freed)
     return fail(ASH_ERR_INVALID, "map has a null buffer");
-  if (m->n_slots < 64 || (m->n_slots & (m->n_slots - 1)) || m->n_slots > (int64_t(1) << 30))
-    return fail(ASH_ERR_INVALID, "n_slots must be a power of two in [64, 2^30]");
+  if (m->n_slots < 64 || (m->n_slots & 1) || m->n_slots > (int64_t(1) << 30))
+    return fail(ASH_ERR_INVALID, "n_slots must be even and in [64, 2^30]");
   if (m->arity < 1) return fail(ASH_ERR_INVALID, "arity must be >= 1");
   if (m->capacity < 1 || m->capacity > INT32_MAX) return fail(ASH_ERR_INVALID, "capacity out of range");
   if (m->n_values < 0 || m->n_values > ASH_MAX_VALUE_BUFFERS) return fail(ASH_ERR_INVALID, "too many value buffers");
@@ -974,6 +1016,11 @@ int arity_class(int arity) { return arity <= 3 ? arity : 0; }
 extern "C" {
 
 int ash_abi_version(void) { return ASH_ABI_VERSION; }
+
+int ash_set_stream_hints(int32_t on) {
+  g_stream_hints = on ? 1u : 0u;
+  return ASH_OK;
+}
 
 int ash_device_setup(int32_t l2_fetch_bytes) {
   if (l2_fetch_bytes < 0 || l2_fetch_bytes > 128 || (l2_fetch_bytes & (l2_fetch_bytes - 1)))
@@ -1124,7 +1171,7 @@ int ash_rehash_from(ash_map_t* dst, const ash_map_t* src, const int32_t* act, in
 
 int ash_rebuild_table(ash_map_t* m, void* new_slots, int64_t new_n_slots, void* stream) {
   if (int rc = check_map(m)) return rc;
-  if (!new_slots || new_n_slots < 64 || (new_n_slots & (new_n_slots - 1)) || new_n_slots > (int64_t(1) << 30))
+  if (!new_slots || new_n_slots < 64 || (new_n_slots & 1) || new_n_slots > (int64_t(1) << 30))
     return fail(ASH_ERR_INVALID, "bad new table");
   cudaStream_t s = as_stream(stream);
   unsigned g = grid_for(new_n_slots, kBlock);
@@ -1166,7 +1213,7 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
   if (int rc = check_batch(n)) return rc;
   if (!(voxel > 0)) return fail(ASH_ERR_INVALID, "voxel size must be > 0");
-  if (ws->n_slots < 2 * n || (ws->n_slots & (ws->n_slots - 1))) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (ws->n_slots < n + n / 4 + 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_scan(ws, n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);

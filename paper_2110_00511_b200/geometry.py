@@ -89,7 +89,7 @@ class _VoxelWorkspace:
             return ws
 
     def reserve(self, n: int) -> None:
-        need = _table_slots(max(n, 1))
+        need = _table_slots(max(n, 1), 2.0)
         if need > self.n_slots:
             self.slots = torch.empty(need * 4, dtype=torch.int32, device=self.device)
             self.n_slots = need

@@ -21,6 +21,8 @@ Differences in mechanism (not in results):
 """
 from __future__ import annotations
 
+import math
+import os
 import threading
 from contextlib import contextmanager
 from dataclasses import dataclass
@@ -182,13 +184,16 @@ def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _table_slots(capacity: int) -> int:
-    """Power-of-two slot count with live load factor <= 0.5."""
-    n = 64
-    while n < 2 * capacity:
-        n *= 2
+TABLE_FACTOR = float(os.environ.get("ASH_TABLE_FACTOR", "2.0"))
+
+
+def _table_slots(capacity: int, factor: float = None) -> int:
+    """Even slot count = factor x capacity (live load factor <= 1/factor)."""
+    f = TABLE_FACTOR if factor is None else factor
+    n = max(64, int(math.ceil(capacity * f)))
+    n += n & 1
     if n > 1 << 30:
-        raise ValueError(f"capacity {capacity} exceeds the single-map limit (2^29)")
+        raise ValueError(f"capacity {capacity} exceeds the single-map table limit (2^30 slots)")
     return n
 
 
