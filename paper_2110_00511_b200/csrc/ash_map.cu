@@ -124,26 +124,41 @@ __device__ __forceinline__ uint64_t stream_policy(uint32_t hints) {
   return pol;
 }
 
+// Stream loads are pure (non-volatile, no clobber) so the compiler can hoist
+// them above earlier stores; they only ever read data this kernel does not
+// write before reading it.  Stores stay volatile (ordered among themselves).
 __device__ __forceinline__ uint32_t ld_stream(const void* p, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 
 __device__ __forceinline__ uint8_t ld_stream_u8(const void* p, uint64_t pol) {
   uint16_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
   return static_cast<uint8_t>(v);
 }
 
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p, uint64_t pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ void st_stream(void* p, uint32_t v, uint64_t pol) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol));
+}
+
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol));
 }
 
 __device__ __forceinline__ void st_stream_u8(void* p, uint8_t v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(p), "h"(static_cast<uint16_t>(v)),
-               "l"(pol)
-               : "memory");
+               "l"(pol));
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -355,6 +370,10 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
         if (st == EMPTY) goto claim;
       } else if (slot_matches<A>(w + 4 * s, st, k, t, batch)) {
         if (st < PEND) return st;  // already present
+        if (st < me) {  // a lower position already holds it: certain loser, no atomic
+          mask[j] = DEMOTED;
+          return PEND | slot;
+        }
         const uint32_t old = atomicMin(&t.slots[slot].w, me);
         if (old < me) {
           mask[j] = DEMOTED;  // a lower position holds the key
@@ -591,7 +610,43 @@ struct ValueArgs {
   int64_t rb[ASH_MAX_VALUE_BUFFERS];
 };
 
-template <int A>
+// Row of VW 32-bit words (VW in {1,2,3,4,8}): one value buffer whose rows
+// are register-sized, so the commit can load every winner's row before it
+// stores any (the generic copy_row path interleaves load and store per row).
+template <int VW>
+struct RowWords {
+  uint32_t w[VW];
+};
+
+template <int VW>
+__device__ __forceinline__ void load_row(RowWords<VW>& r, const uint8_t* src, uint64_t pol) {
+  if (VW % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < VW / 4; ++i) {
+      uint4 q = ld_stream_v4(src + 16 * i, pol);
+      r.w[4 * i] = q.x, r.w[4 * i + 1] = q.y, r.w[4 * i + 2] = q.z, r.w[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VW; ++i) r.w[i] = ld_stream(src + 4 * i, pol);
+  }
+}
+
+template <int VW>
+__device__ __forceinline__ void store_row(uint8_t* dst, const RowWords<VW>& r, uint64_t pol) {
+  if (VW % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < VW / 4; ++i)
+      st_stream_v4(dst + 16 * i, make_uint4(r.w[4 * i], r.w[4 * i + 1], r.w[4 * i + 2], r.w[4 * i + 3]), pol);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VW; ++i) st_stream(dst + 4 * i, r.w[i], pol);
+  }
+}
+
+// VW > 0: exactly one value buffer with VW-word rows (register fast path);
+// VW == 0: no value rows; VW < 0: generic rows via copy_row.
+template <int A, int VW>
 __global__ void __launch_bounds__(kBlock)
     k_commit(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
@@ -616,12 +671,23 @@ __global__ void __launch_bounds__(kBlock)
   uint32_t bal[kItems];
   TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, counters + ASH_CTR_TOP);
   const int arity = A ? A : t.arity;
-  // issue every winner's heap load before any store (they are independent;
-  // stores to the table would otherwise serialise them)
+  // phase 1: every load of every winner (heap index, key words, value row)
+  // before any store, so each thread keeps kItems x several loads in flight
   int32_t hidx[kItems];
+  uint32_t kw[kItems][3];
+  RowWords<(VW > 0 ? VW : 1)> row[kItems];
 #pragma unroll
-  for (int it = 0; it < kItems; ++it)
-    hidx[it] = win[it] ? static_cast<int32_t>(ld_stream(heap + ts.base + item_rank(sm, bal, it), pol)) : 0;
+  for (int it = 0; it < kItems; ++it) {
+    if (!win[it]) continue;
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    hidx[it] = static_cast<int32_t>(ld_stream(heap + ts.base + item_rank(sm, bal, it), pol));
+    const int32_t* kr = keys + p * arity;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (A == 0 || d < A) kw[it][d] = ld_stream(kr + d, pol);
+    if (VW > 0) load_row<(VW > 0 ? VW : 1)>(row[it], va.src[0] + p * (VW > 0 ? VW : 1) * 4, pol);
+  }
+  // phase 2: stores
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
@@ -630,12 +696,19 @@ __global__ void __launch_bounds__(kBlock)
       const int32_t idx = hidx[it];
       const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
       t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
-      const int32_t* kr = keys + p * arity;
       int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
-      for (int d = 0; d < arity; ++d) st_stream(dr + d, ld_stream(kr + d, pol), pol);
 #pragma unroll
-      for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
-        if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
+      for (int d = 0; d < 3; ++d)
+        if (A == 0 || d < A) st_stream(dr + d, kw[it][d], pol);
+      if (A == 0)
+        for (int d = 3; d < arity; ++d) st_stream(dr + d, ld_stream(keys + p * arity + d, pol), pol);
+      if (VW > 0) {
+        store_row<(VW > 0 ? VW : 1)>(va.dst[0] + static_cast<int64_t>(idx) * (VW > 0 ? VW : 1) * 4, row[it], pol);
+      } else if (VW < 0) {
+#pragma unroll
+        for (int b = 0; b < ASH_MAX_VALUE_BUFFERS; ++b)
+          if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
+      }
       active[idx] = 1;
       st_stream(tmp + p, static_cast<uint32_t>(idx), pol);
       st_stream_u8(mask + p, 1, pol);
@@ -1099,9 +1172,27 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
   ValueArgs va = value_args(m, values);
   uint32_t ep = next_epoch(m);
   cudaStream_t s = as_stream(stream);
-  ASH_DISPATCH_ARITY(m->arity, (k_commit<A><<<grid_for(n, kTile), kBlock, 0, s>>>(
-                                   t, keys, n, va, association, out_idx, out_mask, m->heap, m->active,
-                                   m->key_buf, m->counters, m->scan_status, ep)));
+  int vw = -1;  // value-row dispatch (see k_commit)
+  if (va.n == 0) {
+    vw = 0;
+  } else if (va.n == 1 && va.rb[0] % 4 == 0) {
+    const int64_t w = va.rb[0] / 4;
+    if (w == 1 || w == 2 || w == 3 || w == 4 || w == 8) vw = static_cast<int>(w);
+  }
+#define ASH_COMMIT(VW_)                                                                                   \
+  ASH_DISPATCH_ARITY(m->arity, (k_commit<A, VW_><<<grid_for(n, kTile), kBlock, 0, s>>>(                  \
+                                   t, keys, n, va, association, out_idx, out_mask, m->heap, m->active, \
+                                   m->key_buf, m->counters, m->scan_status, ep)))
+  switch (vw) {
+    case 0: ASH_COMMIT(0); break;
+    case 1: ASH_COMMIT(1); break;
+    case 2: ASH_COMMIT(2); break;
+    case 3: ASH_COMMIT(3); break;
+    case 4: ASH_COMMIT(4); break;
+    case 8: ASH_COMMIT(8); break;
+    default: ASH_COMMIT(-1); break;
+  }
+#undef ASH_COMMIT
   return check_launch("ash_insert_commit");
 }
 
