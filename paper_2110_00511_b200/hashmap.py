@@ -184,7 +184,9 @@ def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-TABLE_FACTOR = float(os.environ.get("ASH_TABLE_FACTOR", "2.0"))
+# slots per unit of capacity (max live load 1/1.5); chosen by the r01 A/B
+# matrix (tools/exp_matrix.sh): 1.5 beat 2.0 and 1.25 on the C2 sweep
+TABLE_FACTOR = float(os.environ.get("ASH_TABLE_FACTOR", "1.5"))
 
 
 def _table_slots(capacity: int, factor: float = None) -> int:
