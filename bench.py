@@ -232,7 +232,7 @@ def gpu_single(args, torch, dev):
 
     # per-kernel split (same workload): claim / commit / find, CUDA events on
     # the launching stream
-    kern = {"claim": [], "commit": [], "find": []}
+    kern = {"claim": [], "tile_scan": [], "commit": [], "find": []}
     for _ in range(5):
         m.clear()
         l2_flush(torch, flush)
@@ -240,22 +240,25 @@ def gpu_single(args, torch, dev):
         msk = torch.empty(N_KEYS, dtype=torch.uint8, device=dev)
         vptr = (_lib.c_void_p * 1)(vals.data_ptr())
         m._ensure_scan(N_KEYS)
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         e[0].record(stream)
         _lib.call("ash_insert_claim", m._ptr(), keys.data_ptr(), N_KEYS, idx.data_ptr(), msk.data_ptr(), m._stream())
         e[1].record(stream)
-        _lib.call("ash_insert_commit", m._ptr(), keys.data_ptr(), N_KEYS, vptr, 0, idx.data_ptr(), msk.data_ptr(), m._stream())
+        _lib.call("ash_insert_count", m._ptr(), N_KEYS, idx.data_ptr(), msk.data_ptr(), m._stream())
         e[2].record(stream)
+        _lib.call("ash_insert_commit", m._ptr(), keys.data_ptr(), N_KEYS, vptr, 0, idx.data_ptr(), msk.data_ptr(), m._stream())
+        e[3].record(stream)
         m._size_known = False
         l2_flush(torch, flush)
-        e3 = torch.cuda.Event(enable_timing=True)
-        e3.record(stream)
+        e4 = torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
         m.find(keys)
-        e[3].record(stream)
+        e[4].record(stream)
         torch.cuda.synchronize()
         kern["claim"].append(e[0].elapsed_time(e[1]))
-        kern["commit"].append(e[1].elapsed_time(e[2]))
-        kern["find"].append(e3.elapsed_time(e[3]))
+        kern["tile_scan"].append(e[1].elapsed_time(e[2]))
+        kern["commit"].append(e[2].elapsed_time(e[3]))
+        kern["find"].append(e4.elapsed_time(e[4]))
     kms = {k: statistics.median(v) for k, v in kern.items()}
 
     # e2e: public API with pinned host buffers; H2D of inputs and D2H of the
@@ -285,7 +288,7 @@ def gpu_single(args, torch, dev):
 
     sweep = run_sweep(torch, dev, ash, flush)
     return dict(ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
-                sweep=sweep, launches_per_step=3)
+                sweep=sweep, launches_per_step=4)
 
 
 def run_sweep(torch, dev, ash, flush):
@@ -378,6 +381,7 @@ def main():
         "claim": (12 + 32 + 5) * N_KEYS,                    # key, table sector, scratch idx+mask
         "commit": (5 + 5) * N_KEYS + RHO * (12 + 2 * 4 + 32) * N_KEYS,  # scratch in, out; winner rows + slot
         "find": algorithmic_bytes("find", RHO, 4) * N_KEYS,
+        "tile_scan": 4 * 2 * (N_KEYS / 2048),
     }
     dom = max(kms, key=kms.get)
     achieved = per_kernel_bytes[dom] / (kms[dom] / 1e3) / 1e9
@@ -398,7 +402,7 @@ def main():
                      "kernel_ms": {k: round(v, 4) for k, v in kms.items()}},
         "op_roofline": {
             "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS /
-                                 ((kms["claim"] + kms["commit"]) / 1e3) / 1e9 / bw, 4),
+                                 ((kms["claim"] + kms["tile_scan"] + kms["commit"]) / 1e3) / 1e9 / bw, 4),
             "find_frac": round(per_kernel_bytes["find"] / (kms["find"] / 1e3) / 1e9 / bw, 4)},
         "e2e": {"value": round(2 * N_KEYS / (res["e2e_ms"] / 1e3) / 1e6, 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},

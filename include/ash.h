@@ -43,6 +43,7 @@ extern "C" {
 #define ASH_CTR_ERASED 3   /* keys removed by the last erase               */
 #define ASH_CTR_FLAGS 4    /* sticky error bits, see ASH_FLAG_*            */
 #define ASH_CTR_COUNT 5    /* result count of the last compaction/voxelize */
+#define ASH_CTR_TOP_BASE 6 /* heap top at the start of the current commit   */
 #define ASH_N_COUNTERS 8
 
 #define ASH_FLAG_TABLE_FULL 1  /* a probe wrapped the whole table */
@@ -70,6 +71,8 @@ typedef struct ash_map {
   int32_t* counters;        /* ASH_N_COUNTERS                                  */
   uint64_t* scan_status;    /* single-pass scan tile status, zeroed once       */
   int64_t scan_status_len;  /* >= ash_scan_tiles(max(n, capacity))             */
+  int32_t* tile_counts;     /* per-2048-position winner counts, zero between   */
+  int64_t tile_counts_len;  /* batches; >= ash_scan_tiles(n)                   */
   int64_t capacity;         /* <= 2^31 - 1                                     */
   uint32_t epoch;           /* scan epoch; the library bumps it per launch     */
   uint32_t reserved;
@@ -106,15 +109,17 @@ int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx,
  * value_row_bytes each, batch order) or is NULL for activate/HashSet.
  * association != 0 gives activate masks (found OR winner).
  * Precondition: capacity - size >= n (the caller checks; otherwise use the
- * claim/count/commit|rollback sequence below). */
+ * claim/count/commit|rollback sequence below).  ash_insert = claim + count +
+ * commit. */
 int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n,
                const void* const* values, int32_t association,
                int32_t* out_idx, uint8_t* out_mask, void* stream);
 
 /* Split form of ash_insert for the capacity-uncertain path
  * (hashmap.py:389-396 re-plan on growth, :317-324 CapacityError):
- *   claim -> count (counters[WINNERS]) -> host reads the count ->
- *   commit when it fits, else rollback (map unchanged). */
+ *   claim -> count (counters[WINNERS]; scans the per-tile winner counts the
+ *   claim kept) -> host reads the count -> commit when it fits, else
+ *   rollback (map unchanged).  commit requires the preceding count. */
 int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n,
                      int32_t* out_idx, uint8_t* out_mask, void* stream);
 int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx,

@@ -13,7 +13,7 @@ from .build import LIB_PATH
 
 ASH_OK, ASH_ERR_INVALID, ASH_ERR_CAPACITY, ASH_ERR_CUDA = 0, 1, 2, 3
 MAX_VALUE_BUFFERS = 8
-CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT = 0, 1, 2, 3, 4, 5
+CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT, CTR_TOP_BASE = 0, 1, 2, 3, 4, 5, 6
 N_COUNTERS = 8
 FLAG_TABLE_FULL, FLAG_RANGE = 1, 2
 TILE = 2048  # positions per scan tile (csrc kTile)
@@ -28,7 +28,8 @@ class AshMap(ctypes.Structure):
         ("value_row_bytes", c_int64 * MAX_VALUE_BUFFERS),
         ("heap", c_void_p), ("active", c_void_p), ("erase_claim", c_void_p),
         ("freed", c_void_p), ("counters", c_void_p), ("scan_status", c_void_p),
-        ("scan_status_len", c_int64), ("capacity", c_int64),
+        ("scan_status_len", c_int64), ("tile_counts", c_void_p), ("tile_counts_len", c_int64),
+        ("capacity", c_int64),
         ("epoch", c_uint32), ("reserved", c_uint32),
     ]
 

@@ -347,7 +347,8 @@ __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, u
 template <int A>
 __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k, uint32_t h,
                                                 uint32_t j, const int32_t* batch, uint8_t* mask,
-                                                int32_t* counters, bool* claimed_tomb) {
+                                                int32_t* counters, int32_t* tile_cnt, bool* claimed_tomb,
+                                                bool* candidate) {
   const uint32_t me = PEND | j;
   uint32_t b = home_bucket(h, t.n_buckets);
   int first = 0;
@@ -379,6 +380,8 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
           mask[j] = DEMOTED;  // a lower position holds the key
         } else {
           mask[old & ~PEND] = DEMOTED;  // we displaced a higher position
+          atomicSub(&tile_cnt[(old & ~PEND) / kTile], 1);
+          *candidate = true;
         }
         return PEND | slot;
       }
@@ -395,6 +398,7 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
   claim:
     if (cas128(t.slots + free_slot, free_val, slot_value<A>(k, me))) {
       *claimed_tomb = (free_val.w == TOMB);
+      *candidate = true;
       return PEND | CLAIMER | free_slot;
     }
     // lost the race for free_slot: everything before it is unchanged, so
@@ -461,27 +465,40 @@ __device__ __forceinline__ bool same_key_in_warp(const Key<A>& k, unsigned live,
 template <int A>
 __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                                  int32_t* counters) {
+                                                  int32_t* counters, int32_t* tile_cnt) {
   __shared__ uint32_t stage[kBlock * 3];
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  if (p == 0) counters[ASH_CTR_WINNERS] = 0;
   const bool valid = p < n;
   const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
   Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, stream_policy(t.hints));
   if (!valid) return;
+  const uint32_t h = hash_key<A>(k, t.arity);
   // warp pre-aggregation: equal keys in a warp resolve through their lowest
   // lane (= lowest batch position); the rest are duplicate losers or share
-  // the leader's found index (hashmap.py:125-131 first-occurrence rule)
+  // the leader's found index (hashmap.py:125-131 first-occurrence rule).
+  // One match on the hash first; the exact word matches only run when some
+  // lanes share a hash.
   unsigned grp = 1u << lane;
-  if (A != 0) same_key_in_warp<A>(k, live, &grp);
+  if (A != 0) {
+    grp = __match_any_sync(live, h);
+    if (__any_sync(live, __popc(grp) > 1)) {
+      unsigned g2;
+      same_key_in_warp<A>(k, live, &g2);
+      grp &= g2;
+    }
+  }
   const int leader = __ffs(grp) - 1;
   uint32_t res = 0;
-  bool claimed_tomb = false;
+  bool claimed_tomb = false, candidate = false;
   if (lane == leader)
-    res = probe_claim<A>(t, k, hash_key<A>(k, t.arity), static_cast<uint32_t>(p), keys, mask, counters,
-                         &claimed_tomb);
+    res = probe_claim<A>(t, k, h, static_cast<uint32_t>(p), keys, mask, counters, tile_cnt, &claimed_tomb,
+                         &candidate);
   __syncwarp(live);
+  // exact per-tile winner counts: +1 per candidate (displaced ones were
+  // decremented by their displacer), so no look-back scan is needed later
+  const unsigned cand = __ballot_sync(live, candidate);
+  if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
   const uint32_t lres = __shfl_sync(live, res, leader);
   if (lane == leader) {
     tmp[p] = static_cast<int32_t>(res);
@@ -600,6 +617,85 @@ __device__ __forceinline__ uint32_t item_rank(const ScanSmem& sm, const uint32_t
   return sm.prefix + sm.pre[it * kWarps + warp] + __popc(bal[it] & lanemask_lt());
 }
 
+// Tile scan whose tile prefix is already known (from k_tile_scan): ballots and
+// per-(item, warp) offsets only, one barrier, no cross-tile wait.  Thread 0
+// takes the prefix and clears the count for the next batch.
+__device__ __forceinline__ void tile_scan_known(const bool (&flag)[kItems], uint32_t (&bal)[kItems], ScanSmem& sm,
+                                                int32_t* tile_pre, int64_t tile, const int32_t* base_src) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    sm.prefix = static_cast<uint32_t>(tile_pre[tile]);
+    tile_pre[tile] = 0;
+    sm.base = base_src ? static_cast<uint32_t>(ld_volatile_i32(base_src)) : 0u;
+  }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    bal[it] = __ballot_sync(0xFFFFFFFFu, flag[it]);
+    if (lane == 0) sm.cnt[it * kWarps + warp] = __popc(bal[it]);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t e0 = sm.cnt[2 * lane], e1 = sm.cnt[2 * lane + 1];
+    uint32_t incl = e0 + e1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - e0 - e1;
+    sm.pre[2 * lane] = excl;
+    sm.pre[2 * lane + 1] = excl + e0;
+    if (lane == 31) sm.total = incl;
+  }
+  __syncthreads();
+}
+
+// Exclusive scan of per-tile counts in place (one block; the tile count is
+// small: n / 2048).  Records the heap top the commit starts from and the
+// batch's winner total (what the capacity check needs).
+constexpr int kScanBlock = 1024;
+
+__global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int64_t n_tiles, int32_t* counters,
+                                                          int top_slot, int total_slot) {
+  __shared__ int32_t warp_tot[kScanBlock / 32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n_tiles; base += kScanBlock) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t x = i < n_tiles ? tile_cnt[i] : 0;
+    int32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = warp_tot[lane];
+      int32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const int32_t c = carry;
+    if (i < n_tiles) tile_cnt[i] = c + warp_tot[warp] + incl - x;
+    __syncthreads();
+    if (threadIdx.x == kScanBlock - 1) carry = c + warp_tot[warp] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (top_slot >= 0) counters[top_slot] = counters[ASH_CTR_TOP];
+    counters[total_slot] = carry;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // kernels: insert / activate commit (winner rank -> heap index -> rows)
 
@@ -651,7 +747,7 @@ __global__ void __launch_bounds__(kBlock)
     k_commit(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
              uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
-             uint64_t* status, uint32_t epoch) {
+             int32_t* tile_pre) {
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * kTile;
@@ -669,7 +765,7 @@ __global__ void __launch_bounds__(kBlock)
     }
   }
   uint32_t bal[kItems];
-  TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, counters + ASH_CTR_TOP);
+  tile_scan_known(win, bal, sm, tile_pre, tile, counters + ASH_CTR_TOP_BASE);
   const int arity = A ? A : t.arity;
   // phase 1: every load of every winner (heap index, key words, value row)
   // before any store, so each thread keeps kItems x several loads in flight
@@ -680,7 +776,7 @@ __global__ void __launch_bounds__(kBlock)
   for (int it = 0; it < kItems; ++it) {
     if (!win[it]) continue;
     const int64_t p = base + it * kBlock + threadIdx.x;
-    hidx[it] = static_cast<int32_t>(ld_stream(heap + ts.base + item_rank(sm, bal, it), pol));
+    hidx[it] = static_cast<int32_t>(ld_stream(heap + sm.base + item_rank(sm, bal, it), pol));
     const int32_t* kr = keys + p * arity;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -720,11 +816,10 @@ __global__ void __launch_bounds__(kBlock)
       st_stream_u8(mask + p, 0, pol);
     }
   }
-  if (tile == gridDim.x - 1 && threadIdx.x == 0) {
-    const uint32_t total = ts.prefix + ts.total;
-    counters[ASH_CTR_TOP] = static_cast<int32_t>(ts.base + total);
-    counters[ASH_CTR_WINNERS] = static_cast<int32_t>(total);
-  }
+  // nobody reads TOP during the commit (tiles use TOP_BASE), so any tile may
+  // publish the new top
+  if (tile == 0 && threadIdx.x == 0)
+    counters[ASH_CTR_TOP] = static_cast<int32_t>(sm.base) + ld_volatile_i32(counters + ASH_CTR_WINNERS);
 }
 
 // Block-wide count of a predicate accumulated into *ctr with one atomic per
@@ -740,32 +835,12 @@ __device__ __forceinline__ void block_count_add(bool pred, int32_t* ctr) {
   if (threadIdx.x == 0 && s_cnt) atomicAdd(ctr, s_cnt);
 }
 
-constexpr int kCountItems = 16;  // positions per thread in the counting kernels
-
-__global__ void __launch_bounds__(kBlock) k_count_winners(const int32_t* __restrict__ tmp,
-                                                          const uint8_t* __restrict__ mask, int64_t n,
-                                                          int32_t* counters) {
-  int cnt = 0;
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kBlock) * kCountItems + threadIdx.x;
-#pragma unroll 4
-  for (int it = 0; it < kCountItems; ++it) {
-    const int64_t p = base + it * kBlock;
-    cnt += (p < n && tmp[p] < 0 && !(mask[p] & DEMOTED));
-  }
-  __shared__ int32_t s_cnt;
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  const int w = __reduce_add_sync(0xFFFFFFFFu, cnt);
-  if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_cnt, w);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_cnt) atomicAdd(&counters[ASH_CTR_WINNERS], s_cnt);
-}
-
 __global__ void __launch_bounds__(kBlock) k_rollback(uint4* slots, const int32_t* __restrict__ tmp, int64_t n,
-                                                     int32_t* counters) {
+                                                     int32_t* counters, int32_t* tile_cnt) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   bool claimed = false;
   if (p < n) {
+    if (p % kTile == 0) tile_cnt[p / kTile] = 0;  // ready for the next batch
     const uint32_t v = static_cast<uint32_t>(tmp[p]);
     // a claimed slot reverts to TOMBSTONE: probe chains through it stay intact
     if ((v & PEND) && (v & CLAIMER)) {
@@ -946,7 +1021,8 @@ __global__ void k_quantize(const T* __restrict__ pts, int64_t n, double cell, in
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __restrict__ pts, int64_t n,
                                                         double cell, int32_t* __restrict__ tmp,
-                                                        uint8_t* __restrict__ mask, int32_t* counters) {
+                                                        uint8_t* __restrict__ mask, int32_t* counters,
+                                                        int32_t* tile_cnt) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool valid = p < n;
@@ -958,19 +1034,26 @@ __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __rest
 #pragma unroll
   for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(pts[3 * p + d], cell, &bad));
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
-  unsigned grp;
-  same_key_in_warp<3>(k, live, &grp);
+  const uint32_t h = hash_key<3>(k, 3);
+  unsigned grp = __match_any_sync(live, h);
+  if (__any_sync(live, __popc(grp) > 1)) {
+    unsigned g2;
+    same_key_in_warp<3>(k, live, &g2);
+    grp &= g2;
+  }
   // out-of-range points never claim; the host raises before using results
   const unsigned bad_lanes = __ballot_sync(live, bad);
   grp &= ~bad_lanes;
   if (bad) grp = 1u << lane;
   const int leader = __ffs(grp) - 1;
   uint32_t res = PEND;
-  bool claimed_tomb = false;
+  bool claimed_tomb = false, candidate = false;
   if (lane == leader && !bad)
-    res = probe_claim<3>(t, k, hash_key<3>(k, 3), static_cast<uint32_t>(p), nullptr, mask, counters,
-                         &claimed_tomb);
+    res = probe_claim<3>(t, k, h, static_cast<uint32_t>(p), nullptr, mask, counters, tile_cnt, &claimed_tomb,
+                         &candidate);
   __syncwarp(live);
+  const unsigned cand = __ballot_sync(live, candidate);
+  if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
   if (lane == leader && !bad) {
     tmp[p] = static_cast<int32_t>(res);
   } else {
@@ -983,8 +1066,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
     k_voxel_select(uint4* slots, const T* __restrict__ pts, int64_t n, double cell,
                    const int32_t* __restrict__ tmp, const uint8_t* __restrict__ mask,
-                   int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel, int32_t* counters,
-                   uint64_t* status, uint32_t epoch) {
+                   int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel, int32_t* tile_pre) {
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x, base = tile * kTile;
   int32_t v[kItems];
@@ -1000,7 +1082,7 @@ __global__ void __launch_bounds__(kBlock)
     }
   }
   uint32_t bal[kItems];
-  TileScan ts = tile_scan(win, bal, sm, status, tile, epoch, nullptr);
+  tile_scan_known(win, bal, sm, tile_pre, tile, nullptr);
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     if (!win[it]) continue;
@@ -1013,7 +1095,6 @@ __global__ void __launch_bounds__(kBlock)
     // leave the workspace table EMPTY for the next call
     slots[static_cast<uint32_t>(v[it]) & SLOT_MASK] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
   }
-  if (tile == gridDim.x - 1 && threadIdx.x == 0) counters[ASH_CTR_COUNT] = static_cast<int32_t>(ts.prefix + ts.total);
 }
 
 // ---------------------------------------------------------------------------
@@ -1044,6 +1125,16 @@ int check_batch(int64_t n) {
   if (n < 0) return fail(ASH_ERR_INVALID, "negative batch length");
   if (n >= int64_t(SLOT_MASK)) return fail(ASH_ERR_INVALID, "batch too long (>= 2^30 - 1)");
   return ASH_OK;
+}
+
+int check_tiles(const ash_map_t* m, int64_t n) {
+  if (!m->tile_counts || m->tile_counts_len < tiles_for(n))
+    return fail(ASH_ERR_INVALID, "tile count workspace too small");
+  return ASH_OK;
+}
+
+void launch_tile_scan(const ash_map_t* m, int64_t n, int top_slot, int total_slot, cudaStream_t s) {
+  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot);
 }
 
 int check_scan(const ash_map_t* m, int64_t n) {
@@ -1147,8 +1238,9 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   Table t = make_table(m);
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(out_mask, 0, n, s);
+  if (int rc = check_tiles(m, n)) return rc;
   ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
-                                                                                 m->counters)));
+                                                                                 m->counters, m->tile_counts)));
   return check_launch("ash_insert_claim");
 }
 
@@ -1156,9 +1248,14 @@ int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   cudaStream_t s = as_stream(stream);
-  cudaMemsetAsync(m->counters + ASH_CTR_WINNERS, 0, sizeof(int32_t), s);
-  if (n > 0)
-    k_count_winners<<<grid_for(n, kBlock * kCountItems), kBlock, 0, s>>>(out_idx, out_mask, n, m->counters);
+  if (n == 0) {
+    cudaMemsetAsync(m->counters + ASH_CTR_WINNERS, 0, sizeof(int32_t), s);
+    return check_launch("ash_insert_count");
+  }
+  if (int rc = check_tiles(m, n)) return rc;
+  (void)out_idx;
+  (void)out_mask;
+  launch_tile_scan(m, n, ASH_CTR_TOP_BASE, ASH_CTR_WINNERS, s);
   return check_launch("ash_insert_count");
 }
 
@@ -1167,10 +1264,9 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
-  if (int rc = check_scan(m, n)) return rc;
+  if (int rc = check_tiles(m, n)) return rc;
   Table t = make_table(m);
   ValueArgs va = value_args(m, values);
-  uint32_t ep = next_epoch(m);
   cudaStream_t s = as_stream(stream);
   int vw = -1;  // value-row dispatch (see k_commit)
   if (va.n == 0) {
@@ -1182,7 +1278,7 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
 #define ASH_COMMIT(VW_)                                                                                   \
   ASH_DISPATCH_ARITY(m->arity, (k_commit<A, VW_><<<grid_for(n, kTile), kBlock, 0, s>>>(                  \
                                    t, keys, n, va, association, out_idx, out_mask, m->heap, m->active, \
-                                   m->key_buf, m->counters, m->scan_status, ep)))
+                                   m->key_buf, m->counters, m->tile_counts)))
   switch (vw) {
     case 0: ASH_COMMIT(0); break;
     case 1: ASH_COMMIT(1); break;
@@ -1199,6 +1295,7 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
 int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values, int32_t association,
                int32_t* out_idx, uint8_t* out_mask, void* stream) {
   if (int rc = ash_insert_claim(m, keys, n, out_idx, out_mask, stream)) return rc;
+  if (int rc = ash_insert_count(m, n, out_idx, out_mask, stream)) return rc;
   return ash_insert_commit(m, keys, n, values, association, out_idx, out_mask, stream);
 }
 
@@ -1206,8 +1303,9 @@ int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* s
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
+  if (int rc = check_tiles(m, n)) return rc;
   k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n,
-                                                                    m->counters);
+                                                                    m->counters, m->tile_counts);
   return check_launch("ash_insert_rollback");
 }
 
@@ -1305,23 +1403,26 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   if (int rc = check_batch(n)) return rc;
   if (!(voxel > 0)) return fail(ASH_ERR_INVALID, "voxel size must be > 0");
   if (ws->n_slots < n + n / 4 + 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
-  if (int rc = check_scan(ws, n)) return rc;
+  if (int rc = check_tiles(ws, n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
   if (n == 0) return check_launch("ash_voxelize");
   cudaMemsetAsync(scratch_mask, 0, n, s);
   Table t = make_table(ws);
-  uint32_t ep = next_epoch(ws);
   if (points_are_f64) {
     const double* p = static_cast<const double*>(points);
-    k_voxel_claim<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask, ws->counters);
+    k_voxel_claim<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask,
+                                                                ws->counters, ws->tile_counts);
+    launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
     k_voxel_select<double><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
-                                                                 out_coords, out_sel, ws->counters, ws->scan_status, ep);
+                                                                 out_coords, out_sel, ws->tile_counts);
   } else {
     const float* p = static_cast<const float*>(points);
-    k_voxel_claim<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask, ws->counters);
+    k_voxel_claim<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask,
+                                                               ws->counters, ws->tile_counts);
+    launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
     k_voxel_select<float><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
-                                                                out_coords, out_sel, ws->counters, ws->scan_status, ep);
+                                                                out_coords, out_sel, ws->tile_counts);
   }
   return check_launch("ash_voxelize");
 }

@@ -101,6 +101,9 @@ class _VoxelWorkspace:
             self.scan = torch.zeros(tiles, dtype=torch.int64, device=self.device)
             self.struct.scan_status = self.scan.data_ptr()
             self.struct.scan_status_len = tiles
+            self.tiles = torch.zeros(tiles, dtype=torch.int32, device=self.device)
+            self.struct.tile_counts = self.tiles.data_ptr()
+            self.struct.tile_counts_len = tiles
 
 
 def voxel_downsample(points, voxel_size: float, backend: str = "generic", threads: int = 1,

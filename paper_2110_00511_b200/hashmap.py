@@ -286,6 +286,11 @@ class HashMap:
                                      device=self._device)
             self._struct.scan_status = self._scan.data_ptr()
             self._struct.scan_status_len = self._scan.numel()
+            # per-tile winner counts: zero between batches (the commit or the
+            # rollback clears what the claim counted)
+            self._tiles = torch.zeros(self._scan.numel(), dtype=torch.int32, device=self._device)
+            self._struct.tile_counts = self._tiles.data_ptr()
+            self._struct.tile_counts_len = self._tiles.numel()
 
     def _ptr(self):
         return _lib.ctypes.byref(self._struct)
