@@ -753,17 +753,17 @@ __global__ void __launch_bounds__(kBlock)
   const int64_t base = tile * kTile;
   const uint64_t pol = stream_policy(t.hints);
   int32_t v[kItems];
+  uint8_t mk[kItems];
   bool win[kItems];
+  // all 2 x kItems loads are independent: issue them before any test
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    v[it] = 0;
-    win[it] = false;
-    if (p < n) {
-      v[it] = static_cast<int32_t>(ld_stream(tmp + p, pol));
-      win[it] = v[it] < 0 && !(ld_stream_u8(mask + p, pol) & DEMOTED);
-    }
+    v[it] = p < n ? static_cast<int32_t>(ld_stream(tmp + p, pol)) : 0;
+    mk[it] = p < n ? ld_stream_u8(mask + p, pol) : DEMOTED;
   }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) win[it] = v[it] < 0 && !(mk[it] & DEMOTED);
   uint32_t bal[kItems];
   tile_scan_known(win, bal, sm, tile_pre, tile, counters + ASH_CTR_TOP_BASE);
   const int arity = A ? A : t.arity;
@@ -1070,17 +1070,16 @@ __global__ void __launch_bounds__(kBlock)
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x, base = tile * kTile;
   int32_t v[kItems];
+  uint8_t mk[kItems];
   bool win[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    v[it] = 0;
-    win[it] = false;
-    if (p < n) {
-      v[it] = tmp[p];
-      win[it] = v[it] < 0 && !(mask[p] & DEMOTED);
-    }
+    v[it] = p < n ? __ldg(tmp + p) : 0;
+    mk[it] = p < n ? __ldg(mask + p) : DEMOTED;
   }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) win[it] = v[it] < 0 && !(mk[it] & DEMOTED);
   uint32_t bal[kItems];
   tile_scan_known(win, bal, sm, tile_pre, tile, nullptr);
 #pragma unroll
