@@ -462,55 +462,164 @@ __device__ __forceinline__ bool same_key_in_warp(const Key<A>& k, unsigned live,
   return true;
 }
 
+// Fast path of the claim for a position whose home bucket is already
+// loaded: resolves EMPTY-in-bucket (-> CAS to issue), a match in the bucket
+// (found / join / displace), and reports SLOW when probing must continue.
+enum { kFastDone = 0, kFastCas = 1, kFastSlow = 2 };
+
+template <int A>
+__device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint32_t h, uint32_t j,
+                                          const uint32_t (&w)[8], const int32_t* batch, uint8_t* mask,
+                                          int32_t* tile_cnt, uint32_t* res, bool* candidate, uint32_t* cas_slot,
+                                          uint4* cas_expect) {
+  const uint32_t me = PEND | j;
+  const uint32_t b = home_bucket(h, t.n_buckets);
+  bool have_free = false;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const uint32_t st = w[4 * s + 3];
+    if (st >= TOMB) {
+      if (!have_free) {
+        have_free = true;
+        *cas_slot = 2 * b + s;
+        *cas_expect = make_uint4(w[4 * s], w[4 * s + 1], w[4 * s + 2], st);
+      }
+      if (st == EMPTY) return kFastCas;
+    } else if (slot_matches<A>(w + 4 * s, st, k, t, batch)) {
+      const uint32_t slot = 2 * b + s;
+      *res = PEND | slot;
+      if (st < PEND) {
+        *res = st;
+      } else if (st < me) {
+        mask[j] = DEMOTED;
+      } else {
+        const uint32_t old = atomicMin(&t.slots[slot].w, me);
+        if (old < me) {
+          mask[j] = DEMOTED;
+        } else {
+          mask[old & ~PEND] = DEMOTED;
+          atomicSub(&tile_cnt[(old & ~PEND) / kTile], 1);
+          *candidate = true;
+        }
+      }
+      return kFastDone;
+    }
+  }
+  return kFastSlow;
+}
+
+// Claim pass (insert / activate phase 1).  Each thread owns R positions (one
+// per round, rounds are warp-contiguous), and the long-latency steps of all
+// rounds are issued together: R home-bucket loads, then R 128-bit CASes, so
+// a warp keeps 2R memory round trips in flight instead of 2 serial ones.
+constexpr int kClaimRounds = 2;
+
 template <int A>
 __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
                                                   int32_t* counters, int32_t* tile_cnt) {
-  __shared__ uint32_t stage[kBlock * 3];
-  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  constexpr int R = kClaimRounds;
+  __shared__ uint32_t stage[R][kBlock * 3];
   const int lane = threadIdx.x & 31;
-  const bool valid = p < n;
-  const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
-  Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, stream_policy(t.hints));
-  if (!valid) return;
-  const uint32_t h = hash_key<A>(k, t.arity);
-  // warp pre-aggregation: equal keys in a warp resolve through their lowest
-  // lane (= lowest batch position); the rest are duplicate losers or share
-  // the leader's found index (hashmap.py:125-131 first-occurrence rule).
-  // One match on the hash first; the exact word matches only run when some
-  // lanes share a hash.
-  unsigned grp = 1u << lane;
-  if (A != 0) {
-    grp = __match_any_sync(live, h);
-    if (__any_sync(live, __popc(grp) > 1)) {
-      unsigned g2;
-      same_key_in_warp<A>(k, live, &g2);
-      grp &= g2;
+  const int64_t blk = blockIdx.x * static_cast<int64_t>(kBlock * R);
+  const uint64_t pol = stream_policy(t.hints);
+  Key<A> k[R];
+  uint32_t h[R], res[R];
+  unsigned live[R];
+  int leader[R];
+  bool lead[R], cand[R], tomb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = blk + r * kBlock + threadIdx.x;
+    live[r] = __ballot_sync(0xFFFFFFFFu, p < n);
+    k[r] = load_key_warp<A>(keys, p, n, t.arity, stage[r], pol);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = blk + r * kBlock + threadIdx.x;
+    lead[r] = false;
+    cand[r] = tomb[r] = false;
+    res[r] = 0;
+    leader[r] = lane;
+    if (p >= n) continue;
+    h[r] = hash_key<A>(k[r], t.arity);
+    // warp pre-aggregation: equal keys in a warp resolve through their
+    // lowest lane (= lowest batch position); the rest are duplicate losers or
+    // share the leader's found index (hashmap.py:125-131).  One match on the
+    // hash; exact word matches only when some lanes share a hash.
+    unsigned grp = 1u << lane;
+    if (A != 0) {
+      grp = __match_any_sync(live[r], h[r]);
+      if (__any_sync(live[r], __popc(grp) > 1)) {
+        unsigned g2;
+        same_key_in_warp<A>(k[r], live[r], &g2);
+        grp &= g2;
+      }
+    }
+    leader[r] = __ffs(grp) - 1;
+    lead[r] = lane == leader[r];
+  }
+  // stage 1: every round's home bucket in flight
+  uint32_t w[R][8];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (lead[r]) ld256_relaxed(t.slots + 2 * static_cast<size_t>(home_bucket(h[r], t.n_buckets)), w[r]);
+  // stage 2: classify; stage 3: every round's CAS in flight
+  int state[R];
+  uint32_t cas_slot[R];
+  uint4 cas_expect[R];
+  bool cas_ok[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    state[r] = kFastDone;
+    if (lead[r])
+      state[r] = claim_fast<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * kBlock + threadIdx.x), w[r], keys,
+                               mask, tile_cnt, &res[r], &cand[r], &cas_slot[r], &cas_expect[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    cas_ok[r] = false;
+    if (state[r] == kFastCas) {
+      const uint32_t j = static_cast<uint32_t>(blk + r * kBlock + threadIdx.x);
+      cas_ok[r] = cas128(t.slots + cas_slot[r], cas_expect[r], slot_value<A>(k[r], PEND | j));
     }
   }
-  const int leader = __ffs(grp) - 1;
-  uint32_t res = 0;
-  bool claimed_tomb = false, candidate = false;
-  if (lane == leader)
-    res = probe_claim<A>(t, k, h, static_cast<uint32_t>(p), keys, mask, counters, tile_cnt, &claimed_tomb,
-                         &candidate);
-  __syncwarp(live);
-  // exact per-tile winner counts: +1 per candidate (displaced ones were
-  // decremented by their displacer), so no look-back scan is needed later
-  const unsigned cand = __ballot_sync(live, candidate);
-  if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
-  const uint32_t lres = __shfl_sync(live, res, leader);
-  if (lane == leader) {
-    tmp[p] = static_cast<int32_t>(res);
-  } else if (lres < PEND) {
-    tmp[p] = static_cast<int32_t>(lres);
-  } else {
-    tmp[p] = static_cast<int32_t>(PEND);
-    mask[p] = DEMOTED;
+  // stage 4: resolve; anything unusual takes the full probe loop
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (state[r] == kFastCas && cas_ok[r]) {
+      res[r] = PEND | CLAIMER | cas_slot[r];
+      cand[r] = true;
+      tomb[r] = cas_expect[r].w == TOMB;
+    } else if (state[r] != kFastDone) {
+      res[r] = probe_claim<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * kBlock + threadIdx.x), keys, mask,
+                              counters, tile_cnt, &tomb[r], &cand[r]);
+    }
   }
+  // stage 5: per round, broadcast leader results and count candidates
+  int32_t cand_total = 0, tomb_total = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = blk + r * kBlock + threadIdx.x;
+    if (p >= n) continue;
+    __syncwarp(live[r]);
+    const uint32_t lres = __shfl_sync(live[r], res[r], leader[r]);
+    if (lead[r]) {
+      tmp[p] = static_cast<int32_t>(res[r]);
+    } else if (lres < PEND) {
+      tmp[p] = static_cast<int32_t>(lres);
+    } else {
+      tmp[p] = static_cast<int32_t>(PEND);
+      mask[p] = DEMOTED;
+    }
+    cand_total += __popc(__ballot_sync(live[r], cand[r]));
+    tomb_total += __popc(__ballot_sync(live[r], tomb[r]));
+  }
+  // exact per-tile winner counts: +1 per candidate (displaced ones were
+  // decremented by their displacer), so the commit needs no look-back scan
+  if (lane == 0 && cand_total) atomicAdd(&tile_cnt[blk / kTile], cand_total);
   // tombstones reused by this batch (rare: only after erases)
-  const unsigned ct = __ballot_sync(live, claimed_tomb);
-  if (ct && lane == __ffs(live) - 1) atomicSub(&counters[ASH_CTR_TOMBS], __popc(ct));
+  if (lane == 0 && tomb_total) atomicSub(&counters[ASH_CTR_TOMBS], tomb_total);
 }
 
 // ---------------------------------------------------------------------------
@@ -1238,7 +1347,7 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(out_mask, 0, n, s);
   if (int rc = check_tiles(m, n)) return rc;
-  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
+  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
                                                                                  m->counters, m->tile_counts)));
   return check_launch("ash_insert_claim");
 }
