@@ -512,7 +512,7 @@ __device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint3
 // per round, rounds are warp-contiguous), and the long-latency steps of all
 // rounds are issued together: R home-bucket loads, then R 128-bit CASes, so
 // a warp keeps 2R memory round trips in flight instead of 2 serial ones.
-constexpr int kClaimRounds = 2;
+constexpr int kClaimRounds = 1;
 
 template <int A>
 __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
