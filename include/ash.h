@@ -168,6 +168,31 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64,
                  int64_t n, double voxel, int32_t* out_coords, int64_t* out_sel,
                  int32_t* scratch_idx, uint8_t* scratch_mask, void* stream);
 
+/* ---- hash-partitioned multi-GPU mode (no reference
+ * counterpart): owner(key) = mix64(key) -> [0, world). ---------------------- */
+
+const char* ash_route_last_error(void);
+
+/* int32 scratch words ash_route_partition needs for n keys and world ranks. */
+int64_t ash_route_scratch_len(int64_t n, int32_t world);
+
+/* owner rank of every key (world <= 64). */
+int ash_route_owner(const int32_t* keys, int64_t n, int32_t arity, int32_t world,
+                    int32_t* out, void* stream);
+
+/* Stable partition of a batch by owner: perm lists positions grouped by
+ * owner rank, batch order kept inside each group; counts[world] (int64) are
+ * the group sizes (the all-to-all send splits). */
+int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t world,
+                        int32_t* perm, int64_t* counts, int32_t* scratch,
+                        int64_t scratch_len, void* stream);
+
+/* dst[i] = src[idx[i]] and dst[idx[i]] = src[i] for rows of row_bytes. */
+int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
+                    void* dst, void* stream);
+int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
+                     void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

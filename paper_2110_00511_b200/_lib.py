@@ -56,7 +56,15 @@ _SIGNATURES = {
     "ash_quantize": (c_int32, [c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p, c_void_p]),
     "ash_voxelize": (c_int32, [_M, c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
+    "ash_route_last_error": (c_char_p, []),
+    "ash_route_scratch_len": (c_int64, [c_int64, c_int32]),
+    "ash_route_owner": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    "ash_route_partition": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p,
+                                      c_void_p, c_int64, c_void_p]),
+    "ash_gather_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ash_scatter_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
 }
+_ROUTE_FUNCS = ("ash_route_owner", "ash_route_partition", "ash_gather_rows", "ash_scatter_rows")
 
 EXPORTED = tuple(_SIGNATURES)
 
@@ -89,7 +97,8 @@ def call(name: str, *args) -> None:
     rc = getattr(lib, name)(*args)
     if rc == ASH_OK:
         return
-    msg = (lib.ash_last_error() or b"").decode(errors="replace")
+    err = lib.ash_route_last_error if name in _ROUTE_FUNCS else lib.ash_last_error
+    msg = (err() or b"").decode(errors="replace")
     if rc == ASH_ERR_INVALID:
         raise ValueError(f"{name}: {msg}")
     raise AshError(f"{name} failed ({rc}): {msg}")

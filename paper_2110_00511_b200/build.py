@@ -13,7 +13,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = [PKG / "csrc" / "ash_map.cu"]
+SOURCES = [PKG / "csrc" / "ash_map.cu", PKG / "csrc" / "ash_route.cu"]
 HEADERS = [ROOT / "include" / "ash.h"]
 LIB_DIR = PKG / "lib"
 LIB_PATH = LIB_DIR / "libash.so"

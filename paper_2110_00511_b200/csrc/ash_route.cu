@@ -1,0 +1,261 @@
+// ash_route.cu — multi-GPU routing kernels for the hash-partitioned map.
+//
+// No reference counterpart (the reference has no distributed mode; SURVEY
+// §8(e)).  owner(key) = mix64(key) mapped to [0, world) by multiply-shift;
+// the mix is independent of the in-table bucket hash (ash_map.cu) so shards
+// stay uniformly loaded.  The partition is STABLE: a rank's keys for one
+// owner keep batch order, and NCCL all-to-all concatenates by source rank,
+// so every owner sees its keys in global batch order and first-occurrence
+// winners stay bit-exact (verified on the oracle in SURVEY §8(e)).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/ash.h"
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kItems = 8;
+constexpr int kTile = kBlock * kItems;
+constexpr int kMaxWorld = 64;
+
+thread_local char g_route_err[256] = "";
+
+int rfail(const char* msg) {
+  snprintf(g_route_err, sizeof(g_route_err), "%s", msg);
+  return ASH_ERR_INVALID;
+}
+
+int rcheck(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_route_err, sizeof(g_route_err), "%s: %s", what, cudaGetErrorString(e));
+    return ASH_ERR_CUDA;
+  }
+  return ASH_OK;
+}
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t owner_of(const int32_t* row, int arity, uint32_t world) {
+  uint64_t x = 0x243F6A8885A308D3ull ^ static_cast<uint64_t>(arity);
+  for (int d = 0; d < arity; ++d) x = fmix64(x ^ (static_cast<uint64_t>(static_cast<uint32_t>(row[d])) + 0x9E3779B97F4A7C15ull * (d + 1)));
+  return static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * world) >> 32);
+}
+
+// pass 1: per-tile, per-owner counts -> cnt[owner * n_tiles + tile]
+__global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restrict__ keys, int64_t n, int arity,
+                                                        uint32_t world, int32_t* __restrict__ cnt, int64_t n_tiles) {
+  __shared__ int32_t s_cnt[kMaxWorld];
+  for (int o = threadIdx.x; o < kMaxWorld; o += kBlock) s_cnt[o] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p < n) atomicAdd(&s_cnt[owner_of(keys + p * arity, arity, world)], 1);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < static_cast<int>(world); o += kBlock) cnt[o * n_tiles + blockIdx.x] = s_cnt[o];
+}
+
+// pass 2 (one block): exclusive scan over the owner-major count matrix;
+// per-owner totals to counts[]
+__global__ void __launch_bounds__(1024) k_route_scan(int32_t* cnt, int64_t len, int64_t n_tiles, uint32_t world,
+                                                     int64_t* counts) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < len; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t x = i < len ? cnt[i] : 0;
+    int32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = warp_tot[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    const int32_t c = carry;
+    if (i < len) cnt[i] = c + warp_tot[warp] + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + warp_tot[warp] + incl;
+    __syncthreads();
+  }
+  // per-owner totals from the scanned offsets
+  for (uint32_t o = threadIdx.x; o < world; o += 1024) {
+    const int64_t start = cnt[o * n_tiles];
+    const int64_t end = (o + 1 < world) ? cnt[(o + 1) * n_tiles] : carry;
+    counts[o] = end - start;
+  }
+}
+
+// pass 3: stable scatter of positions: perm[offset(owner, tile) + rank] = p.
+// Position order inside a tile is (item, warp, lane); per-owner group sizes
+// come from __match_any_sync and are scanned per owner in that order.
+__global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restrict__ keys, int64_t n, int arity,
+                                                          uint32_t world, const int32_t* __restrict__ off,
+                                                          int64_t n_tiles, int32_t* __restrict__ perm) {
+  constexpr int kW = kBlock / 32;
+  __shared__ int32_t s_pre[kItems][kW][kMaxWorld];
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < kItems * kW * kMaxWorld; e += kBlock) (&s_pre[0][0][0])[e] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t own[kItems], rank_in_warp[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, own[it]);
+    rank_in_warp[it] = __popc(same & lt);
+    if (p < n && (same & lt) == 0) s_pre[it][warp][own[it]] = __popc(same);
+  }
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
+    int32_t run = off[o * n_tiles + blockIdx.x];
+    for (int it = 0; it < kItems; ++it)
+      for (int w = 0; w < kW; ++w) {
+        const int32_t c = s_pre[it][w][o];
+        s_pre[it][w][o] = run;
+        run += c;
+      }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p < n) perm[s_pre[it][warp][own[it]] + rank_in_warp[it]] = static_cast<int32_t>(p);
+  }
+}
+
+__global__ void k_gather_rows(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                              int64_t words, uint32_t* __restrict__ dst) {
+  // row bytes multiple of 4: thread per (row, word)
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * words) return;
+  const int64_t r = t / words, w = t - r * words;
+  dst[t] = reinterpret_cast<const uint32_t*>(src)[static_cast<int64_t>(idx[r]) * words + w];
+}
+
+__global__ void k_gather_bytes(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                               int64_t rb, uint8_t* __restrict__ dst) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * rb) return;
+  const int64_t r = t / rb, b = t - r * rb;
+  dst[t] = src[static_cast<int64_t>(idx[r]) * rb + b];
+}
+
+__global__ void k_scatter_rows(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                               int64_t words, uint8_t* __restrict__ dst) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * words) return;
+  const int64_t r = t / words, w = t - r * words;
+  reinterpret_cast<uint32_t*>(dst)[static_cast<int64_t>(idx[r]) * words + w] = src[t];
+}
+
+__global__ void k_scatter_bytes(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                                int64_t rb, uint8_t* __restrict__ dst) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * rb) return;
+  const int64_t r = t / rb, b = t - r * rb;
+  dst[static_cast<int64_t>(idx[r]) * rb + b] = src[t];
+}
+
+__global__ void k_owner_of(const int32_t* __restrict__ keys, int64_t n, int arity, uint32_t world,
+                           int32_t* __restrict__ out) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p < n) out[p] = static_cast<int32_t>(owner_of(keys + p * arity, arity, world));
+}
+
+inline unsigned blocks(int64_t work, int per) {
+  int64_t g = (work + per - 1) / per;
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ash_route_last_error(void) { return g_route_err; }
+
+int64_t ash_route_scratch_len(int64_t n, int32_t world) {
+  return ((n + kTile - 1) / kTile) * static_cast<int64_t>(world);
+}
+
+int ash_route_owner(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int32_t* out, void* stream) {
+  if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
+  if (n == 0) return ASH_OK;
+  k_owner_of<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(keys, n, arity,
+                                                                                 static_cast<uint32_t>(world), out);
+  return rcheck("ash_route_owner");
+}
+
+int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int32_t* perm,
+                        int64_t* counts, int32_t* scratch, int64_t scratch_len, void* stream) {
+  if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
+  if (n >= (int64_t(1) << 31)) return rfail("routing batch too long");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n_tiles = (n + kTile - 1) / kTile;
+  if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
+  if (n == 0) {
+    cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, s);
+    return rcheck("ash_route_partition");
+  }
+  const uint32_t w = static_cast<uint32_t>(world);
+  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, scratch, n_tiles);
+  k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts);
+  k_route_scatter<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, scratch, n_tiles, perm);
+  return rcheck("ash_route_partition");
+}
+
+int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
+  if (n < 0 || row_bytes < 0) return rfail("bad gather arguments");
+  if (n == 0 || row_bytes == 0) return ASH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (row_bytes % 4 == 0)
+    k_gather_rows<<<blocks(n * (row_bytes / 4), kBlock), kBlock, 0, s>>>(
+        static_cast<const uint8_t*>(src), idx, n, row_bytes / 4, static_cast<uint32_t*>(dst));
+  else
+    k_gather_bytes<<<blocks(n * row_bytes, kBlock), kBlock, 0, s>>>(static_cast<const uint8_t*>(src), idx, n,
+                                                                    row_bytes, static_cast<uint8_t*>(dst));
+  return rcheck("ash_gather_rows");
+}
+
+int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
+  if (n < 0 || row_bytes < 0) return rfail("bad scatter arguments");
+  if (n == 0 || row_bytes == 0) return ASH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (row_bytes % 4 == 0)
+    k_scatter_rows<<<blocks(n * (row_bytes / 4), kBlock), kBlock, 0, s>>>(
+        static_cast<const uint32_t*>(src), idx, n, row_bytes / 4, static_cast<uint8_t*>(dst));
+  else
+    k_scatter_bytes<<<blocks(n * row_bytes, kBlock), kBlock, 0, s>>>(static_cast<const uint8_t*>(src), idx, n,
+                                                                     row_bytes, static_cast<uint8_t*>(dst));
+  return rcheck("ash_scatter_rows");
+}
+
+}  // extern "C"
