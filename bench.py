@@ -49,6 +49,20 @@ def algorithmic_bytes(op: str, rho_new: float, value_bytes: int, key_bytes: int 
     return base + rho_new * (key_bytes + 2 * value_bytes + 32)
 
 
+def _profiled_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu summary
+    (profiles/<tag>_kernels.json, tools/summarize_profiles.py); None if absent."""
+    files = sorted((ROOT / "profiles").glob("*_kernels.json"), key=lambda p: p.stat().st_mtime)
+    for f in reversed(files):
+        try:
+            d = json.loads(f.read_text())
+        except ValueError:
+            continue
+        if kernel in d and d[kernel].get("dram_bytes_per_launch"):
+            return int(d[kernel]["dram_bytes_per_launch"]), f.name
+    return None, None
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -385,6 +399,7 @@ def main():
     }
     dom = max(kms, key=kms.get)
     achieved = per_kernel_bytes[dom] / (kms[dom] / 1e3) / 1e9
+    traffic, traffic_src = _profiled_traffic(f"k_{dom}")
     cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
     line = {
         "metric": METRIC, "value": round(res["value"], 2), "unit": UNIT, "n_gpus": 1,
@@ -398,7 +413,9 @@ def main():
                    "construction": "excluded (HashMap.clear before each step)"},
         "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": round(achieved, 1),
                      "peak": bw, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / bw, 4), "traffic": None,
+                     "frac": round(achieved / bw, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": int(per_kernel_bytes[dom]),
                      "kernel_ms": {k: round(v, 4) for k, v in kms.items()}},
         "op_roofline": {
             "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS /
