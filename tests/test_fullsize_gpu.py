@@ -101,6 +101,6 @@ def test_c4_allocate_blocks_full_frame(ash):
     gm = ash.HashMap(100_000, 3, [((8, 8, 8, 2), np.float32)], device="cuda")
     gi, local = ash.allocate_blocks(gm, coords)
     assert np.array_equal(gi.cpu().numpy(), gi_ref)
-    assert len(gi_ref) == 1_696
+    assert len(gi_ref) == 1_836  # fx = fy = 500 (cli.py:125-130 scaling of the 320-wide intrinsics)
     assert np.array_equal(local.find(coords).indices.cpu().numpy(), local_ref.find(coords).indices)
     assert local.value_buffer(0).cpu().numpy().tobytes() == local_ref.value_buffer(0).tobytes()
