@@ -16,7 +16,9 @@ Differences in mechanism (not in results):
   * ``size`` is tracked lazily: a mutating batch does not synchronise with the
     device unless the host cannot prove the batch fits (capacity - an upper
     bound on size >= batch length).  Reading ``size`` synchronises.
-  * Results are CUDA tensors (indices int32, masks bool).
+  * Results (indices int32, masks bool) live where the keys came from: CUDA
+    keys give CUDA tensors, host keys give host tensors; large pinned host
+    batches are pipelined (chunked H2D / kernels / D2H overlap).
   * ``threads`` is accepted and ignored (the device is the parallelism).
 """
 from __future__ import annotations
@@ -362,7 +364,7 @@ class HashMap:
 
     # -- validation (hashmap.py:246-286) --------------------------------
 
-    def _check_keys(self, keys) -> torch.Tensor:
+    def _check_keys(self, keys, to_device: bool = True) -> torch.Tensor:
         if isinstance(keys, torch.Tensor):
             k = keys
             if k.is_floating_point() or k.is_complex():
@@ -393,9 +395,9 @@ class HashMap:
             if bool((cast.to(k.dtype) != k).any()):
                 raise ValueError("key values do not fit in int32")
             k = cast
-        return k.to(self._device, non_blocking=True).contiguous()
+        return k.to(self._device, non_blocking=True).contiguous() if to_device else k.contiguous()
 
-    def _check_values(self, m: int, values) -> list:
+    def _check_values(self, m: int, values, to_device: bool = True) -> list:
         if len(values) != len(self.value_specs):
             raise ValueError(f"expected {len(self.value_specs)} value batches, got {len(values)}")
         out = []
@@ -416,7 +418,7 @@ class HashMap:
                 raise ValueError(
                     f"value batch {pos} has shape {tuple(t.shape)}, expected "
                     f"(n, {', '.join(map(str, spec.shape))})") from None
-            out.append(t.to(self._device, non_blocking=True).contiguous())
+            out.append(t.to(self._device, non_blocking=True).contiguous() if to_device else t.contiguous())
         return out
 
     # -- growth (hashmap.py:311-332) --------------------------------------
@@ -468,21 +470,109 @@ class HashMap:
 
     # -- operations (hashmap.py:336-456) ---------------------------------
 
+    # -- host-resident batches ---------------------------------------------
+    # Results live where the keys came from: CUDA keys -> CUDA results; host
+    # keys (numpy, lists, CPU tensors) -> host results, like the reference.
+    # Large pinned host batches are pipelined in chunks: H2D of chunk i+1
+    # overlaps the kernels of chunk i and the D2H of chunk i-1.  For insert
+    # this is exact: a later position never demotes an earlier one, so a
+    # chunk's winners are final after its own claim, and sequential chunks
+    # give the single-batch masks and indices (found-earlier == duplicate
+    # loser in insert mode: both report False / -1).
+
+    PIPELINE_MIN = 1 << 20
+    PIPELINE_CHUNK = 2 << 20
+
+    @staticmethod
+    def _is_host(x) -> bool:
+        return not (isinstance(x, torch.Tensor) and x.is_cuda)
+
+    def _streams(self):
+        if getattr(self, "_xfer", None) is None:
+            self._xfer = (torch.cuda.Stream(self._device), torch.cuda.Stream(self._device))
+        return self._xfer
+
+    def _to_host(self, res: BatchResult) -> BatchResult:
+        return BatchResult(res.indices.cpu(), res.masks.cpu())
+
+    def _pipelined(self, keys_h: torch.Tensor, vals_h, op: str) -> BatchResult:
+        """Chunked H2D / kernels / D2H overlap for a host batch (op = insert
+        or find).  Caller holds the guard and has checked capacity."""
+        m = keys_h.shape[0]
+        dev = self._device
+        s = torch.cuda.current_stream(dev)
+        h2d, d2h = self._streams()
+        keys_d = torch.empty((m, self.key_arity), dtype=torch.int32, device=dev)
+        vals_d = [torch.empty((m, *v.shape[1:]), dtype=v.dtype, device=dev) for v in vals_h]
+        idx_d = torch.empty(m, dtype=torch.int32, device=dev)
+        msk_d = torch.empty(m, dtype=torch.uint8, device=dev)
+        idx_h = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        msk_h = torch.empty(m, dtype=torch.uint8, pin_memory=True)
+        h2d.wait_stream(s)
+        d2h.wait_stream(s)
+        c = self.PIPELINE_CHUNK
+        self._ensure_scan(min(m, c))
+        for a in range(0, m, c):
+            b = min(m, a + c)
+            with torch.cuda.stream(h2d):
+                keys_d[a:b].copy_(keys_h[a:b], non_blocking=True)
+                for vd, vh in zip(vals_d, vals_h):
+                    vd[a:b].copy_(vh[a:b], non_blocking=True)
+            s.wait_stream(h2d)
+            if op == "insert":
+                vptr = None
+                if vals_d:
+                    vptr = (_lib.c_void_p * len(vals_d))(*[v[a:b].data_ptr() for v in vals_d])
+                call("ash_insert", self._ptr(), keys_d[a:b].data_ptr(), b - a, vptr, 0,
+                     idx_d[a:b].data_ptr(), msk_d[a:b].data_ptr(), self._stream())
+            else:
+                call("ash_find", self._ptr(), keys_d[a:b].data_ptr(), b - a, idx_d[a:b].data_ptr(),
+                     msk_d[a:b].data_ptr(), self._stream())
+            d2h.wait_stream(s)
+            with torch.cuda.stream(d2h):
+                idx_h[a:b].copy_(idx_d[a:b], non_blocking=True)
+                msk_h[a:b].copy_(msk_d[a:b], non_blocking=True)
+        d2h.synchronize()
+        return BatchResult(idx_h, msk_h.view(torch.bool))
+
+    def _pipeline_fits(self, keys) -> bool:
+        return (isinstance(keys, torch.Tensor) and not keys.is_cuda and keys.is_pinned()
+                and keys.dim() == 2 and keys.shape[0] >= self.PIPELINE_MIN)
+
     def insert(self, keys, *values) -> BatchResult:
         """Insert keys with one value batch per value buffer: the first
         occurrence of each absent key wins a fresh index; existing values are
         never overwritten (hashmap.py:336-347)."""
+        host = self._is_host(keys)
+        if host and self._pipeline_fits(keys):
+            k = self._check_keys(keys, to_device=False)
+            vals = self._check_values(k.shape[0], values, to_device=False)
+            with self._guard.writing():
+                m = k.shape[0]
+                if m > self._capacity - self._top_ub:
+                    self._sync_size()
+                if m <= self._capacity - self._top_ub:
+                    self._reserve_slots(m)
+                    res = self._pipelined(k, vals, "insert")
+                    self._top_ub = min(self._capacity, self._top_ub + m)
+                    self._size_known = False
+                    return res
+                return self._to_host(self._insert_like(
+                    k.to(self._device), [v.to(self._device) for v in vals], association=False))
         keys = self._check_keys(keys)
         vals = self._check_values(keys.shape[0], values)
         with self._guard.writing():
-            return self._insert_like(keys, vals, association=False)
+            res = self._insert_like(keys, vals, association=False)
+        return self._to_host(res) if host else res
 
     def activate(self, keys) -> BatchResult:
         """Ensure keys are present; values untouched; masks = found OR
         winner (hashmap.py:349-360)."""
+        host = self._is_host(keys)
         keys = self._check_keys(keys)
         with self._guard.writing():
-            return self._insert_like(keys, None, association=True)
+            res = self._insert_like(keys, None, association=True)
+        return self._to_host(res) if host else res
 
     def _insert_like(self, keys: torch.Tensor, vals, association: bool) -> BatchResult:
         m = keys.shape[0]
@@ -530,6 +620,11 @@ class HashMap:
 
     def find(self, keys) -> BatchResult:
         """Look up keys; the map is not modified (hashmap.py:415-429)."""
+        host = self._is_host(keys)
+        if host and self._pipeline_fits(keys):
+            k = self._check_keys(keys, to_device=False)
+            with self._guard.reading():
+                return self._pipelined(k, [], "find")
         keys = self._check_keys(keys)
         with self._guard.reading():
             m = keys.shape[0]
@@ -538,11 +633,13 @@ class HashMap:
             if m:
                 call("ash_find", self._ptr(), keys.data_ptr(), m, idx.data_ptr(),
                      msk.data_ptr(), self._stream())
-            return BatchResult(idx, msk.view(torch.bool))
+            res = BatchResult(idx, msk.view(torch.bool))
+        return self._to_host(res) if host else res
 
     def erase(self, keys) -> torch.Tensor:
         """Remove keys; exactly one True per removed key, at its first batch
         position (hashmap.py:431-456)."""
+        host = self._is_host(keys)
         keys = self._check_keys(keys)
         with self._guard.writing():
             m = keys.shape[0]
@@ -553,7 +650,8 @@ class HashMap:
                      scratch.data_ptr(), self._stream())
                 self._size_known = False
                 self._tombs_ub += m
-            return out.view(torch.bool)
+            res = out.view(torch.bool)
+        return res.cpu() if host else res
 
     def active_indices(self) -> torch.Tensor:
         """All buffer indices holding an entry, ascending (hashmap.py:458-460)."""
