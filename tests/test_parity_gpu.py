@@ -132,3 +132,28 @@ def test_tombstone_churn_triggers_cleanup(ash):
         assert bool(g.erase(keys).all())
     assert g.size == 0
     g.validate()
+
+
+def test_pipelined_host_batches_match_device_path(ash):
+    """Pinned host batches take the chunked H2D/kernel/D2H pipeline; results
+    (on the host) must equal the single-batch device path bit for bit."""
+    import torch
+    from paper_2110_00511_b200.workloads import int3_batch
+    n = 5_000_000
+    keys = torch.from_numpy(int3_batch(n, 0.3, seed=11)).pin_memory()
+    vals = torch.rand((n, 2)).pin_memory()
+    a = ash.HashMap(n, 3, [((2,), np.float32)], device="cuda")
+    b = ash.HashMap(n, 3, [((2,), np.float32)], device="cuda")
+    a.insert(keys[:1000].cuda(), vals[:1000].cuda())  # non-empty start: found vs new mix
+    b.insert(keys[:1000].cuda(), vals[:1000].cuda())
+    ra = a.insert(keys, vals)                      # pipelined (pinned, >= 1M rows)
+    rb = b.insert(keys.cuda(), vals.cuda())        # one device batch
+    assert not ra.indices.is_cuda and rb.indices.is_cuda
+    assert torch.equal(ra.indices, rb.indices.cpu()) and torch.equal(ra.masks, rb.masks.cpu())
+    assert a.size == b.size
+    assert torch.equal(a.value_buffer(0), b.value_buffer(0)) and torch.equal(a._key_buf, b._key_buf)
+    fa, fb = a.find(keys), b.find(keys.cuda())
+    assert torch.equal(fa.indices, fb.indices.cpu()) and bool(fa.masks.all())
+    # host (numpy) input -> host results
+    r = a.find(keys[:10].numpy())
+    assert not r.masks.is_cuda and bool(r.masks.all())
