@@ -297,8 +297,77 @@ def gpu_single(args, torch, dev):
     d2h = 2 * (r.indices.numel() * 4 + r.masks.numel())
 
     sweep = run_sweep(torch, dev, ash, flush)
+    other = run_other_configs(torch, dev, ash, flush, with_cpu=not args.no_cpu_baseline)
     return dict(ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
-                sweep=sweep, launches_per_step=4)
+                sweep=sweep, other=other, launches_per_step=4)
+
+
+def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
+    """configs[2] (voxelize 20M sphere points at 5 mm) and configs[3] (block
+    allocation for a 640x480 plane frame, 1.536M candidates): device time of
+    the map path with CUDA events, and the CPU reference algorithm (oracle
+    port) on a bounded sample beside it."""
+    from paper_2110_00511_b200.workloads import sphere_points
+    from oracle import ash_oracle as O
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    pts_np = sphere_points(20_000_000, seed=0)
+    pts = torch.from_numpy(pts_np).to(dev)
+    ts = []
+    for i in range(6):
+        l2_flush(torch, flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        coords, sel = ash.voxel_downsample(pts, 0.005, device=dev)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    c3 = {"workload": "configs[2]: voxel_downsample of 20M unit-sphere points (float64) at 5 mm",
+          "voxels": int(coords.shape[0]), "ms": round(ms, 3), "mpts_per_s": round(20e6 / ms / 1e3, 1),
+          "note": "includes the count read-back (one 8-byte sync) that sizes the outputs"}
+    if with_cpu:
+        smp = pts_np[:2_000_000]
+        t0 = time.perf_counter()
+        O.voxel_downsample(smp, 0.005)
+        c3["cpu_baseline"] = {"mpts_per_s": round(2.0 / (time.perf_counter() - t0), 3), "cores": 1,
+                              "kind": "port", "sample": "first 2M points of the same cloud"}
+    out["c3_voxelize"] = c3
+    cam = O.scaled_camera(640, 480)
+    depth = O.plane_depth(cam, 1.0)
+    frames = []
+    for f in range(10):
+        pose = np.eye(4)
+        pose[0, 3] = 0.02 * f
+        frames.append(O.candidate_blocks(depth, cam, pose, 0.0058 * 8, 0.04))
+    frames_d = [torch.from_numpy(c).to(dev) for c in frames]
+    gm = ash.HashMap(100_000, 3, [((8, 8, 8, 2), np.float32)], device=dev)
+    ts = []
+    for rep in range(2):
+        gm.clear()
+        for c in frames_d:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ash.allocate_blocks(gm, c)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if rep:
+                ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    c4 = {"workload": "configs[3]: allocate_blocks map calls (local activate, global activate + find, "
+                      "local value scatter), 640x480 plane frames, 1.536M candidates each, 10 frames",
+          "blocks": gm.size, "ms_per_frame": round(ms, 3),
+          "mcand_per_s": round(len(frames[0]) / ms / 1e3, 1),
+          "note": "includes the host syncs of the boolean-mask gathers in the reference call sequence"}
+    if with_cpu:
+        og = O.OracleMap(100_000, 3, [((8, 8, 8, 2), np.float32)])
+        t0 = time.perf_counter()
+        O.allocate_blocks_map_calls(og, frames[0])
+        c4["cpu_baseline"] = {"mcand_per_s": round(len(frames[0]) / (time.perf_counter() - t0) / 1e6, 3),
+                              "cores": 1, "kind": "port", "sample": "first frame"}
+    out["c4_allocate_blocks"] = c4
+    return out
 
 
 def run_sweep(torch, dev, ash, flush):
@@ -422,6 +491,7 @@ def main():
         "gpu_launches": res["launches_per_step"] * args.steps,
         "clocks": res["clocks"],
         "sweep": res["sweep"],
+        "other_configs": res["other"],
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
