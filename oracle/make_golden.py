@@ -264,11 +264,33 @@ def scenario_hash_dedup(R):
     np.savez_compressed(OUT / "hash_dedup.npz", **out)
 
 
+def scenario_snapshot(R):
+    """serialize.py ASHL v1: a snapshot written by the reference after an
+    insert / erase / insert sequence (non-trivial heap, two value schemas)."""
+    rng = np.random.default_rng(77)
+    m = R["HashMap"](64, 3, [((2,), np.float32), ((3,), np.uint8)])
+    keys = rng.integers(-9, 9, size=(40, 3)).astype(np.int32)
+    v0 = rng.random((40, 2), dtype=np.float32)
+    v1 = rng.integers(0, 255, size=(40, 3)).astype(np.uint8)
+    m.insert(keys, v0, v1)
+    m.erase(keys[::4])
+    k2 = rng.integers(-9, 9, size=(10, 3)).astype(np.int32)
+    k2v0 = rng.random((10, 2), dtype=np.float32)
+    k2v1 = rng.integers(0, 255, size=(10, 3)).astype(np.uint8)
+    m.insert(k2, k2v0, k2v1)
+    path = OUT / "snapshot_ref.ashl"
+    m.save(path, metadata={"note": "golden"})
+    np.savez_compressed(OUT / "snapshot.npz", keys=keys, v0=v0, v1=v1, erase=keys[::4], k2=k2,
+                        k2v0=k2v0, k2v1=k2v1, snap=np.frombuffer(path.read_bytes(), np.uint8))
+    path.unlink()
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     R = _ref()
     for fn in (scenario_trace, scenario_c1, scenario_bindings_parity, scenario_random_ops,
-               scenario_growth, scenario_voxel, scenario_alloc_blocks, scenario_hash_dedup):
+               scenario_growth, scenario_voxel, scenario_alloc_blocks, scenario_hash_dedup,
+               scenario_snapshot):
         fn(R)
         print("wrote", fn.__name__)
 

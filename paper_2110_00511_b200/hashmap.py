@@ -710,11 +710,15 @@ class HashMap:
         assert flags & _lib.FLAG_TABLE_FULL == 0, "a probe wrapped the whole table"
 
     def save(self, path, metadata=None) -> None:
-        raise NotImplementedError("ASHL snapshots (serialize.py) are not on the device path yet")
+        """ASHL v1 snapshot, byte-compatible with the reference (hashmap.py:498-500)."""
+        from .serialize import save_map
+        save_map(self, path, metadata)
 
     @classmethod
-    def load(cls, path, backend=None, threads=1):
-        raise NotImplementedError("ASHL snapshots (serialize.py) are not on the device path yet")
+    def load(cls, path, backend=None, threads=1, device=None):
+        """Returns ``(HashMap, metadata)`` (hashmap.py:502-505)."""
+        from .serialize import load_map
+        return load_map(path, backend=backend, threads=threads, device=device)
 
 
 class HashSet(HashMap):
