@@ -5,14 +5,14 @@ batch operation runs hand-written sm_100a kernels from libash.so.
 """
 from .hashmap import (BatchResult, CapacityError, ConcurrentAccessError, HashMap,
                       HashSet, ValueSpec)
-from .geometry import (lattice_offsets, quantize, radius_neighbors, set_intersection,
-                       voxel_downsample)
+from .geometry import (PointCloud, lattice_offsets, quantize, radius_neighbors,
+                       set_intersection, voxel_downsample)
 from .blocks import BlockGrid, allocate_blocks
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchResult", "CapacityError", "ConcurrentAccessError", "HashMap", "HashSet",
-    "ValueSpec", "quantize", "voxel_downsample", "lattice_offsets", "radius_neighbors",
-    "set_intersection", "BlockGrid", "allocate_blocks",
+    "ValueSpec", "PointCloud", "quantize", "voxel_downsample", "lattice_offsets",
+    "radius_neighbors", "set_intersection", "BlockGrid", "allocate_blocks",
 ]

@@ -17,8 +17,45 @@ from . import _lib
 from ._lib import AshMap, call
 from .hashmap import BatchResult, HashMap, HashSet, _stream_handle, _table_slots
 
-__all__ = ["quantize", "voxel_downsample", "lattice_offsets", "radius_neighbors",
+__all__ = ["PointCloud", "quantize", "voxel_downsample", "lattice_offsets", "radius_neighbors",
            "set_intersection"]
+
+
+class PointCloud:
+    """Positions (float64, (n, 3)) plus optional per-point attributes
+    (geometry.py:16-46).  Positions may be a CUDA tensor."""
+
+    def __init__(self, positions, colors=None, normals=None):
+        if isinstance(positions, torch.Tensor):
+            self.positions = positions.to(torch.float64).reshape(-1, 3)
+        else:
+            self.positions = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+        n = len(self.positions)
+        for name, attr in (("colors", colors), ("normals", normals)):
+            if attr is not None:
+                attr = attr if isinstance(attr, torch.Tensor) else np.atleast_2d(np.asarray(attr))
+                if attr.shape[0] != n:
+                    attr = attr.reshape(n, -1)
+                if attr.shape[0] != n:
+                    raise ValueError(f"{name} length {attr.shape[0]} != {n} points")
+            setattr(self, name, attr)
+
+    def __len__(self) -> int:
+        return len(self.positions)
+
+    def select(self, idx) -> "PointCloud":
+        if isinstance(self.positions, np.ndarray) and isinstance(idx, torch.Tensor):
+            idx = idx.cpu().numpy()
+        return PointCloud(self.positions[idx],
+                          None if self.colors is None else self.colors[idx],
+                          None if self.normals is None else self.normals[idx])
+
+
+def _on_host(x) -> bool:
+    """Results follow the input: host inputs (numpy, lists, CPU tensors)
+    get host results, CUDA inputs get CUDA results."""
+    pos = getattr(x, "positions", x)
+    return not (isinstance(pos, torch.Tensor) and pos.is_cuda)
 
 
 def _points_tensor(points, device) -> torch.Tensor:
@@ -50,17 +87,18 @@ def quantize(positions, cell: float, device=None) -> torch.Tensor:
     if cell <= 0:
         raise ValueError("cell size must be > 0")
     dev = _device(device)
+    host = _on_host(positions)
     pts = _points_tensor(positions, dev)
     n = pts.shape[0]
     out = torch.empty((n, 3), dtype=torch.int32, device=dev)
     if n == 0:
-        return out
+        return out.cpu() if host else out
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     call("ash_quantize", pts.data_ptr(), int(pts.dtype == torch.float64), n, float(cell),
          out.data_ptr(), flags.data_ptr(), _stream_handle(dev))
     if int(flags.item()) & _lib.FLAG_RANGE:
         raise ValueError("quantized coordinates exceed int32 range")
-    return out
+    return out.cpu() if host else out
 
 
 class _VoxelWorkspace:
@@ -119,11 +157,12 @@ def voxel_downsample(points, voxel_size: float, backend: str = "generic", thread
     if voxel_size <= 0:
         raise ValueError("cell size must be > 0")
     dev = _device(device)
+    host = _on_host(points)
     pts = _points_tensor(points, dev)
     n = pts.shape[0]
     if n == 0:
-        return (torch.zeros((0, 3), dtype=torch.int32, device=dev),
-                torch.zeros(0, dtype=torch.int64, device=dev))
+        z = (torch.zeros((0, 3), dtype=torch.int32), torch.zeros(0, dtype=torch.int64))
+        return z if host else (z[0].to(dev), z[1].to(dev))
     ws = _VoxelWorkspace.get(dev)
     with _VoxelWorkspace._lock:
         ws.reserve(n)
@@ -138,6 +177,8 @@ def voxel_downsample(points, voxel_size: float, backend: str = "generic", thread
         count, flags = ws.counters[[_lib.CTR_COUNT, _lib.CTR_FLAGS]].tolist()
     if flags & _lib.FLAG_RANGE:
         raise ValueError("quantized coordinates exceed int32 range")
+    if host:
+        return coords[:count].cpu(), sel[:count].cpu()
     return coords[:count], sel[:count]
 
 
@@ -153,27 +194,31 @@ def lattice_offsets(r: int) -> torch.Tensor:
 def radius_neighbors(hashmap: HashMap, coords, r: int = 1) -> BatchResult:
     """find() of every lattice offset around each coordinate
     (geometry.py:87-99); results shaped (n, (2r+1)^3)."""
+    host = HashMap._is_host(coords)
     c = hashmap._check_keys(coords)
     offs = lattice_offsets(r).to(c.device)
     n, k = c.shape[0], offs.shape[0]
     q = (c[:, None, :] + offs[None, :, :]).reshape(n * k, 3)
     res = hashmap.find(q)
-    return BatchResult(res.indices.reshape(n, k), res.masks.reshape(n, k))
+    out = BatchResult(res.indices.reshape(n, k), res.masks.reshape(n, k))
+    return BatchResult(out.indices.cpu(), out.masks.cpu()) if host else out
 
 
 def set_intersection(keys_a, keys_b, backend: str = "generic", threads: int = 1,
                      device=None) -> torch.Tensor:
     """Rows of keys_b present in keys_a, duplicates kept (geometry.py:129-143)."""
     dev = _device(device)
+    host = HashMap._is_host(keys_b)
     a = torch.as_tensor(np.atleast_2d(np.asarray(keys_a, dtype=np.int32))) \
         if not isinstance(keys_a, torch.Tensor) else keys_a.to(torch.int32)
     b = torch.as_tensor(np.atleast_2d(np.asarray(keys_b, dtype=np.int32))) \
         if not isinstance(keys_b, torch.Tensor) else keys_b.to(torch.int32)
     a, b = a.to(dev), b.to(dev)
     if a.shape[0] == 0 or b.shape[0] == 0:
-        return b[:0]
+        return b[:0].cpu() if host else b[:0]
     if a.shape[1] != b.shape[1]:
         raise ValueError("key arity mismatch between the two sets")
     probe = HashSet(a.shape[0], a.shape[1], backend=backend, device=dev)
     probe.insert(a)
-    return b[probe.find(b).masks]
+    out = b[probe.find(b).masks]
+    return out.cpu() if host else out
