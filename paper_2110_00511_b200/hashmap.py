@@ -203,6 +203,10 @@ def _table_slots(capacity: int, factor: float = None) -> int:
 
 _SLOT_LIMIT = 0.75  # rebuild the table when non-EMPTY slots would pass this
 
+# device insert batches run as sequential chunks of this many positions
+# (0 = one batch); exact for insert, see HashMap._pipelined
+INSERT_CHUNK = int(os.environ.get("ASH_INSERT_CHUNK", "0"))
+
 
 class HashMap:
     """Batch-parallel map from fixed-arity int32 keys to value buffers, on a
@@ -592,9 +596,18 @@ class HashMap:
                 self._sync_size()
             free = self._capacity - self._top_ub
             if m <= free:
-                # the whole batch fits: fused path, no host synchronisation
-                call("ash_insert", self._ptr(), keys.data_ptr(), m, vptr, assoc,
-                     idx.data_ptr(), msk.data_ptr(), self._stream())
+                # the whole batch fits: fused path, no host synchronisation.
+                # insert (not activate) may run as sequential chunks with
+                # identical results (see _pipelined); a chunk's table lines
+                # then stay L2-resident between its claim and its commit.
+                c = INSERT_CHUNK if (not association and INSERT_CHUNK > 0) else m
+                for a in range(0, m, c):
+                    b = min(m, a + c)
+                    cp = vptr
+                    if vals:
+                        cp = (_lib.c_void_p * len(vals))(*[v[a:b].data_ptr() for v in vals])
+                    call("ash_insert", self._ptr(), keys[a:b].data_ptr(), b - a, cp, assoc,
+                         idx[a:b].data_ptr(), msk[a:b].data_ptr(), self._stream())
                 self._top_ub = min(self._capacity, self._top_ub + m)
                 break
             call("ash_insert_claim", self._ptr(), keys.data_ptr(), m, idx.data_ptr(),
