@@ -431,6 +431,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="force the hash-partitioned (torch.distributed) path even at N=1")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
     args = ap.parse_args()
@@ -444,7 +446,7 @@ def main():
         return
 
     import torch
-    if world > 1:
+    if world > 1 or args.partitioned:
         from paper_2110_00511_b200 import partitioned
         partitioned.bench_main(args, rank, world)
         return

@@ -201,6 +201,12 @@ def bench_main(args, rank: int, world: int) -> None:
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if "MASTER_ADDR" not in os.environ:  # plain `python bench.py --partitioned`
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]),
+                              RANK="0", WORLD_SIZE="1")
     dist.init_process_group("nccl", device_id=dev)
     per_rank = 10_000_000
     rho = 0.5
@@ -249,6 +255,9 @@ def bench_main(args, rank: int, world: int) -> None:
                                    f"int3 keys per rank per step (uniqueness {rho}), NCCL all-to-all "
                                    f"routing; step time = max over ranks",
                        "parallelism": f"hash-partitioned x{world}"},
-            "gpu_launches": None,
+            # per step: insert = partition (3) + key/value gathers (2) + shard
+            # claim/scan/commit (3) + un-permute (1) + owners (1); find =
+            # partition (3) + gather (1) + shard find (1) + un-permute (1) + owners (1)
+            "gpu_launches": 17 * args.steps,
         }), flush=True)
     dist.destroy_process_group()
