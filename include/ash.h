@@ -182,10 +182,14 @@ int ash_route_owner(const int32_t* keys, int64_t n, int32_t arity, int32_t world
 
 /* Stable partition of a batch by owner: perm lists positions grouped by
  * owner rank, batch order kept inside each group; counts[world] (int64) are
- * the group sizes (the all-to-all send splits). */
+ * the group sizes (the all-to-all send splits); owners[n] (uint8) the owner
+ * of every key.  The send buffers are written in the same pass: keys_out
+ * (n x arity, may be NULL) and one payload row per key (payload_row_bytes
+ * each; payload/payload_out both NULL for none). */
 int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t world,
-                        int32_t* perm, int64_t* counts, int32_t* scratch,
-                        int64_t scratch_len, void* stream);
+                        int32_t* perm, int64_t* counts, uint8_t* owners, int32_t* keys_out,
+                        const void* payload, int64_t payload_row_bytes, void* payload_out,
+                        int32_t* scratch, int64_t scratch_len, void* stream);
 
 /* dst[i] = src[idx[i]] and dst[idx[i]] = src[i] for rows of row_bytes. */
 int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "ash_route_scratch_len": (c_int64, [c_int64, c_int32]),
     "ash_route_owner": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "ash_route_partition": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                       c_void_p, c_int64, c_void_p]),
     "ash_gather_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ash_scatter_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),

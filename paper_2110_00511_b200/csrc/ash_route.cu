@@ -7,6 +7,11 @@
 // owner keep batch order, and NCCL all-to-all concatenates by source rank,
 // so every owner sees its keys in global batch order and first-occurrence
 // winners stay bit-exact (verified on the oracle in SURVEY §8(e)).
+//
+// One partition = three launches: count (owner per key -> uint8 + per-tile
+// per-owner counts), a one-block scan, and a scatter that writes the send
+// buffers directly (key rows + one payload row per key + the permutation),
+// so no separate gather pass touches the batch again.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -47,13 +52,16 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
 
 __device__ __forceinline__ uint32_t owner_of(const int32_t* row, int arity, uint32_t world) {
   uint64_t x = 0x243F6A8885A308D3ull ^ static_cast<uint64_t>(arity);
-  for (int d = 0; d < arity; ++d) x = fmix64(x ^ (static_cast<uint64_t>(static_cast<uint32_t>(row[d])) + 0x9E3779B97F4A7C15ull * (d + 1)));
+  for (int d = 0; d < arity; ++d)
+    x = fmix64(x ^ (static_cast<uint64_t>(static_cast<uint32_t>(__ldg(row + d))) + 0x9E3779B97F4A7C15ull * (d + 1)));
   return static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * world) >> 32);
 }
 
-// pass 1: per-tile, per-owner counts -> cnt[owner * n_tiles + tile]
+// pass 1: owner of every key (uint8) and per-tile, per-owner counts ->
+// cnt[owner * n_tiles + tile]
 __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restrict__ keys, int64_t n, int arity,
-                                                        uint32_t world, int32_t* __restrict__ cnt, int64_t n_tiles) {
+                                                        uint32_t world, uint8_t* __restrict__ owners,
+                                                        int32_t* __restrict__ cnt, int64_t n_tiles) {
   __shared__ int32_t s_cnt[kMaxWorld];
   for (int o = threadIdx.x; o < kMaxWorld; o += kBlock) s_cnt[o] = 0;
   __syncthreads();
@@ -61,7 +69,13 @@ __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restric
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    if (p < n) atomicAdd(&s_cnt[owner_of(keys + p * arity, arity, world)], 1);
+    if (p < n) {
+      const uint32_t o = owner_of(keys + p * arity, arity, world);
+      owners[p] = static_cast<uint8_t>(o);
+      // warp-aggregate the shared-memory increment per owner
+      const unsigned same = __match_any_sync(__activemask(), o);
+      if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_cnt[o], __popc(same));
+    }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < static_cast<int>(world); o += kBlock) cnt[o * n_tiles + blockIdx.x] = s_cnt[o];
@@ -103,7 +117,6 @@ __global__ void __launch_bounds__(1024) k_route_scan(int32_t* cnt, int64_t len, 
     if (threadIdx.x == 1023) carry = c + warp_tot[warp] + incl;
     __syncthreads();
   }
-  // per-owner totals from the scanned offsets
   for (uint32_t o = threadIdx.x; o < world; o += 1024) {
     const int64_t start = cnt[o * n_tiles];
     const int64_t end = (o + 1 < world) ? cnt[(o + 1) * n_tiles] : carry;
@@ -111,12 +124,25 @@ __global__ void __launch_bounds__(1024) k_route_scan(int32_t* cnt, int64_t len, 
   }
 }
 
-// pass 3: stable scatter of positions: perm[offset(owner, tile) + rank] = p.
-// Position order inside a tile is (item, warp, lane); per-owner group sizes
-// come from __match_any_sync and are scanned per owner in that order.
+__device__ __forceinline__ void copy_row_words(uint8_t* dst, const uint8_t* src, int64_t rb) {
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | rb) & 3) == 0) {
+    for (int64_t i = 0; i < rb; i += 4)
+      *reinterpret_cast<uint32_t*>(dst + i) = __ldg(reinterpret_cast<const uint32_t*>(src + i));
+  } else {
+    for (int64_t i = 0; i < rb; ++i) dst[i] = src[i];
+  }
+}
+
+// pass 3: stable scatter.  Destination of position p = offset(owner, tile) +
+// rank of p among the tile's positions with that owner, in (item, warp,
+// lane) = position order.  Writes perm[dst] = p, the key row and one payload
+// row at dst.
 __global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restrict__ keys, int64_t n, int arity,
-                                                          uint32_t world, const int32_t* __restrict__ off,
-                                                          int64_t n_tiles, int32_t* __restrict__ perm) {
+                                                          uint32_t world, const uint8_t* __restrict__ owners,
+                                                          const int32_t* __restrict__ off, int64_t n_tiles,
+                                                          int32_t* __restrict__ perm, int32_t* __restrict__ keys_out,
+                                                          const uint8_t* __restrict__ pay, int64_t pay_rb,
+                                                          uint8_t* __restrict__ pay_out) {
   constexpr int kW = kBlock / 32;
   __shared__ int32_t s_pre[kItems][kW][kMaxWorld];
   const int warp = threadIdx.x >> 5;
@@ -129,7 +155,7 @@ __global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restr
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+    own[it] = p < n ? owners[p] : 0xFFFFFFFFu;
     const unsigned same = __match_any_sync(0xFFFFFFFFu, own[it]);
     rank_in_warp[it] = __popc(same & lt);
     if (p < n && (same & lt) == 0) s_pre[it][warp][own[it]] = __popc(same);
@@ -148,41 +174,26 @@ __global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restr
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    if (p < n) perm[s_pre[it][warp][own[it]] + rank_in_warp[it]] = static_cast<int32_t>(p);
+    if (p >= n) continue;
+    const int64_t dst = s_pre[it][warp][own[it]] + rank_in_warp[it];
+    perm[dst] = static_cast<int32_t>(p);
+    if (keys_out)
+      for (int d = 0; d < arity; ++d) keys_out[dst * arity + d] = __ldg(keys + p * arity + d);
+    if (pay_out) copy_row_words(pay_out + dst * pay_rb, pay + p * pay_rb, pay_rb);
   }
 }
 
+// dst[i] = src[idx[i]] (gather) / dst[idx[i]] = src[i] (scatter): thread per row
 __global__ void k_gather_rows(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
-                              int64_t words, uint32_t* __restrict__ dst) {
-  // row bytes multiple of 4: thread per (row, word)
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= n * words) return;
-  const int64_t r = t / words, w = t - r * words;
-  dst[t] = reinterpret_cast<const uint32_t*>(src)[static_cast<int64_t>(idx[r]) * words + w];
+                              int64_t rb, uint8_t* __restrict__ dst) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) copy_row_words(dst + i * rb, src + static_cast<int64_t>(__ldg(idx + i)) * rb, rb);
 }
 
-__global__ void k_gather_bytes(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+__global__ void k_scatter_rows(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                                int64_t rb, uint8_t* __restrict__ dst) {
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= n * rb) return;
-  const int64_t r = t / rb, b = t - r * rb;
-  dst[t] = src[static_cast<int64_t>(idx[r]) * rb + b];
-}
-
-__global__ void k_scatter_rows(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
-                               int64_t words, uint8_t* __restrict__ dst) {
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= n * words) return;
-  const int64_t r = t / words, w = t - r * words;
-  reinterpret_cast<uint32_t*>(dst)[static_cast<int64_t>(idx[r]) * words + w] = src[t];
-}
-
-__global__ void k_scatter_bytes(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
-                                int64_t rb, uint8_t* __restrict__ dst) {
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= n * rb) return;
-  const int64_t r = t / rb, b = t - r * rb;
-  dst[static_cast<int64_t>(idx[r]) * rb + b] = src[t];
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) copy_row_words(dst + static_cast<int64_t>(__ldg(idx + i)) * rb, src + i * rb, rb);
 }
 
 __global__ void k_owner_of(const int32_t* __restrict__ keys, int64_t n, int arity, uint32_t world,
@@ -215,9 +226,14 @@ int ash_route_owner(const int32_t* keys, int64_t n, int32_t arity, int32_t world
 }
 
 int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int32_t* perm,
-                        int64_t* counts, int32_t* scratch, int64_t scratch_len, void* stream) {
+                        int64_t* counts, uint8_t* owners, int32_t* keys_out, const void* payload,
+                        int64_t payload_row_bytes, void* payload_out, int32_t* scratch, int64_t scratch_len,
+                        void* stream) {
   if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
   if (n >= (int64_t(1) << 31)) return rfail("routing batch too long");
+  if (!perm || !counts || !owners) return rfail("null routing output");
+  if ((payload == nullptr) != (payload_out == nullptr) || payload_row_bytes < 0)
+    return rfail("payload and payload_out must both be given");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n_tiles = (n + kTile - 1) / kTile;
   if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
@@ -226,35 +242,27 @@ int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t w
     return rcheck("ash_route_partition");
   }
   const uint32_t w = static_cast<uint32_t>(world);
-  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, scratch, n_tiles);
+  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, owners, scratch, n_tiles);
   k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts);
-  k_route_scatter<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, scratch, n_tiles, perm);
+  k_route_scatter<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(
+      keys, n, arity, w, owners, scratch, n_tiles, perm, keys_out, static_cast<const uint8_t*>(payload),
+      payload_row_bytes, static_cast<uint8_t*>(payload_out));
   return rcheck("ash_route_partition");
 }
 
 int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
   if (n < 0 || row_bytes < 0) return rfail("bad gather arguments");
   if (n == 0 || row_bytes == 0) return ASH_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (row_bytes % 4 == 0)
-    k_gather_rows<<<blocks(n * (row_bytes / 4), kBlock), kBlock, 0, s>>>(
-        static_cast<const uint8_t*>(src), idx, n, row_bytes / 4, static_cast<uint32_t*>(dst));
-  else
-    k_gather_bytes<<<blocks(n * row_bytes, kBlock), kBlock, 0, s>>>(static_cast<const uint8_t*>(src), idx, n,
-                                                                    row_bytes, static_cast<uint8_t*>(dst));
+  k_gather_rows<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst));
   return rcheck("ash_gather_rows");
 }
 
 int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
   if (n < 0 || row_bytes < 0) return rfail("bad scatter arguments");
   if (n == 0 || row_bytes == 0) return ASH_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (row_bytes % 4 == 0)
-    k_scatter_rows<<<blocks(n * (row_bytes / 4), kBlock), kBlock, 0, s>>>(
-        static_cast<const uint32_t*>(src), idx, n, row_bytes / 4, static_cast<uint8_t*>(dst));
-  else
-    k_scatter_bytes<<<blocks(n * row_bytes, kBlock), kBlock, 0, s>>>(static_cast<const uint8_t*>(src), idx, n,
-                                                                     row_bytes, static_cast<uint8_t*>(dst));
+  k_scatter_rows<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst));
   return rcheck("ash_scatter_rows");
 }
 

@@ -31,7 +31,7 @@ __all__ = ["PartitionedHashMap", "PartitionedResult", "CudaRouter"]
 class PartitionedResult:
     indices: torch.Tensor  # owner-local buffer index, -1 where masks is False
     masks: torch.Tensor
-    owners: torch.Tensor   # owner rank of every key
+    owners: torch.Tensor   # owner rank of every key (uint8)
 
     def __iter__(self):
         return iter((self.indices, self.masks))
@@ -59,17 +59,27 @@ class CudaRouter:
                        out.data_ptr(), self._stream())
         return out
 
-    def plan(self, keys: torch.Tensor):
+    def plan(self, keys: torch.Tensor, payloads=()):
+        """Partition by owner and build the send buffers in one pass.
+        Returns (perm, counts, owners, send_keys, send_payloads)."""
         n = keys.shape[0]
         need = int(self._lib.lib.ash_route_scratch_len(n, self.world))
         if self._scratch.numel() < need:
             self._scratch = torch.empty(max(need, 1), dtype=torch.int32, device=self.device)
         perm = torch.empty(n, dtype=torch.int32, device=self.device)
         counts = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        owners = torch.empty(n, dtype=torch.uint8, device=self.device)
+        send_keys = torch.empty_like(keys)
+        first = payloads[0].contiguous() if payloads else None
+        send_first = torch.empty_like(first) if first is not None else None
+        rb = first[0].numel() * first.element_size() if (first is not None and n) else 0
         self._lib.call("ash_route_partition", keys.data_ptr(), n, keys.shape[1], self.world,
-                       perm.data_ptr(), counts.data_ptr(), self._scratch.data_ptr(),
-                       self._scratch.numel(), self._stream())
-        return perm, counts
+                       perm.data_ptr(), counts.data_ptr(), owners.data_ptr(), send_keys.data_ptr(),
+                       first.data_ptr() if first is not None else None, rb,
+                       send_first.data_ptr() if send_first is not None else None,
+                       self._scratch.data_ptr(), self._scratch.numel(), self._stream())
+        sends = ([send_first] if first is not None else []) + [self.gather(p, perm) for p in payloads[1:]]
+        return perm, counts, owners, send_keys, sends
 
     def gather(self, src: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
         src = src.contiguous()
@@ -115,16 +125,16 @@ class PartitionedHashMap:
         return recv
 
     def _forward(self, keys: torch.Tensor, payloads=()):
-        perm, send_counts = self.router.plan(keys)
+        perm, send_counts, owners, skeys, spay = self.router.plan(keys, list(payloads))
         recv_counts = torch.empty_like(send_counts)
         dist.all_to_all_single(recv_counts, send_counts, group=self.group)
         ss, rs = send_counts.tolist(), recv_counts.tolist()
-        rkeys = self._a2a(self.router.gather(keys, perm), ss, rs)
-        rpay = [self._a2a(self.router.gather(p, perm), ss, rs) for p in payloads]
-        return rkeys, rpay, (perm, ss, rs)
+        rkeys = self._a2a(skeys, ss, rs)
+        rpay = [self._a2a(p, ss, rs) for p in spay]
+        return rkeys, rpay, (perm, ss, rs, owners)
 
     def _backward(self, local_out: torch.Tensor, ctx) -> torch.Tensor:
-        perm, ss, rs = ctx
+        perm, ss, rs, _ = ctx
         back = self._a2a(local_out.contiguous(), rs, ss)
         return self.router.scatter(back, perm)
 
@@ -146,9 +156,9 @@ class PartitionedHashMap:
                        t.reshape(0, *t.shape[1:]).to(self.device))
         return out
 
-    def _result(self, keys, idx) -> PartitionedResult:
+    def _result(self, idx, ctx) -> PartitionedResult:
         idx = idx.reshape(-1)
-        return PartitionedResult(idx, idx >= 0, self.router.owners(keys))
+        return PartitionedResult(idx, idx >= 0, ctx[3])
 
     # -- operations --------------------------------------------------------
 
@@ -157,19 +167,19 @@ class PartitionedHashMap:
         vals = self._values(keys.shape[0], values)
         rkeys, rvals, ctx = self._forward(keys, vals)
         res = self.local.insert(rkeys, *rvals)  # the shard reshapes (n, -1) rows itself
-        return self._result(keys, self._backward(torch.as_tensor(res.indices), ctx))
+        return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def activate(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
         rkeys, _, ctx = self._forward(keys)
         res = self.local.activate(rkeys)
-        return self._result(keys, self._backward(torch.as_tensor(res.indices), ctx))
+        return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def find(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
         rkeys, _, ctx = self._forward(keys)
         res = self.local.find(rkeys)
-        return self._result(keys, self._backward(torch.as_tensor(res.indices), ctx))
+        return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def erase(self, keys) -> torch.Tensor:
         keys = self._keys(keys)

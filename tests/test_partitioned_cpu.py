@@ -44,11 +44,12 @@ class NumpyRouter:
     def owners(self, keys):
         return torch.from_numpy(owner_of_np(keys.numpy(), self.world))
 
-    def plan(self, keys):
+    def plan(self, keys, payloads=()):
         own = owner_of_np(keys.numpy(), self.world)
-        perm = np.argsort(own, kind="stable").astype(np.int32)
+        perm = torch.from_numpy(np.argsort(own, kind="stable").astype(np.int32))
         counts = np.bincount(own, minlength=self.world).astype(np.int64)
-        return torch.from_numpy(perm), torch.from_numpy(counts)
+        return (perm, torch.from_numpy(counts), torch.from_numpy(own.astype(np.uint8)),
+                self.gather(keys, perm), [self.gather(p, perm) for p in payloads])
 
     def gather(self, src, perm):
         return src[perm.long()].contiguous()

@@ -27,9 +27,16 @@ def test_partition_is_stable_owner_sort(router_cls, world, n):
     kt = torch.from_numpy(k).cuda()
     own = owner_of_np(k, world)
     assert np.array_equal(r.owners(kt).cpu().numpy(), own)
-    perm, counts = r.plan(kt)
-    assert np.array_equal(perm.cpu().numpy(), np.argsort(own, kind="stable"))
+    pay = torch.from_numpy(rng.integers(0, 2 ** 31, size=(n, 5)).astype(np.int32)).cuda()
+    pay2 = torch.from_numpy(rng.integers(0, 255, size=(n, 3)).astype(np.uint8)).cuda()
+    perm, counts, owners, skeys, spay = r.plan(kt, [pay, pay2])
+    order = np.argsort(own, kind="stable")
+    assert np.array_equal(perm.cpu().numpy(), order)
     assert np.array_equal(counts.cpu().numpy(), np.bincount(own, minlength=world))
+    assert np.array_equal(owners.cpu().numpy(), own.astype(np.uint8))
+    assert np.array_equal(skeys.cpu().numpy(), k[order])
+    assert np.array_equal(spay[0].cpu().numpy(), pay.cpu().numpy()[order])
+    assert np.array_equal(spay[1].cpu().numpy(), pay2.cpu().numpy()[order])
     if n:
         g = r.gather(kt, perm)
         assert np.array_equal(g.cpu().numpy(), k[np.argsort(own, kind="stable")])
