@@ -231,16 +231,17 @@ int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t w
                         void* stream) {
   if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
   if (n >= (int64_t(1) << 31)) return rfail("routing batch too long");
-  if (!perm || !counts || !owners) return rfail("null routing output");
-  if ((payload == nullptr) != (payload_out == nullptr) || payload_row_bytes < 0)
-    return rfail("payload and payload_out must both be given");
+  if (!counts) return rfail("null routing output");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t n_tiles = (n + kTile - 1) / kTile;
-  if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
-  if (n == 0) {
+  if (n == 0) {  // empty tensors may carry null pointers
     cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, s);
     return rcheck("ash_route_partition");
   }
+  if (!perm || !owners || !scratch) return rfail("null routing output");
+  if ((payload == nullptr) != (payload_out == nullptr) || payload_row_bytes < 0)
+    return rfail("payload and payload_out must both be given");
+  const int64_t n_tiles = (n + kTile - 1) / kTile;
+  if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
   const uint32_t w = static_cast<uint32_t>(world);
   k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, owners, scratch, n_tiles);
   k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts);
