@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ASH_ABI_VERSION 1
+#define ASH_ABI_VERSION 2
 
 #define ASH_OK 0
 #define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
@@ -44,6 +44,7 @@ extern "C" {
 #define ASH_CTR_FLAGS 4    /* sticky error bits, see ASH_FLAG_*            */
 #define ASH_CTR_COUNT 5    /* result count of the last compaction/voxelize */
 #define ASH_CTR_TOP_BASE 6 /* heap top at the start of the current commit   */
+#define ASH_CTR_HEAP_DIRTY 7 /* heap[i] == i for every i >= this value     */
 #define ASH_N_COUNTERS 8
 
 #define ASH_FLAG_TABLE_FULL 1  /* a probe wrapped the whole table */
@@ -72,10 +73,14 @@ typedef struct ash_map {
   uint64_t* scan_status;    /* single-pass scan tile status, zeroed once       */
   int64_t scan_status_len;  /* >= ash_scan_tiles(max(n, capacity))             */
   int32_t* tile_counts;     /* per-2048-position winner counts, zero between   */
-  int64_t tile_counts_len;  /* batches; >= ash_scan_tiles(n)                   */
+  int64_t tile_counts_len;  /* batches; >= ash_scan_tiles(n); with H =        */
+                            /* (len-1)/2 >= tiles, inserts count in [0, H) and */
+                            /* keep the tile prefixes in [H, 2H]               */
   int64_t capacity;         /* <= 2^31 - 1                                     */
   uint32_t epoch;           /* scan epoch; the library bumps it per launch     */
   uint32_t reserved;
+  int32_t* rank_words;      /* optional: 2 x ceil(n / 32) int32, lets the     */
+  int64_t rank_words_len;   /* table-sweep commit rank winners without tmp    */
 } ash_map_t;
 
 int ash_abi_version(void);
@@ -89,6 +94,15 @@ int ash_device_setup(int32_t l2_fetch_bytes);
 /* Mark batch streams (keys, values, scratch, outputs) L2 evict-first so the
  * table keeps the L2 (default on; process-wide). */
 int ash_set_stream_hints(int32_t on);
+
+/* Insert commit strategy (process-wide; same results in every mode).
+ *   bulk = 1: TMA-staged persistent commit where the batch qualifies (arity
+ *             <= 3, one register-sized value buffer or none, 16-byte aligned
+ *             streams, tile workspace >= 2 * tiles + 1); 0: plain commit.
+ *   sweep_div > 0: batches with >= n_buckets / sweep_div winners commit the
+ *             slot states in one sequential table pass instead of random
+ *             stores; 0: never.  Defaults: 1, 5. */
+int ash_set_commit_mode(int32_t bulk, int32_t sweep_div);
 
 /* Scan-status words needed for a single-pass scan over n items. */
 int64_t ash_scan_tiles(int64_t n);

@@ -14,6 +14,7 @@ from .build import LIB_PATH
 ASH_OK, ASH_ERR_INVALID, ASH_ERR_CAPACITY, ASH_ERR_CUDA = 0, 1, 2, 3
 MAX_VALUE_BUFFERS = 8
 CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT, CTR_TOP_BASE = 0, 1, 2, 3, 4, 5, 6
+CTR_HEAP_DIRTY = 7
 N_COUNTERS = 8
 FLAG_TABLE_FULL, FLAG_RANGE = 1, 2
 TILE = 2048  # positions per scan tile (csrc kTile)
@@ -31,6 +32,7 @@ class AshMap(ctypes.Structure):
         ("scan_status_len", c_int64), ("tile_counts", c_void_p), ("tile_counts_len", c_int64),
         ("capacity", c_int64),
         ("epoch", c_uint32), ("reserved", c_uint32),
+        ("rank_words", c_void_p), ("rank_words_len", c_int64),
     ]
 
 
@@ -40,6 +42,7 @@ _SIGNATURES = {
     "ash_last_error": (c_char_p, []),
     "ash_device_setup": (c_int32, [c_int32]),
     "ash_set_stream_hints": (c_int32, [c_int32]),
+    "ash_set_commit_mode": (c_int32, [c_int32, c_int32]),
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -80,13 +83,15 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ash_abi_version() != 1:
+    if lib.ash_abi_version() != 2:
         raise ImportError("libash.so ABI version mismatch; rebuild")
     return lib
 
 
 lib = _load()
 lib.ash_set_stream_hints(int(_os.environ.get("ASH_STREAM_HINTS", "1")))
+lib.ash_set_commit_mode(int(_os.environ.get("ASH_COMMIT_BULK", "1")),
+                        int(_os.environ.get("ASH_SWEEP_DIV", "5")))
 
 
 class AshError(RuntimeError):

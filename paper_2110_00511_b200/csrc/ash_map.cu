@@ -764,8 +764,10 @@ __device__ __forceinline__ void tile_scan_known(const bool (&flag)[kItems], uint
 // batch's winner total (what the capacity check needs).
 constexpr int kScanBlock = 1024;
 
+// With pre_out, the exclusive prefixes (plus the total at [n_tiles]) go to
+// pre_out and the counts are zeroed in place for the next batch.
 __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int64_t n_tiles, int32_t* counters,
-                                                          int top_slot, int total_slot) {
+                                                          int top_slot, int total_slot, int32_t* pre_out) {
   __shared__ int32_t warp_tot[kScanBlock / 32];
   __shared__ int32_t carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -794,7 +796,14 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int
     }
     __syncthreads();
     const int32_t c = carry;
-    if (i < n_tiles) tile_cnt[i] = c + warp_tot[warp] + incl - x;
+    if (i < n_tiles) {
+      if (pre_out) {
+        pre_out[i] = c + warp_tot[warp] + incl - x;
+        tile_cnt[i] = 0;
+      } else {
+        tile_cnt[i] = c + warp_tot[warp] + incl - x;
+      }
+    }
     __syncthreads();
     if (threadIdx.x == kScanBlock - 1) carry = c + warp_tot[warp] + incl;
     __syncthreads();
@@ -802,6 +811,7 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int
   if (threadIdx.x == 0) {
     if (top_slot >= 0) counters[top_slot] = counters[ASH_CTR_TOP];
     counters[total_slot] = carry;
+    if (pre_out) pre_out[n_tiles] = carry;
   }
 }
 
@@ -856,11 +866,15 @@ __global__ void __launch_bounds__(kBlock)
     k_commit(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
              uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
-             int32_t* tile_pre) {
+             int32_t* tile_pre, int64_t sweep_min, int32_t* __restrict__ rank_words) {
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * kTile;
   const uint64_t pol = stream_policy(t.hints);
+  // large batches leave the slot states to k_commit_sweep (see there); the
+  // winners' indices in tmp must then stay L2-resident for it
+  const bool defer = ld_volatile_i32(counters + ASH_CTR_WINNERS) >= sweep_min;
+  const uint64_t tpol = defer && !rank_words ? stream_policy(0) : pol;
   int32_t v[kItems];
   uint8_t mk[kItems];
   bool win[kItems];
@@ -875,6 +889,15 @@ __global__ void __launch_bounds__(kBlock)
   for (int it = 0; it < kItems; ++it) win[it] = v[it] < 0 && !(mk[it] & DEMOTED);
   uint32_t bal[kItems];
   tile_scan_known(win, bal, sm, tile_pre, tile, counters + ASH_CTR_TOP_BASE);
+  if (defer && rank_words && (threadIdx.x & 31) == 0) {
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t w0 = base + it * kBlock + warp * 32;
+      if (w0 < n)
+        reinterpret_cast<uint2*>(rank_words)[w0 >> 5] = make_uint2(bal[it], sm.prefix + sm.pre[it * kWarps + warp]);
+    }
+  }
   const int arity = A ? A : t.arity;
   // phase 1: every load of every winner (heap index, key words, value row)
   // before any store, so each thread keeps kItems x several loads in flight
@@ -900,7 +923,7 @@ __global__ void __launch_bounds__(kBlock)
     if (win[it]) {
       const int32_t idx = hidx[it];
       const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
-      t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+      if (!defer) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
       int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
@@ -915,7 +938,7 @@ __global__ void __launch_bounds__(kBlock)
           if (b < va.n) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
       }
       active[idx] = 1;
-      st_stream(tmp + p, static_cast<uint32_t>(idx), pol);
+      st_stream(tmp + p, static_cast<uint32_t>(idx), tpol);
       st_stream_u8(mask + p, 1, pol);
     } else if (v[it] >= 0) {
       st_stream(tmp + p, static_cast<uint32_t>(assoc ? v[it] : -1), pol);
@@ -929,6 +952,327 @@ __global__ void __launch_bounds__(kBlock)
   // publish the new top
   if (tile == 0 && threadIdx.x == 0)
     counters[ASH_CTR_TOP] = static_cast<int32_t>(sm.base) + ld_volatile_i32(counters + ASH_CTR_WINNERS);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged commit (persistent, warp-specialised).
+//
+// The plain k_commit is latency bound (ncu r01g: ~40% of stall samples wait
+// on the first scratch loads, ~15% on the heap/key/value loads behind the
+// tile scan; 3 blocks/SM at 80 registers).  Every per-tile input of the
+// commit is a contiguous byte range: the scratch index/mask words, the key
+// rows, small value rows, and the tile's heap segment
+// heap[top + pre[t] .. top + pre[t+1]).  A producer warp streams them into
+// shared memory with cp.async.bulk (TMA 1-D) two tiles ahead, completion on an
+// mbarrier; eight consumer warps rank the winners and issue only stores.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-byte
+// aligned), completion counted on `bar`; L2 evict-first (read-once stream)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Copy `bytes` from src to dst: the 16-byte multiple through the bulk engine,
+// the tail (< 16 bytes) by the calling thread.  Returns the bulk byte count.
+__device__ __forceinline__ uint32_t stage_range(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                uint64_t pol) {
+  const uint32_t main = bytes & ~15u;
+  if (main) bulk_g2s(dst, src, main, bar, pol);
+  if ((bytes & 3) == 0) {
+    for (uint32_t b = main; b < bytes; b += 4)
+      *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dst) + b) =
+          __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(src) + b));
+  } else {
+    for (uint32_t b = main; b < bytes; ++b)
+      static_cast<uint8_t*>(dst)[b] = __ldg(static_cast<const uint8_t*>(src) + b);
+  }
+  return main;
+}
+
+constexpr int kCommitConsumers = kBlock;             // 8 consumer warps
+constexpr int kCommitThreads = kBlock + 32;          // + 1 producer warp
+constexpr int kCommitStages = 2;
+
+__host__ __device__ constexpr uint32_t align128(uint32_t x) { return (x + 127u) & ~127u; }
+
+// Per-stage shared layout for arity A (inline keys) and SV staged value words.
+template <int A, int SV>
+struct CommitStage {
+  static constexpr uint32_t kTmp = 0;
+  static constexpr uint32_t kMask = align128(kTmp + kTile * 4);
+  static constexpr uint32_t kKeys = align128(kMask + kTile);
+  static constexpr uint32_t kVals = align128(kKeys + kTile * A * 4);
+  static constexpr uint32_t kHeap = align128(kVals + kTile * SV * 4);
+  static constexpr uint32_t kBytes = align128(kHeap + (kTile + 8) * 4);
+};
+
+struct CommitStageInfo {
+  int32_t heap_off;  // s_heap index of this tile's first winner
+  int32_t rows;
+  uint32_t pre;      // winners before this tile
+};
+
+// SV = value words staged through shared memory (VW when VW <= 4, else 0:
+// 32-byte rows are loaded per winner, issued before the tile scan).
+template <int A, int VW>
+__global__ void __launch_bounds__(kCommitThreads)
+    k_commit_bulk(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
+                  int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
+                  int64_t capacity, uint8_t* __restrict__ active, int32_t* __restrict__ key_buf,
+                  int32_t* counters, const int32_t* __restrict__ tile_pre, int64_t n_tiles,
+                  int64_t sweep_min, int32_t* __restrict__ rank_words) {
+  constexpr int SV = (VW > 0 && VW <= 4) ? VW : 0;
+  using L = CommitStage<A, SV>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kCommitStages], empty[kCommitStages];
+  __shared__ CommitStageInfo info[kCommitStages];
+  __shared__ ScanSmem sm;
+  __shared__ uint32_t s_top;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol = stream_policy(t.hints);
+  const bool defer = ld_volatile_i32(counters + ASH_CTR_WINNERS) >= sweep_min;  // see k_commit_sweep
+  const uint64_t tpol = defer && !rank_words ? stream_policy(0) : pol;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kCommitStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCommitConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
+  }
+  __syncthreads();
+  const uint32_t top = s_top;
+
+  if (warp == kCommitConsumers / 32) {
+    // ---------------- producer warp (lane 0 issues) ----------------
+    if (lane == 0) {
+      int i = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+        const int s = i & 1;
+        if (i >= kCommitStages) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        uint8_t* st = smem + s * L::kBytes;
+        const int64_t base = tile * kTile;
+        const uint32_t rows = static_cast<uint32_t>(n - base < kTile ? n - base : kTile);
+        const uint32_t pre = static_cast<uint32_t>(__ldg(tile_pre + tile));
+        const uint32_t nxt = static_cast<uint32_t>(__ldg(tile_pre + tile + 1));
+        const uint32_t hs = top + pre, he = top + nxt;
+        const uint32_t hs_al = hs & ~3u;
+        info[s].heap_off = static_cast<int32_t>(hs - hs_al);
+        info[s].rows = static_cast<int32_t>(rows);
+        info[s].pre = pre;
+        uint32_t tx = 0;
+        tx += stage_range(st + L::kTmp, tmp + base, rows * 4, &full[s], pol);
+        tx += stage_range(st + L::kMask, mask + base, rows, &full[s], pol);
+        tx += stage_range(st + L::kKeys, keys + base * A, rows * A * 4, &full[s], pol);
+        if (SV) tx += stage_range(st + L::kVals, va.src[0] + base * SV * 4, rows * SV * 4, &full[s], pol);
+        if (he > hs) tx += stage_range(st + L::kHeap, heap + hs_al, (he - hs_al) * 4, &full[s], pol);
+        (void)capacity;
+        mbar_arrive_expect_tx(&full[s], tx);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int arity = A;
+  int i = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
+    const int s = i & 1;
+    mbar_wait(&full[s], (i >> 1) & 1);
+    const uint8_t* st = smem + s * L::kBytes;
+    const int32_t* s_tmp = reinterpret_cast<const int32_t*>(st + L::kTmp);
+    const uint8_t* s_mask = st + L::kMask;
+    const uint32_t* s_keys = reinterpret_cast<const uint32_t*>(st + L::kKeys);
+    const uint32_t* s_vals = reinterpret_cast<const uint32_t*>(st + L::kVals);
+    const int32_t* s_heap = reinterpret_cast<const int32_t*>(st + L::kHeap);
+    const int rows = info[s].rows;
+    const int heap_off = info[s].heap_off;
+    const int64_t base = tile * kTile;
+
+    int32_t v[kItems];
+    bool win[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int r = it * kBlock + threadIdx.x;
+      v[it] = r < rows ? s_tmp[r] : 0;
+      win[it] = r < rows && v[it] < 0 && !(s_mask[r] & DEMOTED);
+    }
+    RowWords<(VW > 4 ? VW : 1)> grow[kItems];
+    if (VW > 4) {  // large rows: per-winner loads, in flight across the scan
+#pragma unroll
+      for (int it = 0; it < kItems; ++it)
+        if (win[it])
+          load_row<(VW > 4 ? VW : 1)>(grow[it], va.src[0] + (base + it * kBlock + threadIdx.x) * VW * 4, pol);
+    }
+    // in-tile ranks (ballots + one warp scan; consumer-only named barrier)
+    uint32_t bal[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      bal[it] = __ballot_sync(0xFFFFFFFFu, win[it]);
+      if (lane == 0) sm.cnt[it * kWarps + warp] = __popc(bal[it]);
+    }
+    named_sync(1, kCommitConsumers);
+    if (warp == 0) {
+      const uint32_t e0 = sm.cnt[2 * lane], e1 = sm.cnt[2 * lane + 1];
+      uint32_t incl = e0 + e1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - e0 - e1;
+      sm.pre[2 * lane] = excl;
+      sm.pre[2 * lane + 1] = excl + e0;
+    }
+    named_sync(1, kCommitConsumers);
+    if (defer && rank_words && lane == 0) {
+      const uint32_t tpre = info[s].pre;
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int r0 = it * kBlock + warp * 32;
+        if (r0 < rows)
+          reinterpret_cast<uint2*>(rank_words)[(base + r0) >> 5] =
+              make_uint2(bal[it], tpre + sm.pre[it * kWarps + warp]);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int r = it * kBlock + threadIdx.x;
+      if (r >= rows) continue;
+      const int64_t p = base + r;
+      if (win[it]) {
+        const uint32_t rank = sm.pre[it * kWarps + warp] + __popc(bal[it] & lanemask_lt());
+        const int32_t idx = s_heap[heap_off + rank];
+        const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
+        if (!defer) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+        int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
+#pragma unroll
+        for (int d = 0; d < A; ++d) st_stream(dr + d, s_keys[r * A + d], pol);
+        if (SV) {
+          RowWords<(SV ? SV : 1)> row;
+          if (SV == 4) {
+            const uint4 q = reinterpret_cast<const uint4*>(s_vals)[r];
+            row.w[0] = q.x, row.w[(SV > 1) ? 1 : 0] = q.y, row.w[(SV > 2) ? 2 : 0] = q.z, row.w[(SV > 3) ? 3 : 0] = q.w;
+          } else if (SV == 2) {
+            const uint2 q = reinterpret_cast<const uint2*>(s_vals)[r];
+            row.w[0] = q.x, row.w[(SV > 1) ? 1 : 0] = q.y;
+          } else {
+#pragma unroll
+            for (int w = 0; w < SV; ++w) row.w[w] = s_vals[r * SV + w];
+          }
+          store_row<(SV ? SV : 1)>(va.dst[0] + static_cast<int64_t>(idx) * SV * 4, row, pol);
+        } else if (VW > 4) {
+          store_row<(VW > 4 ? VW : 1)>(va.dst[0] + static_cast<int64_t>(idx) * VW * 4, grow[it], pol);
+        }
+        active[idx] = 1;
+        st_stream(tmp + p, static_cast<uint32_t>(idx), tpol);
+        st_stream_u8(mask + p, 1, pol);
+      } else if (v[it] >= 0) {
+        st_stream(tmp + p, static_cast<uint32_t>(assoc ? v[it] : -1), pol);
+        st_stream_u8(mask + p, assoc ? 1 : 0, pol);
+      } else {
+        st_stream(tmp + p, 0xFFFFFFFFu, pol);
+        st_stream_u8(mask + p, 0, pol);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    counters[ASH_CTR_TOP] = static_cast<int32_t>(top) + ld_volatile_i32(counters + ASH_CTR_WINNERS);
+}
+
+// Slot-state commit as one sequential pass over the table.  A random 4-byte
+// store into a sector that left the L2 since the claim costs a DRAM fill plus
+// a write-back (HBM3e has no write mask), ~20 G stores/s measured; streaming
+// the whole table through the L2 costs n_buckets x 32 B of reads plus the
+// dirty sectors.  When the batch has at least sweep_min winners, the commit
+// skips the slot stores and this pass turns every PENDING|pos slot into the
+// index of winner pos: top + rank(pos) (heap[top + rank] once frees have
+// touched the heap above top), the rank from the per-32-position winner bits
+// and prefixes the commit wrote to rank_words (2.5 MB at 10M positions, L2
+// resident); without rank_words, the index the commit wrote to tmp[pos].
+__global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t* __restrict__ tmp,
+                                                         const int32_t* __restrict__ rank_words,
+                                                         const int32_t* __restrict__ heap,
+                                                         const int32_t* counters, int64_t sweep_min) {
+  if (ld_volatile_i32(counters + ASH_CTR_WINNERS) < sweep_min) return;
+  const uint32_t stride = gridDim.x * kBlock;
+  const uint32_t top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
+  // fresh heap region (no frees at or above top): index = top + rank
+  const bool ident = ld_volatile_i32(counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(top);
+  constexpr int U = 2;  // buckets per thread per round; all loads of a round issued together
+  for (uint32_t b0 = blockIdx.x * kBlock + threadIdx.x; b0 < t.n_buckets; b0 += U * stride) {
+    uint32_t w[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t b = b0 + u * stride;
+      if (b < t.n_buckets) ld256_nc(t.slots + 2 * static_cast<size_t>(b), w[u]);
+      else w[u][3] = w[u][7] = EMPTY;
+    }
+    uint32_t idx[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const uint32_t st = w[u][4 * s + 3];
+        if ((st & 0xC0000000u) != PEND) continue;  // not PENDING (EMPTY / TOMB have both top bits)
+        const uint32_t j = st & ~PEND;
+        if (rank_words) {
+          const uint2 rw = __ldg(reinterpret_cast<const uint2*>(rank_words) + (j >> 5));
+          idx[u][s] = rw.y + __popc(rw.x & ((1u << (j & 31)) - 1u));  // rank
+        } else {
+          idx[u][s] = static_cast<uint32_t>(__ldg(tmp + j));
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const uint32_t st = w[u][4 * s + 3];
+        if ((st & 0xC0000000u) != PEND) continue;
+        uint32_t v = idx[u][s];
+        if (rank_words) v = ident ? top + v : static_cast<uint32_t>(__ldg(heap + top + v));
+        t.slots[2 * static_cast<size_t>(b0 + u * stride) + s].w = v;
+      }
+  }
 }
 
 // Block-wide count of a predicate accumulated into *ctr with one atomic per
@@ -1026,6 +1370,9 @@ __global__ void __launch_bounds__(kBlock) k_free_compact(uint8_t* freed, int64_t
   if (tile == gridDim.x - 1 && threadIdx.x == 0) {
     counters[ASH_CTR_TOP] = static_cast<int32_t>(start);
     counters[ASH_CTR_TOMBS] += erased;
+    // heap[start, ts.base) now holds freed indices, not the identity
+    if (static_cast<int32_t>(ts.base) > counters[ASH_CTR_HEAP_DIRTY])
+      counters[ASH_CTR_HEAP_DIRTY] = static_cast<int32_t>(ts.base);
   }
 }
 
@@ -1241,8 +1588,19 @@ int check_tiles(const ash_map_t* m, int64_t n) {
   return ASH_OK;
 }
 
-void launch_tile_scan(const ash_map_t* m, int64_t n, int top_slot, int total_slot, cudaStream_t s) {
-  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot);
+// Insert batches keep the tile prefixes apart from the counts when the
+// workspace has room for both: counts in [0, H), prefixes in [H, 2H] with
+// H = (tile_counts_len - 1) / 2 >= tiles.  The staged commit needs pre[t + 1]
+// of a neighbouring tile, so nothing may be zeroed in place during the commit;
+// the fixed split keeps the count half all-zero between batches of any size.
+int32_t* split_prefix(const ash_map_t* m, int64_t n) {
+  const int64_t half = (m->tile_counts_len - 1) / 2;
+  return half >= tiles_for(n) ? m->tile_counts + half : nullptr;
+}
+
+void launch_tile_scan(const ash_map_t* m, int64_t n, int top_slot, int total_slot, cudaStream_t s,
+                      int32_t* pre_out = nullptr) {
+  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot, pre_out);
 }
 
 int check_scan(const ash_map_t* m, int64_t n) {
@@ -1272,6 +1630,49 @@ ValueArgs value_args(const ash_map_t* m, const void* const* values) {
 
 int arity_class(int arity) { return arity <= 3 ? arity : 0; }
 
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int g_commit_bulk = -1;  // ASH_COMMIT_BULK=0 selects the plain commit (A/B runs)
+int g_sweep_div = 5;     // table sweep when winners >= n_buckets / g_sweep_div (0: never)
+
+void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words, const ash_map_t* m, int64_t sweep_min,
+                  cudaStream_t s) {
+  if (sweep_min == INT64_MAX) return;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  unsigned g = grid_for(t.n_buckets, kBlock);
+  const unsigned cap = static_cast<unsigned>(sms) * 8;
+  k_commit_sweep<<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min);
+}
+
+template <int A, int VW>
+int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const ValueArgs& va, int assoc,
+                       int32_t* out_idx, uint8_t* out_mask, const ash_map_t* m, const int32_t* pre,
+                       int64_t sweep_min, int32_t* rank_words, cudaStream_t s) {
+  constexpr int SV = (VW > 0 && VW <= 4) ? VW : 0;
+  constexpr size_t smem = kCommitStages * CommitStage<A, SV>::kBytes;
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaFuncSetAttribute(k_commit_bulk<A, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_commit_bulk<A, VW>, kCommitThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks_per_sm < 1) return fail(ASH_ERR_CUDA, "k_commit_bulk does not fit on an SM");
+  }
+  const int64_t T = tiles_for(n);
+  const int64_t cap = static_cast<int64_t>(blocks_per_sm) * sms;
+  const unsigned grid = static_cast<unsigned>(T < cap ? T : cap);
+  k_commit_bulk<A, VW><<<grid, kCommitThreads, smem, s>>>(t, keys, n, va, assoc, out_idx, out_mask, m->heap,
+                                                          m->capacity, m->active, m->key_buf, m->counters, pre, T,
+                                                          sweep_min, rank_words);
+  return ASH_OK;
+}
+
 #define ASH_DISPATCH_ARITY(arity, KERNEL_CALL) \
   switch (arity_class(arity)) {                \
     case 1: { constexpr int A = 1; KERNEL_CALL; break; } \
@@ -1288,6 +1689,13 @@ int arity_class(int arity) { return arity <= 3 ? arity : 0; }
 extern "C" {
 
 int ash_abi_version(void) { return ASH_ABI_VERSION; }
+
+int ash_set_commit_mode(int32_t bulk, int32_t sweep_div) {
+  if (sweep_div < 0) return fail(ASH_ERR_INVALID, "sweep divisor must be >= 0");
+  g_commit_bulk = bulk ? 1 : 0;
+  g_sweep_div = sweep_div;
+  return ASH_OK;
+}
 
 int ash_set_stream_hints(int32_t on) {
   g_stream_hints = on ? 1u : 0u;
@@ -1363,7 +1771,7 @@ int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint
   if (int rc = check_tiles(m, n)) return rc;
   (void)out_idx;
   (void)out_mask;
-  launch_tile_scan(m, n, ASH_CTR_TOP_BASE, ASH_CTR_WINNERS, s);
+  launch_tile_scan(m, n, ASH_CTR_TOP_BASE, ASH_CTR_WINNERS, s, split_prefix(m, n));
   return check_launch("ash_insert_count");
 }
 
@@ -1383,10 +1791,37 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
     const int64_t w = va.rb[0] / 4;
     if (w == 1 || w == 2 || w == 3 || w == 4 || w == 8) vw = static_cast<int>(w);
   }
+  int32_t* pre = split_prefix(m, n);
+  // winners at which the slot states are committed by the table sweep
+  const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
+  int32_t* rank_words = (m->rank_words && m->rank_words_len >= 2 * ((n + 31) / 32)) ? m->rank_words : nullptr;
+  if (pre && vw >= 0 && m->arity <= 3 && g_commit_bulk && aligned16(keys) && aligned16(out_idx) &&
+      aligned16(out_mask) && aligned16(m->heap) && (vw == 0 || aligned16(va.src[0]))) {
+    int rc = ASH_OK;
+#define ASH_BULK(VW_)                                                                                    \
+  switch (m->arity) {                                                                                    \
+    case 1: rc = launch_commit_bulk<1, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
+    case 2: rc = launch_commit_bulk<2, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
+    default: rc = launch_commit_bulk<3, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
+  }
+    switch (vw) {
+      case 0: ASH_BULK(0); break;
+      case 1: ASH_BULK(1); break;
+      case 2: ASH_BULK(2); break;
+      case 3: ASH_BULK(3); break;
+      case 4: ASH_BULK(4); break;
+      default: ASH_BULK(8); break;
+    }
+#undef ASH_BULK
+    if (rc) return rc;
+    launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
+    return check_launch("ash_insert_commit");
+  }
+  int32_t* tile_pre = pre ? pre : m->tile_counts;
 #define ASH_COMMIT(VW_)                                                                                   \
   ASH_DISPATCH_ARITY(m->arity, (k_commit<A, VW_><<<grid_for(n, kTile), kBlock, 0, s>>>(                  \
                                    t, keys, n, va, association, out_idx, out_mask, m->heap, m->active, \
-                                   m->key_buf, m->counters, m->tile_counts)))
+                                   m->key_buf, m->counters, tile_pre, sweep_min, rank_words)))
   switch (vw) {
     case 0: ASH_COMMIT(0); break;
     case 1: ASH_COMMIT(1); break;
@@ -1397,6 +1832,7 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
     default: ASH_COMMIT(-1); break;
   }
 #undef ASH_COMMIT
+  launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
   return check_launch("ash_insert_commit");
 }
 

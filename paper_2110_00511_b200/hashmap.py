@@ -294,9 +294,16 @@ class HashMap:
             self._struct.scan_status_len = self._scan.numel()
             # per-tile winner counts: zero between batches (the commit or the
             # rollback clears what the claim counted)
-            self._tiles = torch.zeros(self._scan.numel(), dtype=torch.int32, device=self._device)
+            # [0, T): counts, [T, 2T]: exclusive prefixes of the staged commit
+            self._tiles = torch.zeros(2 * self._scan.numel() + 1, dtype=torch.int32,
+                                      device=self._device)
             self._struct.tile_counts = self._tiles.data_ptr()
             self._struct.tile_counts_len = self._tiles.numel()
+            # per 32 positions: winner bits + rank of the first (table-sweep commit)
+            self._rank_words = torch.empty(2 * (_lib.TILE // 32) * self._scan.numel(),
+                                           dtype=torch.int32, device=self._device)
+            self._struct.rank_words = self._rank_words.data_ptr()
+            self._struct.rank_words_len = self._rank_words.numel()
 
     def _ptr(self):
         return _lib.ctypes.byref(self._struct)
