@@ -492,7 +492,7 @@ class HashMap:
     # loser in insert mode: both report False / -1).
 
     PIPELINE_MIN = 1 << 20
-    PIPELINE_CHUNK = 2 << 20
+    PIPELINE_CHUNK = int(os.environ.get("ASH_PIPELINE_CHUNK", 1 << 20))
 
     @staticmethod
     def _is_host(x) -> bool:
