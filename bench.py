@@ -298,6 +298,7 @@ def gpu_single(args, torch, dev):
 
     sweep = run_sweep(torch, dev, ash, flush)
     other = run_other_configs(torch, dev, ash, flush, with_cpu=not args.no_cpu_baseline)
+    other["c5_stream_1gpu"] = run_c5(torch, dev, ash)
     return dict(ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
                 sweep=sweep, other=other, launches_per_step=4)
 
@@ -367,6 +368,53 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
         c4["cpu_baseline"] = {"mcand_per_s": round(len(frames[0]) / (time.perf_counter() - t0) / 1e6, 3),
                               "cores": 1, "kind": "port", "sample": "first frame"}
     out["c4_allocate_blocks"] = c4
+    return out
+
+
+C5_TOTAL = 400_000_000
+C5_BATCH = 1 << 25
+
+
+def run_c5(torch, dev, ash):
+    """configs[4] on one GPU: the 400M-key map built by the mixed stream
+    (each step inserts 2^25 new keys and finds 2^25 keys, half present),
+    keys generated in HBM by the counter-based generator.  The N-GPU
+    hash-partitioned run of the same stream is `bench.py --c5` under torchrun."""
+    from paper_2110_00511_b200.workloads import c5_step_batches
+    stream = torch.cuda.current_stream(dev)
+    steps = -(-C5_TOTAL // C5_BATCH)
+    m = ash.HashMap(C5_TOTAL, 3, [np.float32], device=dev)
+    ms_ins, ms_find, ops = [], [], 0
+    for s in range(steps):
+        ins, q = c5_step_batches(s * C5_BATCH, min(C5_BATCH, C5_TOTAL - s * C5_BATCH), C5_TOTAL, device=dev)
+        vals = torch.rand((len(ins), 1), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        r = m.insert(ins, vals)
+        b.record(stream)
+        f = m.find(q)
+        c.record(stream)
+        torch.cuda.synchronize()
+        ms_ins.append(a.elapsed_time(b))
+        ms_find.append(b.elapsed_time(c))
+        ops += 2 * len(ins)
+        assert bool(r.masks.all())
+        hits = int(f.masks.sum())
+        assert hits == len(q) // 2, hits
+        del ins, q, vals, r, f
+    assert m.size == C5_TOTAL
+    tot = sum(ms_ins) + sum(ms_find)
+    out = {"workload": "configs[4] at N=1: 400M-key map built by a mixed stream, 12 steps of "
+                       "2^25 inserts (new keys, f32[1] values) + 2^25 finds (50% present)",
+           "keys": C5_TOTAL, "ms_total": round(tot, 2), "mops": round(ops / tot / 1e3, 1),
+           "insert_ms_first_last": [round(ms_ins[0], 3), round(ms_ins[-2], 3)],
+           "find_ms_first_last": [round(ms_find[0], 3), round(ms_find[-2], 3)],
+           "note": "table 9.6 GB (600M 16-byte slots); the map grows from 0 to 400M keys; "
+                   "key generation and value fill excluded; no CPU baseline (400M is infeasible "
+                   "for the reference)"}
+    del m
+    torch.cuda.empty_cache()
     return out
 
 

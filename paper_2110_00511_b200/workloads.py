@@ -57,3 +57,40 @@ def sphere_points(count: int, seed: int = 0) -> np.ndarray:
     d = np.random.default_rng(seed).normal(size=(count, 3))
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     return d
+
+
+def _signed64(c: int) -> int:
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def keys_from_counters_torch(counters, seed: int = 0):
+    """Device twin of ``keys_from_counters`` (torch int64 arithmetic wraps
+    mod 2^64; masking to 63 bits keeps every shift logical), so the 400M-key
+    C5 stream is generated in HBM instead of crossing PCIe."""
+    import torch
+    m = (1 << 63) - 1
+    x = (counters.to(torch.int64) + ((seed * 0x9E3779B97F4A7C15) & m)) & m
+    x = (x * _signed64(_M1)) & m
+    x ^= x >> 29
+    x = (x * _signed64(_M2)) & m
+    x ^= x >> 32
+    x = (x * _signed64(_M1)) & m
+    x ^= x >> 27
+    f = 0x1FFFFF
+    return torch.stack([(x & f) - (1 << 20), ((x >> 21) & f) - (1 << 20),
+                        ((x >> 42) & f) - (1 << 20)], dim=1).to(torch.int32)
+
+
+def c5_step_batches(start: int, size: int, total: int, seed: int = 0, device=None):
+    """configs[4] stream: a step inserts pool keys
+    [start, start + size) and finds ``size`` keys, half drawn from the keys
+    inserted so far and half from never-inserted pool indices >= total."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed * 1000003 + start)
+    ins = torch.arange(start, start + size, device=device)
+    half = size // 2
+    hit = torch.randint(0, start + size, (half,), generator=g, device=device)
+    miss = torch.randint(total, 2 * total, (size - half,), generator=g, device=device)
+    q = torch.cat([hit, miss])
+    q = q[torch.randperm(size, generator=g, device=device)]
+    return keys_from_counters_torch(ins, seed), keys_from_counters_torch(q, seed)
