@@ -117,6 +117,14 @@ int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream);
 int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx,
              uint8_t* out_mask, void* stream);
 
+/* radius_neighbors (geometry.py:87-99): for each of n int3 coordinates and
+ * each of the (2r+1)^3 lattice offsets in lexicographic order (dx outer),
+ * find(coords[i] + offset[j]) -> out_idx / out_mask [i * (2r+1)^3 + j].
+ * The offset queries are generated in-kernel (no n x 27 key buffer).
+ * Requires key arity 3 and 0 <= r <= 15. */
+int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r,
+                     int32_t* out_idx, uint8_t* out_mask, void* stream);
+
 /* HashMap.insert / activate (hashmap.py:336-413), generic-backend semantics:
  * winners are first occurrences of absent keys, winner of rank r gets
  * heap[top + r].  `values` holds n_values device pointers (rows of
@@ -210,6 +218,34 @@ int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_
                     void* dst, void* stream);
 int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
                      void* dst, void* stream);
+
+/* Block candidates of one depth frame (tsdf/grid.py:98-125 _candidate_blocks
+ * + block_of :24-27).  depth: height x width float64 (row-major, device);
+ * cam = {fx, fy, cx, cy, depth_min, depth_max}; pose: 4x4 row-major float64
+ * camera-to-world (host).  neighbor = 0: ray mode (samples at half-block
+ * spacing within +-trunc of the surface), 1: surface block + 26 neighbours.
+ * Virtual position p = pixel * per_pixel + sample, per_pixel =
+ * ash_frame_positions(...) / (height * width).  Float64 arithmetic follows
+ * the reference's operation order (FrameSrc in ash_map.cu). */
+int64_t ash_frame_positions(int64_t height, int64_t width, double block_size, double trunc,
+                            int32_t neighbor);
+
+/* Every virtual position's candidate (out_coords: positions x 3) and
+ * out_valid = 1 where its pixel is valid (Frame.valid_mask); the reference's
+ * candidate list is out_coords[out_valid].  flags |= ASH_FLAG_RANGE when a
+ * block coordinate leaves int32. */
+int ash_frame_candidates(const double* depth, int64_t height, int64_t width, const double* cam,
+                         const double* pose, double block_size, double trunc, int32_t neighbor,
+                         int32_t* out_coords, uint8_t* out_valid, int32_t* flags, void* stream);
+
+/* Fused candidates + dedup (the local activate of grid.py:140-142): the
+ * frame's distinct block coordinates in first-occurrence order, written to
+ * out_coords[0 .. ws->counters[ASH_CTR_COUNT]).  ws is an all-EMPTY workspace
+ * table as for ash_voxelize (left EMPTY again); scratch: positions entries. */
+int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t width,
+                     const double* cam, const double* pose, double block_size, double trunc,
+                     int32_t neighbor, int32_t* out_coords, int32_t* scratch_idx,
+                     uint8_t* scratch_mask, void* stream);
 
 #ifdef __cplusplus
 }

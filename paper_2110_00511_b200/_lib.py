@@ -46,6 +46,7 @@ _SIGNATURES = {
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_find_lattice": (c_int32, [_M, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p]),
     "ash_insert": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ash_insert_claim": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "ash_insert_count": (c_int32, [_M, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -59,6 +60,11 @@ _SIGNATURES = {
     "ash_quantize": (c_int32, [c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p, c_void_p]),
     "ash_voxelize": (c_int32, [_M, c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
+    "ash_frame_positions": (c_int64, [c_int64, c_int64, c_double, c_double, c_int32]),
+    "ash_frame_candidates": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,
+                                       c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ash_frame_blocks": (c_int32, [_M, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,
+                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ash_route_last_error": (c_char_p, []),
     "ash_route_scratch_len": (c_int64, [c_int64, c_int32]),
     "ash_route_owner": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),

@@ -5,12 +5,17 @@ survivors are activated in the persistent global map, and each local entry
 stores its block's global buffer index."""
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
-from .hashmap import HashMap, ValueSpec
+from . import _lib
+from ._lib import call
+from .hashmap import HashMap, ValueSpec, _stream_handle
 
-__all__ = ["allocate_blocks", "BlockGrid"]
+__all__ = ["allocate_blocks", "BlockGrid", "frame_candidates", "frame_blocks", "allocate_frame",
+           "LocalBlockMap"]
 
 
 def allocate_blocks(global_map: HashMap, coords, threads: int = 1):
@@ -37,8 +42,12 @@ class BlockGrid:
     (tsdf/grid.py:47-68); ``allocate(coords)`` runs the double-map scheme."""
 
     def __init__(self, block_resolution: int = 8, capacity: int = 10000,
-                 with_color: bool = False, device=None):
+                 with_color: bool = False, device=None, voxel_size: float = 0.0058,
+                 trunc: float = 0.04, allocation: str = "ray"):
+        if allocation not in ("ray", "neighbor"):
+            raise ValueError("allocation must be 'ray' or 'neighbor'")
         l = int(block_resolution)
+        self.voxel_size, self.trunc, self.allocation = float(voxel_size), float(trunc), allocation
         specs = [ValueSpec((l, l, l, 2), np.float32)]
         if with_color:
             specs.append(ValueSpec((l, l, l, 3), np.float32))
@@ -54,5 +63,142 @@ class BlockGrid:
         return gi
 
     @property
+    def block_size(self) -> float:
+        """Block edge in meters (TsdfConfig.block_size, tsdf/types.py:102-104)."""
+        return self.voxel_size * self.block_resolution
+
+    def allocate_frame(self, depth, intrinsics, pose, depth_min: float = 0.2,
+                       depth_max: float = 3.0) -> torch.Tensor:
+        """VoxelBlockGrid.allocate_blocks(frame) (tsdf/grid.py:127-150) from
+        the depth image, candidates generated on the device."""
+        gi, local = allocate_frame(self.global_map, depth, intrinsics, pose, self.block_size,
+                                   self.trunc, depth_min, depth_max, self.allocation)
+        self.local_map = local
+        self._local_indices = gi
+        return gi
+
+    @property
     def block_count(self) -> int:
         return self.global_map.size
+
+
+# -- fused frame path (§8(f) row 1: tsdf/grid.py:98-150 from the depth image) --
+
+def _frame_args(depth, intrinsics, pose, block_size: float, trunc: float, depth_min: float,
+                depth_max: float, allocation: str, device):
+    if allocation not in ("ray", "neighbor"):
+        raise ValueError("allocation must be 'ray' or 'neighbor'")
+    if not depth_min < depth_max:
+        raise ValueError("depth_min must be < depth_max")
+    if isinstance(depth, torch.Tensor):
+        d = depth.to(device=device, dtype=torch.float64).contiguous()
+    else:
+        d = torch.from_numpy(np.ascontiguousarray(np.asarray(depth, dtype=np.float64))).to(device)
+    if d.dim() != 2:
+        raise ValueError("depth must be a (height, width) image")
+    h, w = d.shape
+    iw, ih = getattr(intrinsics, "width", w), getattr(intrinsics, "height", h)
+    if (ih, iw) != (h, w):
+        raise ValueError(f"depth shape {(h, w)} does not match intrinsics ({ih}, {iw})")
+    cam = (ctypes.c_double * 6)(float(intrinsics.fx), float(intrinsics.fy), float(intrinsics.cx),
+                                float(intrinsics.cy), float(depth_min), float(depth_max))
+    p = np.asarray(pose, dtype=np.float64).reshape(4, 4)
+    pose_c = (ctypes.c_double * 16)(*p.ravel().tolist())
+    return d, h, w, cam, pose_c, int(allocation == "neighbor")
+
+
+def frame_candidates(depth, intrinsics, pose, block_size: float, trunc: float,
+                     depth_min: float = 0.2, depth_max: float = 3.0, allocation: str = "ray",
+                     device=None) -> torch.Tensor:
+    """The frame's block candidates in the reference's order
+    (VoxelBlockGrid._candidate_blocks, tsdf/grid.py:98-125): valid pixels
+    row-major, then ray samples (or the 27 lattice neighbours)."""
+    from .geometry import _device
+    dev = _device(device)
+    d, h, w, cam, pose_c, nb = _frame_args(depth, intrinsics, pose, block_size, trunc, depth_min,
+                                           depth_max, allocation, dev)
+    n = int(_lib.lib.ash_frame_positions(h, w, float(block_size), float(trunc), nb))
+    out = torch.empty((n, 3), dtype=torch.int32, device=dev)
+    valid = torch.empty(n, dtype=torch.uint8, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    if n:
+        call("ash_frame_candidates", d.data_ptr(), h, w, cam, pose_c, float(block_size), float(trunc),
+             nb, out.data_ptr(), valid.data_ptr(), flags.data_ptr(), _stream_handle(dev))
+    if int(flags.item()) & _lib.FLAG_RANGE:
+        raise ValueError("block coordinates exceed int32 range")
+    return out[valid.view(torch.bool)]
+
+
+def frame_blocks(depth, intrinsics, pose, block_size: float, trunc: float,
+                 depth_min: float = 0.2, depth_max: float = 3.0, allocation: str = "ray",
+                 device=None) -> torch.Tensor:
+    """Distinct block coordinates of the frame in first-occurrence order —
+    ``coords[local.activate(coords).masks]`` of tsdf/grid.py:140-142 — in one
+    fused pass (candidate generation + quantise + dedup, libash
+    ``ash_frame_blocks``); the candidate list is never materialised."""
+    from .geometry import _device, _VoxelWorkspace
+    dev = _device(device)
+    d, h, w, cam, pose_c, nb = _frame_args(depth, intrinsics, pose, block_size, trunc, depth_min,
+                                           depth_max, allocation, dev)
+    n = int(_lib.lib.ash_frame_positions(h, w, float(block_size), float(trunc), nb))
+    if n == 0:
+        return torch.zeros((0, 3), dtype=torch.int32, device=dev)
+    ws = _VoxelWorkspace.get(dev)
+    with _VoxelWorkspace._lock:
+        ws.reserve(n)
+        coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
+        scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
+        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        call("ash_frame_blocks", ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c,
+             float(block_size), float(trunc), nb, coords.data_ptr(), scratch_idx.data_ptr(),
+             scratch_mask.data_ptr(), _stream_handle(dev))
+        count, flags = ws.counters[[_lib.CTR_COUNT, _lib.CTR_FLAGS]].tolist()
+    if flags & _lib.FLAG_RANGE:
+        raise ValueError("block coordinates exceed int32 range")
+    return coords[:count]
+
+
+class LocalBlockMap:
+    """The per-frame local map of tsdf/grid.py:140-149 (block coordinate ->
+    global buffer index), built on first use from the frame's distinct blocks:
+    activating them in first-occurrence order gives the same indices the
+    reference's activate over the full candidate list gives (winner ranks)."""
+
+    def __init__(self, blocks: torch.Tensor, gi: torch.Tensor, n_candidates, device):
+        self._blocks, self._gi, self._n, self._device = blocks, gi, n_candidates, device
+        self._map = None
+
+    @property
+    def map(self) -> HashMap:
+        if self._map is None:
+            n = self._n() if callable(self._n) else self._n  # capacity = len(candidates)
+            m = HashMap(max(int(n), 1), 3, value_specs=[np.int32], device=self._device)
+            li, _ = m.activate(self._blocks)
+            m.value_buffer(0)[li.long(), 0] = self._gi
+            self._map = m
+        return self._map
+
+    def __getattr__(self, name):
+        return getattr(self.map, name)
+
+
+def allocate_frame(global_map: HashMap, depth, intrinsics, pose, block_size: float, trunc: float,
+                   depth_min: float = 0.2, depth_max: float = 3.0, allocation: str = "ray"):
+    """VoxelBlockGrid.allocate_blocks (tsdf/grid.py:127-150) from the depth
+    image: fused candidate dedup, then the global activate whose indices are
+    the frame's global buffer indices (the reference's follow-up find returns
+    the same indices).  Returns ``(gi, local_map)``."""
+    dev = global_map.device
+    blocks = frame_blocks(depth, intrinsics, pose, block_size, trunc, depth_min, depth_max,
+                          allocation, device=dev)
+    if blocks.shape[0] == 0:
+        return torch.zeros(0, dtype=torch.int32, device=dev), None
+    gi, gmask = global_map.activate(blocks)
+    d = depth if isinstance(depth, torch.Tensor) else torch.from_numpy(np.asarray(depth, np.float64))
+    per_pixel = int(_lib.lib.ash_frame_positions(1, 1, float(block_size), float(trunc),
+                                                 int(allocation == "neighbor")))
+
+    def n_candidates():  # valid pixels x samples (Frame.valid_mask, tsdf/types.py:67-69)
+        valid = (d > 0) & (d >= depth_min) & (d <= depth_max)
+        return int(valid.sum()) * per_pixel
+    return gi, LocalBlockMap(blocks, gi, n_candidates, dev)

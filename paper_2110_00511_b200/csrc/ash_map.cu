@@ -450,6 +450,30 @@ __global__ void __launch_bounds__(kBlock) k_find(Table t, const int32_t* __restr
   st_stream_u8(out_mask + p, idx >= 0, pol);
 }
 
+// radius_neighbors (geometry.py:87-99): find() of coords[i] + offset[j] for
+// the (2r+1)^3 lattice offsets in lexicographic order (dx outer, dz inner),
+// generated on the fly: thread q handles point q / K, offset q % K, so the
+// (n, K) outputs are written in order and the n x K query rows are never
+// materialised.  int32 addition wraps, as numpy's does.
+__global__ void __launch_bounds__(kBlock) k_find_lattice(Table t, const int32_t* __restrict__ coords, int64_t n,
+                                                         int r, int32_t* __restrict__ out_idx,
+                                                         uint8_t* __restrict__ out_mask) {
+  const int s = 2 * r + 1, K = s * s * s;
+  const int64_t q = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (q >= n * K) return;
+  const int64_t p = q / K;
+  const int j = static_cast<int>(q - p * K);
+  const uint64_t pol = stream_policy(t.hints);
+  Key<3> k;
+  k.row = nullptr;
+  k.w[0] = static_cast<uint32_t>(__ldg(coords + 3 * p)) + static_cast<uint32_t>(j / (s * s) - r);
+  k.w[1] = static_cast<uint32_t>(__ldg(coords + 3 * p + 1)) + static_cast<uint32_t>((j / s) % s - r);
+  k.w[2] = static_cast<uint32_t>(__ldg(coords + 3 * p + 2)) + static_cast<uint32_t>(j % s - r);
+  const int32_t idx = probe_find<3>(t, k, hash_key<3>(k, 3), nullptr);
+  st_stream(out_idx + q, static_cast<uint32_t>(idx), pol);
+  st_stream_u8(out_mask + q, idx >= 0, pol);
+}
+
 // ---------------------------------------------------------------------------
 // kernels: insert / activate claim pass
 
@@ -1474,22 +1498,81 @@ __global__ void k_quantize(const T* __restrict__ pts, int64_t n, double cell, in
   if (bad) atomicOr(flags, ASH_FLAG_RANGE);
 }
 
+// Point sources for the dedup-select path (claim into an all-EMPTY workspace
+// table, then the ascending select of first occurrences).  key() builds the
+// int3 key of virtual position p; false = no candidate at p.
+
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __restrict__ pts, int64_t n,
-                                                        double cell, int32_t* __restrict__ tmp,
+struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
+  const T* pts;
+  double cell;
+  __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(pts[3 * p + d], cell, bad));
+    return true;
+  }
+};
+
+// tsdf/grid.py:98-125 _candidate_blocks + grid.py:24-27 block_of, per depth
+// pixel (row-major) x per sample: ray mode samples the ray within +-trunc of
+// the surface at half-block spacing (tsdf/grid.py:115-125); neighbor mode is
+// the surface block plus the 26 lattice neighbours (grid.py:108-113).  Every
+// float64 operation is IEEE round-to-nearest in the reference's order:
+// (u - cx) / fx (types.py:27), (z - trunc) + t, p * depth, and the pose
+// product as numpy's OpenBLAS dgemm evaluates it (an FMA chain over k =
+// 0, 1, 2 from p0 * R[i][0]), then + trans, floor(x / block).
+struct FrameSrc {
+  const double* depth;
+  int64_t width;
+  int per_pixel;  // n_steps (ray) or 27 (neighbor)
+  int neighbor;
+  double fx, fy, cx, cy, dmin, dmax, trunc, two_trunc, step, block;
+  double R[9], tr[3];
+  __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
+    const int64_t pix = p / per_pixel;
+    const int s = static_cast<int>(p - pix * per_pixel);
+    const double z = __ldg(depth + pix);
+    if (!(z > 0.0 && z >= dmin && z <= dmax)) return false;  // Frame.valid_mask (types.py:67-69)
+    const int64_t v = pix / width, u = pix - v * width;
+    const double x = __ddiv_rn(__dsub_rn(static_cast<double>(u), cx), fx);
+    const double y = __ddiv_rn(__dsub_rn(static_cast<double>(v), cy), fy);
+    double d = z;
+    if (!neighbor) {
+      const double t = fmin(__dmul_rn(static_cast<double>(s), step), two_trunc);
+      d = fmax(__dadd_rn(__dsub_rn(z, trunc), t), 1e-6);
+    }
+    const double p0 = __dmul_rn(x, d), p1 = __dmul_rn(y, d), p2 = d;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double wi = __dadd_rn(__fma_rn(p2, R[3 * i + 2], __fma_rn(p1, R[3 * i + 1], __dmul_rn(p0, R[3 * i]))),
+                                  tr[i]);
+      k.w[i] = static_cast<uint32_t>(quantize_one<double>(wi, block, bad));
+    }
+    if (neighbor) {  // lattice_offsets(1)[s], lexicographic; int32 wrap
+      k.w[0] += static_cast<uint32_t>(s / 9 - 1);
+      k.w[1] += static_cast<uint32_t>((s / 3) % 3 - 1);
+      k.w[2] += static_cast<uint32_t>(s % 3 - 1);
+    }
+    return true;
+  }
+};
+
+template <typename Src>
+__global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, Src src, int64_t n, int32_t* __restrict__ tmp,
                                                         uint8_t* __restrict__ mask, int32_t* counters,
                                                         int32_t* tile_cnt) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool valid = p < n;
-  const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
-  if (!valid) return;
+  const bool inside = p < n;
+  const unsigned live = __ballot_sync(0xFFFFFFFFu, inside);
+  if (!inside) return;
   bool bad = false;
   Key<3> k;
   k.row = nullptr;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(pts[3 * p + d], cell, &bad));
+  k.w[0] = k.w[1] = k.w[2] = 0;
+  const bool has = src.key(p, k, &bad);
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
+  const bool skip = bad || !has;  // out-of-range points never claim; the host raises first
   const uint32_t h = hash_key<3>(k, 3);
   unsigned grp = __match_any_sync(live, h);
   if (__any_sync(live, __popc(grp) > 1)) {
@@ -1497,20 +1580,19 @@ __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __rest
     same_key_in_warp<3>(k, live, &g2);
     grp &= g2;
   }
-  // out-of-range points never claim; the host raises before using results
-  const unsigned bad_lanes = __ballot_sync(live, bad);
-  grp &= ~bad_lanes;
-  if (bad) grp = 1u << lane;
+  const unsigned skip_lanes = __ballot_sync(live, skip);
+  grp &= ~skip_lanes;
+  if (skip) grp = 1u << lane;
   const int leader = __ffs(grp) - 1;
   uint32_t res = PEND;
   bool claimed_tomb = false, candidate = false;
-  if (lane == leader && !bad)
+  if (lane == leader && !skip)
     res = probe_claim<3>(t, k, h, static_cast<uint32_t>(p), nullptr, mask, counters, tile_cnt, &claimed_tomb,
                          &candidate);
   __syncwarp(live);
   const unsigned cand = __ballot_sync(live, candidate);
   if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
-  if (lane == leader && !bad) {
+  if (lane == leader && !skip) {
     tmp[p] = static_cast<int32_t>(res);
   } else {
     tmp[p] = static_cast<int32_t>(PEND);
@@ -1518,11 +1600,11 @@ __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, const T* __rest
   }
 }
 
-template <typename T>
+template <typename Src>
 __global__ void __launch_bounds__(kBlock)
-    k_voxel_select(uint4* slots, const T* __restrict__ pts, int64_t n, double cell,
-                   const int32_t* __restrict__ tmp, const uint8_t* __restrict__ mask,
-                   int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel, int32_t* tile_pre) {
+    k_voxel_select(uint4* slots, Src src, int64_t n, const int32_t* __restrict__ tmp,
+                   const uint8_t* __restrict__ mask, int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel,
+                   int32_t* tile_pre) {
   __shared__ ScanSmem sm;
   const int64_t tile = blockIdx.x, base = tile * kTile;
   int32_t v[kItems];
@@ -1544,12 +1626,32 @@ __global__ void __launch_bounds__(kBlock)
     const int64_t p = base + it * kBlock + threadIdx.x;
     const uint32_t r = item_rank(sm, bal, it);
     bool bad = false;
+    Key<3> k;
+    k.row = nullptr;
+    src.key(p, k, &bad);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) out_coords[3 * static_cast<int64_t>(r) + d] = quantize_one<T>(pts[3 * p + d], cell, &bad);
-    out_sel[r] = p;
+    for (int d = 0; d < 3; ++d) out_coords[3 * static_cast<int64_t>(r) + d] = static_cast<int32_t>(k.w[d]);
+    if (out_sel) out_sel[r] = p;
     // leave the workspace table EMPTY for the next call
     slots[static_cast<uint32_t>(v[it]) & SLOT_MASK] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
   }
+}
+
+// Every candidate of a frame in virtual-position order (parity tests and the
+// reference's _candidate_blocks API); valid = 0 where the pixel is invalid.
+__global__ void k_frame_candidates(FrameSrc src, int64_t n, int32_t* __restrict__ out, uint8_t* __restrict__ valid,
+                                   int32_t* flags) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  if (p >= n) return;
+  bool bad = false;
+  Key<3> k;
+  k.row = nullptr;
+  k.w[0] = k.w[1] = k.w[2] = 0;
+  const bool has = src.key(p, k, &bad);
+  if (bad) atomicOr(flags, ASH_FLAG_RANGE);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[3 * p + d] = static_cast<int32_t>(k.w[d]);
+  valid[p] = has;
 }
 
 // ---------------------------------------------------------------------------
@@ -1681,6 +1783,43 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
     default: { constexpr int A = 0; KERNEL_CALL; break; } \
   }
 
+template <typename Src>
+void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
+                      int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s) {
+  k_voxel_claim<Src><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, src, n, scratch_idx, scratch_mask, ws->counters,
+                                                            ws->tile_counts);
+  launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
+  k_voxel_select<Src><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask, out_coords,
+                                                             out_sel, ws->tile_counts);
+}
+
+int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t width, const double* cam,
+                   const double* pose, double block_size, double trunc, int32_t neighbor, int64_t* n) {
+  if (!depth || !cam || !pose) return fail(ASH_ERR_INVALID, "null frame pointer");
+  if (height < 1 || width < 1) return fail(ASH_ERR_INVALID, "image size must be positive");
+  if (!(cam[0] > 0) || !(cam[1] > 0)) return fail(ASH_ERR_INVALID, "focal lengths must be > 0");
+  if (!(block_size > 0)) return fail(ASH_ERR_INVALID, "block size must be > 0");
+  if (!(trunc > 0)) return fail(ASH_ERR_INVALID, "truncation must be > 0");
+  f->depth = depth;
+  f->width = width;
+  f->neighbor = neighbor ? 1 : 0;
+  f->fx = cam[0], f->fy = cam[1], f->cx = cam[2], f->cy = cam[3], f->dmin = cam[4], f->dmax = cam[5];
+  f->trunc = trunc;
+  f->two_trunc = 2 * trunc;
+  f->step = block_size / 2;
+  f->block = block_size;
+  // n_steps = int(ceil(2 * trunc / step)) + 1 (tsdf/grid.py:117)
+  const double ns = ceil((2 * trunc) / f->step) + 1;
+  if (!(ns >= 1 && ns <= 4096)) return fail(ASH_ERR_INVALID, "too many ray samples per pixel");
+  f->per_pixel = neighbor ? 27 : static_cast<int>(ns);
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) f->R[3 * i + j] = pose[4 * i + j];
+    f->tr[i] = pose[4 * i + 3];
+  }
+  *n = height * width * f->per_pixel;
+  return check_batch(*n);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1743,6 +1882,21 @@ int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uin
   cudaStream_t s = as_stream(stream);
   ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask)));
   return check_launch("ash_find");
+}
+
+int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, int32_t* out_idx,
+                     uint8_t* out_mask, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (m->arity != 3) return fail(ASH_ERR_INVALID, "lattice queries need a map with key arity 3");
+  if (r < 0 || r > 15) return fail(ASH_ERR_INVALID, "lattice radius must be in [0, 15]");
+  if (n < 0) return fail(ASH_ERR_INVALID, "negative batch length");
+  const int64_t K = static_cast<int64_t>(2 * r + 1) * (2 * r + 1) * (2 * r + 1);
+  if (n == 0) return ASH_OK;
+  if (n > (int64_t(1) << 38) / K) return fail(ASH_ERR_INVALID, "too many lattice queries");
+  if (!coords || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
+  Table t = make_table(m);
+  k_find_lattice<<<grid_for(n * K, kBlock), kBlock, 0, as_stream(stream)>>>(t, coords, n, r, out_idx, out_mask);
+  return check_launch("ash_find_lattice");
 }
 
 int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
@@ -1954,21 +2108,46 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   cudaMemsetAsync(scratch_mask, 0, n, s);
   Table t = make_table(ws);
   if (points_are_f64) {
-    const double* p = static_cast<const double*>(points);
-    k_voxel_claim<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask,
-                                                                ws->counters, ws->tile_counts);
-    launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
-    k_voxel_select<double><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
-                                                                 out_coords, out_sel, ws->tile_counts);
+    run_dedup_select(t, ws, CloudSrc<double>{static_cast<const double*>(points), voxel}, n, out_coords, out_sel,
+                     scratch_idx, scratch_mask, s);
   } else {
-    const float* p = static_cast<const float*>(points);
-    k_voxel_claim<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, p, n, voxel, scratch_idx, scratch_mask,
-                                                               ws->counters, ws->tile_counts);
-    launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
-    k_voxel_select<float><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, p, n, voxel, scratch_idx, scratch_mask,
-                                                                out_coords, out_sel, ws->tile_counts);
+    run_dedup_select(t, ws, CloudSrc<float>{static_cast<const float*>(points), voxel}, n, out_coords, out_sel,
+                     scratch_idx, scratch_mask, s);
   }
   return check_launch("ash_voxelize");
+}
+
+int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t width, const double* cam,
+                     const double* pose, double block_size, double trunc, int32_t neighbor, int32_t* out_coords,
+                     int32_t* scratch_idx, uint8_t* scratch_mask, void* stream) {
+  if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
+  FrameSrc f;
+  int64_t n = 0;
+  if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
+  if (ws->n_slots < n + n / 4 + 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (int rc = check_tiles(ws, n)) return rc;
+  if (!out_coords || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null output pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
+  cudaMemsetAsync(scratch_mask, 0, n, s);
+  run_dedup_select(make_table(ws), ws, f, n, out_coords, nullptr, scratch_idx, scratch_mask, s);
+  return check_launch("ash_frame_blocks");
+}
+
+int ash_frame_candidates(const double* depth, int64_t height, int64_t width, const double* cam, const double* pose,
+                         double block_size, double trunc, int32_t neighbor, int32_t* out_coords, uint8_t* out_valid,
+                         int32_t* flags, void* stream) {
+  FrameSrc f;
+  int64_t n = 0;
+  if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
+  if (!out_coords || !out_valid || !flags) return fail(ASH_ERR_INVALID, "null output pointer");
+  k_frame_candidates<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(f, n, out_coords, out_valid, flags);
+  return check_launch("ash_frame_candidates");
+}
+
+int64_t ash_frame_positions(int64_t height, int64_t width, double block_size, double trunc, int32_t neighbor) {
+  if (neighbor) return height * width * 27;
+  return height * width * (static_cast<int64_t>(ceil((2 * trunc) / (block_size / 2))) + 1);
 }
 
 }  // extern "C"

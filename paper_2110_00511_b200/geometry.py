@@ -193,14 +193,27 @@ def lattice_offsets(r: int) -> torch.Tensor:
 
 def radius_neighbors(hashmap: HashMap, coords, r: int = 1) -> BatchResult:
     """find() of every lattice offset around each coordinate
-    (geometry.py:87-99); results shaped (n, (2r+1)^3)."""
+    (geometry.py:87-99); results shaped (n, (2r+1)^3), column j is
+    ``lattice_offsets(r)[j]``.  One kernel generates the offset queries on
+    the fly (libash ``ash_find_lattice``); r = 0 is exactly ``find``."""
+    if r < 0:
+        raise ValueError("radius must be >= 0")
     host = HashMap._is_host(coords)
-    c = hashmap._check_keys(coords)
-    offs = lattice_offsets(r).to(c.device)
-    n, k = c.shape[0], offs.shape[0]
-    q = (c[:, None, :] + offs[None, :, :]).reshape(n * k, 3)
-    res = hashmap.find(q)
-    out = BatchResult(res.indices.reshape(n, k), res.masks.reshape(n, k))
+    if isinstance(coords, torch.Tensor):
+        c = coords.reshape(-1, 3)
+        if c.is_floating_point():  # np.asarray(coords, dtype=np.int32) truncates
+            c = c.to(torch.int32)
+    else:
+        c = torch.from_numpy(np.ascontiguousarray(np.asarray(coords, dtype=np.int32).reshape(-1, 3)))
+    c = hashmap._check_keys(c)
+    n, k = c.shape[0], (2 * r + 1) ** 3
+    idx = torch.empty((n, k), dtype=torch.int32, device=hashmap.device)
+    msk = torch.empty((n, k), dtype=torch.uint8, device=hashmap.device)
+    with hashmap._guard.reading():
+        if n:
+            call("ash_find_lattice", hashmap._ptr(), c.data_ptr(), n, int(r), idx.data_ptr(),
+                 msk.data_ptr(), hashmap._stream())
+    out = BatchResult(idx, msk.view(torch.bool))
     return BatchResult(out.indices.cpu(), out.masks.cpu()) if host else out
 
 
