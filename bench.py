@@ -368,6 +368,38 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
         c4["cpu_baseline"] = {"mcand_per_s": round(len(frames[0]) / (time.perf_counter() - t0) / 1e6, 3),
                               "cores": 1, "kind": "port", "sample": "first frame"}
     out["c4_allocate_blocks"] = c4
+    # the same frames end to end from the depth image: fused candidate
+    # generation + dedup on the device (§8(f) row 1), then the global activate
+    depth_d = torch.from_numpy(depth).to(dev)
+    grid = ash.BlockGrid(8, capacity=100_000, device=dev)
+    ts = []
+    for rep in range(2):
+        grid.global_map.clear()
+        for f in range(10):
+            pose = np.eye(4)
+            pose[0, 3] = 0.02 * f
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            grid.allocate_frame(depth_d, cam, pose)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if rep:
+                ts.append(a.elapsed_time(b))
+    assert grid.block_count == gm.size
+    ms = statistics.median(ts)
+    c4f = {"workload": "configs[3] from the depth image: fused candidate generation (ray mode, "
+                       "fp64 in the reference's order) + dedup + global activate, 640x480 plane frames",
+           "blocks": grid.block_count, "ms_per_frame": round(ms, 3),
+           "mcand_per_s": round(len(frames[0]) / ms / 1e3, 1),
+           "note": "includes the one 8-byte count read-back that sizes the frame's block list"}
+    if with_cpu:
+        og = O.OracleMap(100_000, 3, [((8, 8, 8, 2), np.float32)])
+        t0 = time.perf_counter()
+        O.allocate_blocks_map_calls(og, O.candidate_blocks(depth, cam, np.eye(4), 0.0058 * 8, 0.04))
+        c4f["cpu_baseline"] = {"mcand_per_s": round(len(frames[0]) / (time.perf_counter() - t0) / 1e6, 3),
+                               "cores": 1, "kind": "port",
+                               "sample": "first frame: candidate generation + map calls"}
+    out["c4_frame_fused"] = c4f
     return out
 
 
