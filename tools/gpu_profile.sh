@@ -19,7 +19,7 @@ if [[ $what == all || $what == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --profile \
     > $OUT/launches_$TAG.stdout 2>&1; echo "ncu launches rc=$?"
-  for k in k_claim k_commit k_find; do
+  for k in ${KERNELS:-k_claim k_commit_bulk k_commit_sweep k_find}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
       -o $OUT/prof_${k}_$TAG -f python bench.py --steps 1 --warmup 3 --profile \
       > $OUT/prof_${k}_$TAG.stdout 2>&1; echo "ncu $k rc=$?"
