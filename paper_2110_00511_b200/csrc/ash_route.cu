@@ -66,16 +66,20 @@ __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restric
   for (int o = threadIdx.x; o < kMaxWorld; o += kBlock) s_cnt[o] = 0;
   __syncthreads();
   const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+  // every item's owner first (all key loads of the tile in flight), then the
+  // warp-aggregated shared-memory counts
+  uint32_t own[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
-    if (p < n) {
-      const uint32_t o = owner_of(keys + p * arity, arity, world);
-      owners[p] = static_cast<uint8_t>(o);
-      // warp-aggregate the shared-memory increment per owner
-      const unsigned same = __match_any_sync(__activemask(), o);
-      if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_cnt[o], __popc(same));
-    }
+    own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p < n) owners[p] = static_cast<uint8_t>(own[it]);
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, own[it]);
+    if (own[it] != 0xFFFFFFFFu && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_cnt[own[it]], __popc(same));
   }
   __syncthreads();
   for (int o = threadIdx.x; o < static_cast<int>(world); o += kBlock) cnt[o * n_tiles + blockIdx.x] = s_cnt[o];
@@ -171,6 +175,31 @@ __global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restr
       }
   }
   __syncthreads();
+  if (arity == 3 && keys_out &&
+      (!pay_out || (pay_rb == 4 && ((reinterpret_cast<uintptr_t>(pay) | reinterpret_cast<uintptr_t>(pay_out)) & 3) == 0))) {
+    // common case (int3 keys, one 4-byte payload word): every load of the
+    // thread's items before any store
+    uint32_t kw[kItems][3], pw[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      if (p >= n) continue;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) kw[it][d] = static_cast<uint32_t>(__ldg(keys + p * 3 + d));
+      if (pay_out) pw[it] = __ldg(reinterpret_cast<const uint32_t*>(pay) + p);
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      if (p >= n) continue;
+      const int64_t dst = s_pre[it][warp][own[it]] + rank_in_warp[it];
+      perm[dst] = static_cast<int32_t>(p);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) keys_out[dst * 3 + d] = static_cast<int32_t>(kw[it][d]);
+      if (pay_out) reinterpret_cast<uint32_t*>(pay_out)[dst] = pw[it];
+    }
+    return;
+  }
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const int64_t p = base + it * kBlock + threadIdx.x;
@@ -194,6 +223,13 @@ __global__ void k_scatter_rows(const uint8_t* __restrict__ src, const int32_t* _
                                int64_t rb, uint8_t* __restrict__ dst) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) copy_row_words(dst + static_cast<int64_t>(__ldg(idx + i)) * rb, src + i * rb, rb);
+}
+
+// 4-byte rows (the routed result indices): two independent loads per row
+__global__ void k_scatter_words(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                                uint32_t* __restrict__ dst) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) dst[__ldg(idx + i)] = __ldg(src + i);
 }
 
 __global__ void k_owner_of(const int32_t* __restrict__ keys, int64_t n, int arity, uint32_t world,
@@ -262,6 +298,11 @@ int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_
 int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
   if (n < 0 || row_bytes < 0) return rfail("bad scatter arguments");
   if (n == 0 || row_bytes == 0) return ASH_OK;
+  if (row_bytes == 4 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3) == 0) {
+    k_scatter_words<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint32_t*>(src), idx, n, static_cast<uint32_t*>(dst));
+    return rcheck("ash_scatter_rows");
+  }
   k_scatter_rows<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst));
   return rcheck("ash_scatter_rows");
