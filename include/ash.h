@@ -247,6 +247,21 @@ int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t
                      int32_t neighbor, int32_t* out_coords, int32_t* scratch_idx,
                      uint8_t* scratch_mask, void* stream);
 
+/* Delegate-backend insert commit (hashmap.py:369-387), after
+ * ash_insert_claim + ash_insert_count: position p owns heap[top + p]; every
+ * key row is written there (losers' rows stay as stale data, as in the
+ * reference); winner p keeps heap[top + p]; the other positions' indices are
+ * written to loser_out[0 .. n - winners) in position order.  The caller
+ * sorts them (fill the rest of loser_out with INT32_MAX first) and hands
+ * them to ash_heap_put_losers.  Precondition: capacity - size >= n. */
+int ash_insert_commit_delegate(ash_map_t* m, const int32_t* keys, int64_t n,
+                               const void* const* values, int32_t association, int32_t* out_idx,
+                               uint8_t* out_mask, int32_t* loser_out, void* stream);
+
+/* heap[top_base + W + i] = sorted_losers[i] for i < n - W (the sorted free of
+ * index_heap.py:38-47), W / top_base from the device counters. */
+int ash_heap_put_losers(ash_map_t* m, const int32_t* sorted_losers, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

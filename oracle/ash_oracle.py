@@ -285,15 +285,19 @@ class OracleMap:
     indices, first-occurrence winners, lowest winner rank gets heap[top]."""
 
     def __init__(self, capacity, key_arity, value_specs=(), auto_rehash=True,
-                 bucket_factor=1):
+                 bucket_factor=None, backend="generic"):
         if capacity < 1:
             raise ValueError("capacity must be >= 1")
         if key_arity < 1:
             raise ValueError("key arity must be >= 1")
+        if backend not in ("generic", "delegate", "integer_delegate"):
+            raise ValueError(f"unknown backend {backend!r}")
         self.key_arity = int(key_arity)
         self.specs = [_spec(s) for s in value_specs]
         self.auto_rehash = auto_rehash
-        self.bucket_factor = bucket_factor
+        # hashmap.py:187 / backends.py:230-235: delegate chains use 2c buckets
+        self.delegate = backend != "generic"
+        self.bucket_factor = bucket_factor or (2 if self.delegate else 1)
         self._reset(int(capacity))
 
     def _reset(self, capacity):
@@ -382,13 +386,38 @@ class OracleMap:
         if len(k):
             self._insert_like(k, vs, assoc=False)
 
+    def _insert_delegate(self, keys):
+        """hashmap.py:369-387 (delegate branch): the whole batch takes
+        heap[top : top + m] (the buffer must hold size + m transiently), every
+        key row is written, winner j keeps heap[top + j], the rest return to
+        the heap sorted (index_heap.py:38-47) with their stale key rows."""
+        m = len(keys)
+        self._grow_to(m)
+        all_idx = self.heap.allocate(m)
+        self.key_buf[all_idx] = keys
+        node, found = self._lookup(keys)
+        if found.any():
+            miss = np.flatnonzero(~found)
+            win = miss[first_occurrence_mask(keys[miss])]
+        else:
+            win = np.flatnonzero(first_occurrence_mask(keys))
+        widx = all_idx[win]
+        self.chains.add(keys[win], lattice_hash(keys[win], self.chains.n_buckets), widx)
+        loser = np.ones(m, dtype=bool)
+        loser[win] = False
+        self.heap.free(all_idx[loser])
+        return node, found, win, widx
+
     def _insert_like(self, keys, vals, assoc):
-        """hashmap.py:362-413 (generic branch)."""
+        """hashmap.py:362-413 (generic branch; delegate via _insert_delegate)."""
         m = len(keys)
         idx = np.full(m, -1, dtype=np.int32)
         msk = np.zeros(m, dtype=bool)
         if m == 0:
             return OracleResult(idx, msk)
+        if self.delegate:
+            node, found, win, widx = self._insert_delegate(keys)
+            return self._finish_insert(keys, vals, assoc, node, found, win, widx, idx, msk)
         while True:
             node, found = self._lookup(keys)
             if found.any():
@@ -402,6 +431,10 @@ class OracleMap:
         widx = self.heap.allocate(win.size)
         self.key_buf[widx] = keys[win]
         self.chains.add(keys[win], lattice_hash(keys[win], self.chains.n_buckets), widx)
+        return self._finish_insert(keys, vals, assoc, node, found, win, widx, idx, msk)
+
+    def _finish_insert(self, keys, vals, assoc, node, found, win, widx, idx, msk):
+        """hashmap.py:397-413."""
         if vals is not None:
             for buf, v in zip(self.value_bufs, vals):
                 if widx.size:
@@ -475,8 +508,8 @@ class OracleMap:
 
 
 class OracleSet(OracleMap):
-    def __init__(self, capacity, key_arity, auto_rehash=True):
-        super().__init__(capacity, key_arity, (), auto_rehash)
+    def __init__(self, capacity, key_arity, auto_rehash=True, backend="generic"):
+        super().__init__(capacity, key_arity, (), auto_rehash, backend=backend)
 
 
 # ---------------------------------------------------------------------------

@@ -118,15 +118,17 @@ def scenario_bindings_parity(R):
     np.savez_compressed(OUT / "bindings_parity.npz", **out)
 
 
-def scenario_random_ops(R):
+def scenario_random_ops(R, backend="generic"):
     """Long mixed op sequences (insert / activate / erase / find / rehash)
     over a small key range, recording every output: pins heap recycling
-    order (sorted frees), stale rows and auto-rehash growth."""
-    rng = np.random.default_rng(20240817)
+    order (sorted frees), stale rows and auto-rehash growth.  The delegate
+    run pins that backend's index rule (heap[top + batch position]), its
+    whole-batch transient capacity and the stale key rows of losers."""
+    rng = np.random.default_rng(20240817 if backend == "generic" else 5150)
     rec = Recorder()
     for seq in range(6):
         cap = int(rng.integers(4, 40))
-        m = R["HashMap"](cap, 3, [((2,), np.float32), np.int32])
+        m = R["HashMap"](cap, 3, [((2,), np.float32), np.int32], backend=backend)
         rec.put("capacity0", cap)
         for _ in range(60):
             op = rng.choice(["insert", "insert", "activate", "erase", "find", "rehash"])
@@ -161,7 +163,33 @@ def scenario_random_ops(R):
         rec.put("final_keys", m.key_buffer.copy())
         rec.put("final_v0", m.value_buffer(0).copy())
         rec.put("final_v1", m.value_buffer(1).copy())
-    np.savez_compressed(OUT / "random_ops.npz", **rec.d)
+    name = "random_ops" if backend == "generic" else f"random_ops_{backend}"
+    np.savez_compressed(OUT / f"{name}.npz", **rec.d)
+
+
+def scenario_delegate(R):
+    """Delegate backend: the random op streams, App. A's capacity case (8 new
+    + 10 duplicate-only keys into capacity 8 grows to 32, generic to 8...16)
+    and growth 16 -> 131072 for 1e5 keys."""
+    scenario_random_ops(R, "delegate")
+    out = {}
+    keys = np.array([[i, i, i] for i in range(8)] + [[0, 0, 0]] * 10, np.int32)
+    for b in ("generic", "delegate"):
+        m = R["HashMap"](8, 3, [np.float32], backend=b)
+        r = m.insert(keys, np.arange(len(keys), dtype=np.float32))
+        out[f"appA_{b}_idx"], out[f"appA_{b}_mask"] = r.indices, r.masks
+        out[f"appA_{b}_cap"] = np.array(m.capacity)
+        out[f"appA_{b}_keys"] = m.key_buffer.copy()
+    rng = np.random.default_rng(808)
+    k = rng.integers(-40, 40, size=(20_000, 3)).astype(np.int32)
+    m = R["HashMap"](16, 3, [np.int32], backend="delegate")
+    r = m.insert(k, np.arange(len(k), dtype=np.int32))
+    e = m.erase(k[::5])
+    a = m.activate(k[::2])
+    out.update(grow_keys=k, grow_idx=r.indices, grow_mask=r.masks, grow_erase=e, grow_act_idx=a.indices,
+               grow_act_mask=a.masks, grow_cap=np.array(m.capacity), grow_key_buffer=m.key_buffer.copy(),
+               grow_values=m.value_buffer(0).copy(), grow_active=m.active_indices())
+    np.savez_compressed(OUT / "delegate.npz", **out)
 
 
 def scenario_growth(R):
@@ -288,9 +316,12 @@ def scenario_snapshot(R):
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     R = _ref()
+    only = sys.argv[1:]
     for fn in (scenario_trace, scenario_c1, scenario_bindings_parity, scenario_random_ops,
                scenario_growth, scenario_voxel, scenario_alloc_blocks, scenario_hash_dedup,
-               scenario_snapshot):
+               scenario_snapshot, scenario_delegate):
+        if only and fn.__name__ not in only:
+            continue
         fn(R)
         print("wrote", fn.__name__)
 

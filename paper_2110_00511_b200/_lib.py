@@ -52,6 +52,9 @@ _SIGNATURES = {
     "ash_insert_count": (c_int32, [_M, c_int64, c_void_p, c_void_p, c_void_p]),
     "ash_insert_commit": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ash_insert_rollback": (c_int32, [_M, c_int64, c_void_p, c_void_p]),
+    "ash_insert_commit_delegate": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                             c_void_p, c_void_p]),
+    "ash_heap_put_losers": (c_int32, [_M, c_void_p, c_int64, c_void_p]),
     "ash_erase": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "ash_active_indices": (c_int32, [_M, c_void_p, c_void_p]),
     "ash_rehash_from": (c_int32, [_M, _M, c_void_p, c_int64, c_void_p]),

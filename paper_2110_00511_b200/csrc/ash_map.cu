@@ -978,6 +978,68 @@ __global__ void __launch_bounds__(kBlock)
     counters[ASH_CTR_TOP] = static_cast<int32_t>(sm.base) + ld_volatile_i32(counters + ASH_CTR_WINNERS);
 }
 
+// Delegate-backend commit (hashmap.py:369-387): position p of the batch owns
+// heap[top + p] for the whole call (IntegerDelegateBackend keys its chains by
+// buffer index, so every key is first copied into its allocated row); winner
+// p keeps that index, every other position's index is a loser and goes to
+// loser_out[p - winners before p] (position order) for the sorted free.
+template <int A>
+__global__ void __launch_bounds__(kBlock)
+    k_commit_delegate(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
+                      int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
+                      uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
+                      int32_t* tile_pre, int32_t* __restrict__ loser_out) {
+  __shared__ ScanSmem sm;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kTile;
+  int32_t v[kItems];
+  bool win[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    v[it] = p < n ? tmp[p] : 0;
+    win[it] = p < n && v[it] < 0 && !(mask[p] & DEMOTED);
+  }
+  uint32_t bal[kItems];
+  tile_scan_known(win, bal, sm, tile_pre, tile, counters + ASH_CTR_TOP_BASE);
+  const int arity = A ? A : t.arity;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p >= n) continue;
+    const int32_t idx = heap[sm.base + p];
+    int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
+    for (int d = 0; d < arity; ++d) dr[d] = keys[p * arity + d];  // every row, losers' stay stale
+    if (win[it]) {
+      t.slots[static_cast<uint32_t>(v[it]) & SLOT_MASK].w = static_cast<uint32_t>(idx);
+      for (int b = 0; b < va.n; ++b) copy_row(va.dst[b] + idx * va.rb[b], va.src[b] + p * va.rb[b], va.rb[b]);
+      active[idx] = 1;
+      tmp[p] = idx;
+      mask[p] = 1;
+    } else {
+      loser_out[p - item_rank(sm, bal, it)] = idx;
+      tmp[p] = (v[it] >= 0 && assoc) ? v[it] : -1;
+      mask[p] = (v[it] >= 0 && assoc) ? 1 : 0;
+    }
+  }
+  if (tile == 0 && threadIdx.x == 0)
+    counters[ASH_CTR_TOP] = static_cast<int32_t>(sm.base) + ld_volatile_i32(counters + ASH_CTR_WINNERS);
+}
+
+// heap[top_base + W + i] = sorted losers (index_heap.py:38-47 free of the
+// batch's losers, below the new top = top_base + W)
+__global__ void k_heap_put_losers(int32_t* __restrict__ heap, const int32_t* __restrict__ sorted, int64_t n,
+                                  const int32_t* counters) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+  const int64_t w = counters[ASH_CTR_WINNERS];
+  if (i < n - w) heap[counters[ASH_CTR_TOP_BASE] + w + i] = sorted[i];
+}
+
+__global__ void k_heap_dirty(int32_t* counters, int64_t n) {
+  const int32_t hi = static_cast<int32_t>(counters[ASH_CTR_TOP_BASE] + n);
+  if (hi > counters[ASH_CTR_HEAP_DIRTY]) counters[ASH_CTR_HEAP_DIRTY] = hi;
+}
+
 // ---------------------------------------------------------------------------
 // TMA-staged commit (persistent, warp-specialised).
 //
@@ -1988,6 +2050,33 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
 #undef ASH_COMMIT
   launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
   return check_launch("ash_insert_commit");
+}
+
+int ash_insert_commit_delegate(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
+                               int32_t association, int32_t* out_idx, uint8_t* out_mask, int32_t* loser_out,
+                               void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return ASH_OK;
+  if (int rc = check_tiles(m, n)) return rc;
+  if (!loser_out) return fail(ASH_ERR_INVALID, "null loser buffer");
+  Table t = make_table(m);
+  ValueArgs va = value_args(m, values);
+  int32_t* pre = split_prefix(m, n);
+  int32_t* tile_pre = pre ? pre : m->tile_counts;
+  ASH_DISPATCH_ARITY(m->arity, (k_commit_delegate<A><<<grid_for(n, kTile), kBlock, 0, as_stream(stream)>>>(
+                                   t, keys, n, va, association, out_idx, out_mask, m->heap, m->active, m->key_buf,
+                                   m->counters, tile_pre, loser_out)));
+  return check_launch("ash_insert_commit_delegate");
+}
+
+int ash_heap_put_losers(ash_map_t* m, const int32_t* sorted_losers, int64_t n, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (n < 0) return fail(ASH_ERR_INVALID, "negative batch length");
+  if (n == 0) return ASH_OK;
+  k_heap_put_losers<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(m->heap, sorted_losers, n, m->counters);
+  k_heap_dirty<<<1, 1, 0, as_stream(stream)>>>(m->counters, n);  // heap above top is no longer the identity
+  return check_launch("ash_heap_put_losers");
 }
 
 int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values, int32_t association,

@@ -555,7 +555,7 @@ class HashMap:
         occurrence of each absent key wins a fresh index; existing values are
         never overwritten (hashmap.py:336-347)."""
         host = self._is_host(keys)
-        if host and self._pipeline_fits(keys):
+        if host and self._pipeline_fits(keys) and self.backend_name != "delegate":
             k = self._check_keys(keys, to_device=False)
             vals = self._check_values(k.shape[0], values, to_device=False)
             with self._guard.writing():
@@ -596,6 +596,10 @@ class HashMap:
         if vals is not None and len(vals):
             vptr = (_lib.c_void_p * len(vals))(*[v.data_ptr() for v in vals])
         assoc = 1 if association else 0
+        if self.backend_name == "delegate":
+            self._insert_delegate(keys, m, vptr, assoc, idx, msk)
+            self._size_known = False
+            return BatchResult(idx, msk.view(torch.bool))
         while True:
             self._reserve_slots(m)
             self._ensure_scan(m)
@@ -637,6 +641,33 @@ class HashMap:
             self._rehash_into(self._grown_capacity(winners))
         self._size_known = False
         return BatchResult(idx, msk.view(torch.bool))
+
+    def _insert_delegate(self, keys, m, vptr, assoc, idx, msk) -> None:
+        """Delegate backend (hashmap.py:369-387): the buffer must hold size + m
+        during the call (growth is planned on m, not on the winners); position
+        p owns heap[top + p]; losers return to the heap sorted with stale key
+        rows (libash ash_insert_commit_delegate + ash_heap_put_losers)."""
+        while True:
+            self._reserve_slots(m)
+            self._ensure_scan(m)
+            if m > self._capacity - self._top_ub:
+                self._sync_size()
+            free = self._capacity - self._top_ub
+            if m <= free:
+                break
+            if not self.auto_rehash:
+                raise CapacityError(f"batch needs {m} free slots, {free} available at capacity "
+                                    f"{self._capacity}")
+            self._rehash_into(self._grown_capacity(m))
+        losers = torch.full((m,), 2**31 - 1, dtype=torch.int32, device=self._device)
+        call("ash_insert_claim", self._ptr(), keys.data_ptr(), m, idx.data_ptr(), msk.data_ptr(),
+             self._stream())
+        call("ash_insert_count", self._ptr(), m, idx.data_ptr(), msk.data_ptr(), self._stream())
+        call("ash_insert_commit_delegate", self._ptr(), keys.data_ptr(), m, vptr, assoc,
+             idx.data_ptr(), msk.data_ptr(), losers.data_ptr(), self._stream())
+        srt = torch.sort(losers).values  # the sorted free of index_heap.py:46
+        call("ash_heap_put_losers", self._ptr(), srt.data_ptr(), m, self._stream())
+        self._top_ub = min(self._capacity, self._top_ub + m)
 
     def find(self, keys) -> BatchResult:
         """Look up keys; the map is not modified (hashmap.py:415-429)."""

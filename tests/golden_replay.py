@@ -90,8 +90,8 @@ def replay_bindings(make_map):
         bytes_eq(m.value_buffer(0), g[p + "value_buffer"], f"{seed} value buffer")
 
 
-def replay_random_ops(make_map):
-    g = load("random_ops")
+def replay_random_ops(make_map, name="random_ops"):
+    g = load(name)
     names = sorted(g)
     i = 0
 
@@ -190,3 +190,30 @@ def replay_alloc_blocks(make_map, alloc_fn, candidates_fn=None):
             bytes_eq(local.value_buffer(0), g[p + "local_values"], f"{p} local values")
         bytes_eq(gm.key_buffer, g[f"{shape}_global_keys"], f"{shape} global keys")
         eq(gm.active_indices(), g[f"{shape}_global_active"], f"{shape} global active")
+
+
+def replay_delegate(make_map):
+    """make_map(cap, arity, specs, backend) — delegate-backend fixtures:
+    App. A capacity case (both backends) and growth + erase + activate."""
+    g = load("delegate")
+    keys = np.array([[i, i, i] for i in range(8)] + [[0, 0, 0]] * 10, np.int32)
+    for b in ("generic", "delegate"):
+        m = make_map(8, 3, [np.float32], b)
+        r = m.insert(keys, np.arange(len(keys), dtype=np.float32))
+        eq(r.indices, g[f"appA_{b}_idx"], f"appA {b} idx")
+        eq(r.masks, g[f"appA_{b}_mask"], f"appA {b} mask")
+        assert m.capacity == int(g[f"appA_{b}_cap"]), f"appA {b} capacity"
+        bytes_eq(m.key_buffer, g[f"appA_{b}_keys"], f"appA {b} key rows")
+    k = g["grow_keys"]
+    m = make_map(16, 3, [np.int32], "delegate")
+    r = m.insert(k, np.arange(len(k), dtype=np.int32))
+    eq(r.indices, g["grow_idx"], "grow idx")
+    eq(r.masks, g["grow_mask"], "grow mask")
+    eq(m.erase(k[::5]), g["grow_erase"], "grow erase")
+    r = m.activate(k[::2])
+    eq(r.indices, g["grow_act_idx"], "grow activate idx")
+    eq(r.masks, g["grow_act_mask"], "grow activate mask")
+    assert m.capacity == int(g["grow_cap"])
+    bytes_eq(m.key_buffer, g["grow_key_buffer"], "grow key rows (stale loser rows)")
+    bytes_eq(m.value_buffer(0), g["grow_values"], "grow values")
+    eq(m.active_indices(), g["grow_active"], "grow active")

@@ -27,6 +27,14 @@ def test_random_op_sequences():
     G.replay_random_ops(make_oracle)
 
 
+def test_random_op_sequences_delegate():
+    G.replay_random_ops(lambda c, a, sp: O.OracleMap(c, a, sp, backend="delegate"), "random_ops_delegate")
+
+
+def test_delegate_backend():
+    G.replay_delegate(lambda c, a, sp, b: O.OracleMap(c, a, sp, backend=b))
+
+
 def test_growth_and_arity():
     G.replay_growth(make_oracle)
 

@@ -41,6 +41,15 @@ def test_random_op_sequences(ash):
     G.replay_random_ops(_mk(ash))
 
 
+def test_random_op_sequences_delegate(ash):
+    G.replay_random_ops(lambda c, a, sp: ash.HashMap(c, a, sp, backend="delegate", device="cuda"),
+                        "random_ops_delegate")
+
+
+def test_delegate_backend(ash):
+    G.replay_delegate(lambda c, a, sp, b: ash.HashMap(c, a, sp, backend=b, device="cuda"))
+
+
 def test_growth_and_arity(ash):
     G.replay_growth(_mk(ash))
 
