@@ -647,6 +647,363 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
 }
 
 // ---------------------------------------------------------------------------
+// Binned claim (insert / activate phase 1 for dense batches).
+//
+// The plain claim makes every position a random 32-byte probe plus, for new
+// keys, a random 128-bit CAS: ~20 M random L2 misses for a 10M batch, bound
+// by the random-access rate.  When the batch is dense relative to
+// the table (n >= n_slots / kBinDensity), the positions are first binned by
+// the table region of their home bucket (regions of kRegionBuckets buckets,
+// 64 KB of slots): two streaming passes (count, scatter of {key, pos}
+// records).  One CTA per region then loads the region's slots into shared
+// memory, claims / finds / joins every record with shared-memory atomics,
+// writes the dirty buckets back and the per-position results (same scratch
+// encoding as k_claim).  The table layout is unchanged (global linear
+// probing): a record whose probe would run past the region's last bucket
+// "spills" and is claimed afterwards on the global table by k_claim_spill,
+// together with every record of an oversized (heavily duplicated) region.
+// All records of one key share a home bucket, so they resolve in the same
+// place, and the lowest position still wins (atomicMin on the pending state).
+
+constexpr int kRegionBuckets = 2048;
+constexpr int kRegionSlots = 2 * kRegionBuckets;
+constexpr int kRegionMaxRecords = 1 << 16;  // beyond: the region's records spill
+constexpr int kMaxRegions = 12288;          // shared histogram limit (48 KB)
+constexpr int kBinThreads = 512;
+constexpr int kBinItems = 16;
+constexpr int kRegionThreads = 512;
+constexpr uint32_t LOCK = 0xFFFFFFFDu;      // region-claim slot being written
+
+template <int A>
+__device__ __forceinline__ uint32_t region_of_key(const Key<A>& k, uint32_t n_buckets, uint32_t* home) {
+  *home = home_bucket(hash_key<A>(k, A), n_buckets);
+  return *home / kRegionBuckets;
+}
+
+template <int A>
+__global__ void __launch_bounds__(kBinThreads) k_bin_count(const int32_t* __restrict__ keys, int64_t n,
+                                                           uint32_t n_buckets, int n_regions,
+                                                           int32_t* __restrict__ region_cnt) {
+  extern __shared__ int32_t s_hist[];
+  for (int i = threadIdx.x; i < n_regions; i += kBinThreads) s_hist[i] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kBinThreads * kBinItems);
+#pragma unroll 4
+  for (int it = 0; it < kBinItems; ++it) {
+    const int64_t p = base + it * kBinThreads + threadIdx.x;
+    if (p < n) {
+      uint32_t home;
+      atomicAdd(&s_hist[region_of_key<A>(load_key<A>(keys, p, A), n_buckets, &home)], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_regions; i += kBinThreads)
+    if (s_hist[i]) atomicAdd(&region_cnt[i], s_hist[i]);
+}
+
+// exclusive prefix of n counts (one block); out[n] = total; cursor = copy
+__global__ void __launch_bounds__(1024) k_excl_scan(const int32_t* __restrict__ cnt, int n, int32_t* __restrict__ out,
+                                                    int32_t* __restrict__ cursor) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int32_t x = i < n ? cnt[i] : 0;
+    int32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int32_t w = warp_tot[lane];
+      int32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    const int32_t c = carry;
+    if (i < n) out[i] = cursor[i] = c + warp_tot[warp] + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + warp_tot[warp] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+template <int A>
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const int32_t* __restrict__ keys, int64_t n,
+                                                             uint32_t n_buckets, int n_regions,
+                                                             int32_t* __restrict__ cursor, uint4* __restrict__ bins) {
+  extern __shared__ int32_t s_hist[];
+  constexpr int kItems = kBinItems / 2;
+  for (int i = threadIdx.x; i < n_regions; i += kBinThreads) s_hist[i] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kBinThreads * kItems);
+  uint32_t reg[kItems], lrank[kItems];
+  Key<A> k[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBinThreads + threadIdx.x;
+    if (p < n) {
+      k[it] = load_key<A>(keys, p, A);
+      uint32_t home;
+      reg[it] = region_of_key<A>(k[it], n_buckets, &home);
+      lrank[it] = static_cast<uint32_t>(atomicAdd(&s_hist[reg[it]], 1));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_regions; i += kBinThreads)
+    if (s_hist[i]) s_hist[i] = atomicAdd(&cursor[i], s_hist[i]);
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBinThreads + threadIdx.x;
+    if (p < n)
+      bins[s_hist[reg[it]] + lrank[it]] = make_uint4(k[it].w[0], k[it].w[1], k[it].w[2], static_cast<uint32_t>(p));
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_ld_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+enum { kRegFound = 0, kRegClaimed = 1, kRegJoined = 2, kRegSpill = 3 };
+
+// Pass 1 of a record inside its region (shared-memory slots s, nb local
+// buckets).  EMPTY -> LOCK (CAS) -> key words -> PEND|pos, so a reader that
+// sees a state other than EMPTY / LOCK / TOMB may compare the key words.
+template <int A>
+__device__ int region_claim(uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3], uint32_t pos,
+                            uint32_t* dirty, int* tombs_used) {
+  const uint32_t me = PEND | pos;
+  int free_slot = -1;
+  uint32_t sl = 2 * lb;
+  while (sl < 2 * nb) {
+    uint32_t* stp = &s[sl].w;
+    uint32_t st = smem_ld_volatile(stp);
+    while (st == LOCK) {  // the writer may be in this warp: yield so it can finish
+      __nanosleep(32);
+      st = smem_ld_volatile(stp);
+    }
+    if (st == EMPTY) {
+      const int target = free_slot >= 0 ? free_slot : static_cast<int>(sl);
+      const uint32_t expect = free_slot >= 0 ? TOMB : EMPTY;
+      if (atomicCAS(&s[target].w, expect, LOCK) == expect) {
+        volatile uint32_t* vs = reinterpret_cast<volatile uint32_t*>(&s[target]);
+        vs[0] = w[0];
+        vs[1] = w[1];
+        vs[2] = w[2];
+        __threadfence_block();
+        vs[3] = me;
+        atomicOr(&dirty[target >> 6], 1u << ((target >> 1) & 31));
+        if (free_slot >= 0) ++*tombs_used;
+        return kRegClaimed;
+      }
+      if (free_slot >= 0) {  // the tombstone went to another key (maybe ours): rescan from it
+        sl = static_cast<uint32_t>(free_slot);
+        free_slot = -1;
+      }
+      continue;  // re-read this slot
+    }
+    if (st == TOMB) {
+      if (free_slot < 0) free_slot = static_cast<int>(sl);
+      ++sl;
+      continue;
+    }
+    __threadfence_block();
+    const volatile uint32_t* vs = reinterpret_cast<const volatile uint32_t*>(&s[sl]);
+    const bool match = vs[0] == w[0] && (A < 2 || vs[1] == w[1]) && (A < 3 || vs[2] == w[2]);
+    if (match) {
+      if (st < PEND) return kRegFound;
+      if (st > me) atomicMin(stp, me);
+      return kRegJoined;
+    }
+    ++sl;
+  }
+  return kRegSpill;
+}
+
+// Pass 2 (read-only, after every claim of the region): where did pos end up?
+template <int A>
+__device__ __forceinline__ int region_lookup(const uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3],
+                                             uint32_t* slot, uint32_t* state) {
+  for (uint32_t sl = 2 * lb; sl < 2 * nb; ++sl) {
+    const uint4 v = s[sl];
+    if (v.w == EMPTY) return kRegSpill;  // cannot happen: pass 1 would have claimed it
+    if (v.w == TOMB) continue;
+    if (v.x == w[0] && (A < 2 || v.y == w[1]) && (A < 3 || v.z == w[2])) {
+      *slot = sl;
+      *state = v.w;
+      return v.w < PEND ? kRegFound : kRegJoined;
+    }
+  }
+  return kRegSpill;
+}
+
+template <int A>
+__global__ void __launch_bounds__(kRegionThreads)
+    k_region_claim(Table t, const uint4* __restrict__ bins, const int32_t* __restrict__ region_off,
+                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, int32_t* counters,
+                   int32_t* __restrict__ spill, int32_t* spill_cnt) {
+  extern __shared__ __align__(16) uint4 s_slots[];
+  __shared__ uint32_t s_dirty[kRegionBuckets / 32];
+  __shared__ int s_tombs;
+  const int r = blockIdx.x;
+  const uint32_t b0 = static_cast<uint32_t>(r) * kRegionBuckets;
+  const uint32_t nb = min(static_cast<uint32_t>(kRegionBuckets), t.n_buckets - b0);
+  const int32_t lo = region_off[r], hi = region_off[r + 1];
+  const int32_t cnt = hi - lo;
+  const int lane = threadIdx.x & 31;
+  if (cnt == 0) return;
+  if (cnt > kRegionMaxRecords) {  // heavy duplication: the global claim handles it
+    __shared__ int32_t s_base;
+    if (threadIdx.x == 0) s_base = atomicAdd(spill_cnt, cnt);
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < cnt; i += kRegionThreads) {
+      const uint32_t pos = bins[lo + i].w;
+      spill[s_base + i] = static_cast<int32_t>(pos);
+      mask[pos] = 0;
+    }
+    return;
+  }
+  const uint4* src = t.slots + 2 * static_cast<size_t>(b0);
+  for (uint32_t i = threadIdx.x; i < 2 * nb; i += kRegionThreads) s_slots[i] = src[i];
+  for (int i = threadIdx.x; i < kRegionBuckets / 32; i += kRegionThreads) s_dirty[i] = 0;
+  if (threadIdx.x == 0) s_tombs = 0;
+  __syncthreads();
+  int tombs = 0;
+  for (int32_t i = lo + threadIdx.x; i < hi; i += kRegionThreads) {
+    const uint4 rec = bins[i];
+    const uint32_t w[3] = {rec.x, rec.y, rec.z};
+    Key<A> k;
+    k.row = nullptr;
+    k.w[0] = rec.x, k.w[1] = rec.y, k.w[2] = rec.z;
+    const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
+    region_claim<A>(s_slots, nb, lb, w, rec.w, s_dirty, &tombs);
+  }
+  if (tombs) atomicAdd(&s_tombs, tombs);
+  __syncthreads();
+  for (int32_t i0 = lo; i0 < hi; i0 += kRegionThreads) {
+    const int32_t i = i0 + threadIdx.x;
+    bool spilled = false;
+    uint32_t pos = 0;
+    if (i < hi) {
+      const uint4 rec = bins[i];
+      pos = rec.w;
+      const uint32_t w[3] = {rec.x, rec.y, rec.z};
+      Key<A> k;
+      k.row = nullptr;
+      k.w[0] = rec.x, k.w[1] = rec.y, k.w[2] = rec.z;
+      const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
+      uint32_t sl = 0, st = 0;
+      const int res = region_lookup<A>(s_slots, nb, lb, w, &sl, &st);
+      if (res == kRegFound) {
+        tmp[pos] = static_cast<int32_t>(st);
+        mask[pos] = 0;
+      } else if (res == kRegJoined && st == (PEND | pos)) {
+        tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + sl));
+        mask[pos] = 0;
+      } else if (res == kRegJoined) {
+        tmp[pos] = static_cast<int32_t>(PEND);
+        mask[pos] = DEMOTED;
+      } else {
+        spilled = true;
+        mask[pos] = 0;
+      }
+    }
+    const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
+    if (sp) {
+      int32_t base = 0;
+      if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
+      base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
+      if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
+    }
+  }
+  // dirty buckets back to the table (32 bytes each)
+  uint4* dst = t.slots + 2 * static_cast<size_t>(b0);
+  for (uint32_t b = threadIdx.x; b < nb; b += kRegionThreads) {
+    if (s_dirty[b >> 5] & (1u << (b & 31))) {
+      dst[2 * b] = s_slots[2 * b];
+      dst[2 * b + 1] = s_slots[2 * b + 1];
+    }
+  }
+  if (threadIdx.x == 0 && s_tombs) atomicSub(&counters[ASH_CTR_TOMBS], s_tombs);
+}
+
+// Spilled records on the global table (k_claim's probe); the list is in no
+// particular order, so a group of equal keys in a warp resolves through its
+// lowest batch position, not its lowest lane.
+template <int A>
+__global__ void __launch_bounds__(kBlock) k_claim_spill(Table t, const int32_t* __restrict__ keys,
+                                                        const int32_t* __restrict__ spill, const int32_t* spill_cnt,
+                                                        int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
+                                                        int32_t* counters, int32_t* tile_cnt) {
+  const int32_t n = *spill_cnt;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kBlock;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(kBlock) + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool valid = i < n;
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
+    if (!valid) continue;
+    const uint32_t pos = static_cast<uint32_t>(spill[i]);
+    Key<A> k = load_key<A>(keys, pos, A);
+    const uint32_t h = hash_key<A>(k, A);
+    unsigned grp = __match_any_sync(live, h);
+    unsigned g2;
+    same_key_in_warp<A>(k, live, &g2);
+    grp &= g2;
+    const uint32_t minpos = __reduce_min_sync(grp, pos);
+    const int leader = __ffs(__ballot_sync(grp, pos == minpos)) - 1;
+    uint32_t res = 0;
+    bool tomb = false, cand = false;
+    if (lane == leader)
+      res = probe_claim<A>(t, k, h, pos, keys, mask, counters, tile_cnt, &tomb, &cand);
+    if (tomb) atomicSub(&counters[ASH_CTR_TOMBS], 1);
+    const uint32_t lres = __shfl_sync(grp, res, leader);
+    if (lane == leader) {
+      tmp[pos] = static_cast<int32_t>(res);
+    } else if (lres < PEND) {
+      tmp[pos] = static_cast<int32_t>(lres);
+    } else {
+      tmp[pos] = static_cast<int32_t>(PEND);
+      mask[pos] = DEMOTED;
+    }
+  }
+}
+
+// Winners per 2048-position tile from the scratch encoding (overwrites the
+// counts; the binned claim does not keep them incrementally)
+__global__ void __launch_bounds__(kBlock) k_tile_count(const int32_t* __restrict__ tmp,
+                                                       const uint8_t* __restrict__ mask, int64_t n,
+                                                       int32_t* __restrict__ tile_cnt) {
+  __shared__ int32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+  int c = 0;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p < n && tmp[p] < 0 && !(mask[p] & DEMOTED)) ++c;
+  }
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_cnt;
+}
+
+// ---------------------------------------------------------------------------
 // single-pass (decoupled look-back) tile scan over a 0/1 predicate
 
 constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
@@ -1797,6 +2154,10 @@ int arity_class(int arity) { return arity <= 3 ? arity : 0; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int g_commit_bulk = -1;  // ASH_COMMIT_BULK=0 selects the plain commit (A/B runs)
+int g_bin_div = 0;       // binned claim when n * g_bin_div >= n_slots (0: never)
+constexpr int64_t kMinBinned = 1 << 16;
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 int g_sweep_div = 5;     // table sweep when winners >= n_buckets / g_sweep_div (0: never)
 
 void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words, const ash_map_t* m, int64_t sweep_min,
@@ -1898,6 +2259,12 @@ int ash_set_commit_mode(int32_t bulk, int32_t sweep_div) {
   return ASH_OK;
 }
 
+int ash_set_claim_mode(int32_t bin_div) {
+  if (bin_div < 0) return fail(ASH_ERR_INVALID, "bin divisor must be >= 0");
+  g_bin_div = bin_div;
+  return ASH_OK;
+}
+
 int ash_set_stream_hints(int32_t on) {
   g_stream_hints = on ? 1u : 0u;
   return ASH_OK;
@@ -1961,6 +2328,11 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
   return check_launch("ash_find_lattice");
 }
 
+int64_t ash_bin_ws_bytes(int64_t n, int64_t n_slots) {
+  const int64_t regions = (n_slots / 2 + kRegionBuckets - 1) / kRegionBuckets;
+  return align256(n * 16) + align256(n * 4) + 3 * align256((regions + 1) * 4) + 256;
+}
+
 int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
                      void* stream) {
   if (int rc = check_map(m)) return rc;
@@ -1969,8 +2341,59 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   if (!keys || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
   Table t = make_table(m);
   cudaStream_t s = as_stream(stream);
-  cudaMemsetAsync(out_mask, 0, n, s);
   if (int rc = check_tiles(m, n)) return rc;
+  const int64_t n_regions = (t.n_buckets + kRegionBuckets - 1) / kRegionBuckets;
+  if (g_bin_div > 0 && m->arity <= 3 && n >= kMinBinned && n * g_bin_div >= m->n_slots && n_regions <= kMaxRegions &&
+      m->bin_ws && m->bin_ws_bytes >= ash_bin_ws_bytes(n, m->n_slots)) {
+    uint8_t* ws = static_cast<uint8_t*>(m->bin_ws);
+    uint4* bins = reinterpret_cast<uint4*>(ws);
+    ws += align256(n * 16);
+    int32_t* spill = reinterpret_cast<int32_t*>(ws);
+    ws += align256(n * 4);
+    int32_t* region_cnt = reinterpret_cast<int32_t*>(ws);
+    ws += align256((n_regions + 1) * 4);
+    int32_t* region_off = reinterpret_cast<int32_t*>(ws);
+    ws += align256((n_regions + 1) * 4);
+    int32_t* cursor = reinterpret_cast<int32_t*>(ws);
+    ws += align256((n_regions + 1) * 4);
+    int32_t* spill_cnt = reinterpret_cast<int32_t*>(ws);
+    cudaMemsetAsync(region_cnt, 0, sizeof(int32_t) * n_regions, s);
+    cudaMemsetAsync(spill_cnt, 0, sizeof(int32_t), s);
+    const int nr = static_cast<int>(n_regions);
+    const size_t hist = sizeof(int32_t) * nr;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(k_region_claim<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
+      cudaFuncSetAttribute(k_region_claim<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
+      cudaFuncSetAttribute(k_region_claim<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
+      attr_done = true;
+    }
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+#define ASH_BINNED(A_)                                                                                             \
+  k_bin_count<A_><<<grid_for(n, kBinThreads * kBinItems), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr,      \
+                                                                                   region_cnt);                  \
+  k_excl_scan<<<1, 1024, 0, s>>>(region_cnt, nr, region_off, cursor);                                            \
+  k_bin_scatter<A_><<<grid_for(n, kBinThreads * kBinItems / 2), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr, \
+                                                                                       cursor, bins);             \
+  k_region_claim<A_><<<nr, kRegionThreads, kRegionSlots * 16, s>>>(t, bins, region_off, out_idx, out_mask,         \
+                                                                   m->counters, spill, spill_cnt);               \
+  k_claim_spill<A_><<<sms * 4, kBlock, 0, s>>>(t, keys, spill, spill_cnt, out_idx, out_mask, m->counters,         \
+                                               m->tile_counts);
+    switch (m->arity) {
+      case 1: ASH_BINNED(1); break;
+      case 2: ASH_BINNED(2); break;
+      default: ASH_BINNED(3); break;
+    }
+#undef ASH_BINNED
+    k_tile_count<<<grid_for(n, kTile), kBlock, 0, s>>>(out_idx, out_mask, n, m->tile_counts);
+    return check_launch("ash_insert_claim (binned)");
+  }
+  cudaMemsetAsync(out_mask, 0, n, s);
   ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
                                                                                  m->counters, m->tile_counts)));
   return check_launch("ash_insert_claim");
