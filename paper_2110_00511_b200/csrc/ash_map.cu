@@ -188,6 +188,68 @@ __device__ __forceinline__ void copy_row(uint8_t* dst, const uint8_t* src, int64
 }
 
 // ---------------------------------------------------------------------------
+// mbarrier / bulk-copy (TMA 1-D) helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-byte
+// aligned), completion counted on `bar`; L2 evict-first (read-once stream)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Copy `bytes` from src to dst: the 16-byte multiple through the bulk engine,
+// the tail (< 16 bytes) by the calling thread.  Returns the bulk byte count.
+__device__ __forceinline__ uint32_t stage_range(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                uint64_t pol) {
+  const uint32_t main = bytes & ~15u;
+  if (main) bulk_g2s(dst, src, main, bar, pol);
+  if ((bytes & 3) == 0) {
+    for (uint32_t b = main; b < bytes; b += 4)
+      *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dst) + b) =
+          __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(src) + b));
+  } else {
+    for (uint32_t b = main; b < bytes; ++b)
+      static_cast<uint8_t*>(dst)[b] = __ldg(static_cast<const uint8_t*>(src) + b);
+  }
+  return main;
+}
+
+// ---------------------------------------------------------------------------
 // hashing: murmur3-style word mix; only bucket_count is observable in the
 // reference (tests/test_hashmap.py:26-28), so the table uses its own hash.
 
@@ -665,14 +727,14 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
 // All records of one key share a home bucket, so they resolve in the same
 // place, and the lowest position still wins (atomicMin on the pending state).
 
-constexpr int kRegionBuckets = 2048;
+constexpr int kRegionBuckets = 1024;
 constexpr int kRegionSlots = 2 * kRegionBuckets;
 constexpr int kRegionMaxRecords = 1 << 16;  // beyond: the region's records spill
-constexpr int kMaxRegions = 12288;          // shared histogram limit (48 KB)
+constexpr int kMaxRegions = 8192;           // 18-bit packing, 32 KB shared histogram
 constexpr int kBinThreads = 512;
 constexpr int kBinItems = 16;
-constexpr int kRegionThreads = 512;
-constexpr uint32_t LOCK = 0xFFFFFFFDu;      // region-claim slot being written
+constexpr int kRegionThreads = 256;
+constexpr int kRegionItems = 8;  // records cached in registers per thread (fast path)
 
 template <int A>
 __device__ __forceinline__ uint32_t region_of_key(const Key<A>& k, uint32_t n_buckets, uint32_t* home) {
@@ -688,12 +750,22 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_count(const int32_t* __rest
   for (int i = threadIdx.x; i < n_regions; i += kBinThreads) s_hist[i] = 0;
   __syncthreads();
   const int64_t base = blockIdx.x * static_cast<int64_t>(kBinThreads * kBinItems);
-#pragma unroll 4
-  for (int it = 0; it < kBinItems; ++it) {
-    const int64_t p = base + it * kBinThreads + threadIdx.x;
-    if (p < n) {
-      uint32_t home;
-      atomicAdd(&s_hist[region_of_key<A>(load_key<A>(keys, p, A), n_buckets, &home)], 1);
+  constexpr int kHalf = kBinItems / 2;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    Key<A> k[kHalf];
+#pragma unroll
+    for (int it = 0; it < kHalf; ++it) {  // all loads of the half first
+      const int64_t p = base + (h * kHalf + it) * kBinThreads + threadIdx.x;
+      if (p < n) k[it] = load_key<A>(keys, p, A);
+    }
+#pragma unroll
+    for (int it = 0; it < kHalf; ++it) {
+      const int64_t p = base + (h * kHalf + it) * kBinThreads + threadIdx.x;
+      if (p < n) {
+        uint32_t home;
+        atomicAdd(&s_hist[region_of_key<A>(k[it], n_buckets, &home)], 1);
+      }
     }
   }
   __syncthreads();
@@ -740,98 +812,58 @@ __global__ void __launch_bounds__(1024) k_excl_scan(const int32_t* __restrict__ 
   if (threadIdx.x == 0) out[n] = carry;
 }
 
+constexpr int kScatterThreads = 1024;
+constexpr int kScatterItems = 16;
+
 template <int A>
-__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const int32_t* __restrict__ keys, int64_t n,
-                                                             uint32_t n_buckets, int n_regions,
-                                                             int32_t* __restrict__ cursor, uint4* __restrict__ bins) {
+__global__ void __launch_bounds__(kScatterThreads) k_bin_scatter(const int32_t* __restrict__ keys, int64_t n,
+                                                                 uint32_t n_buckets, int n_regions,
+                                                                 int32_t* __restrict__ cursor,
+                                                                 uint4* __restrict__ bins) {
+  // 16K positions per block, so each region's cursor is reserved once per
+  // block for a run of ~n / (blocks x regions) records; (region, rank in
+  // block) packed in one register per item, key words re-read (L2-hot) for
+  // the record writes
   extern __shared__ int32_t s_hist[];
-  constexpr int kItems = kBinItems / 2;
-  for (int i = threadIdx.x; i < n_regions; i += kBinThreads) s_hist[i] = 0;
+  for (int i = threadIdx.x; i < n_regions; i += kScatterThreads) s_hist[i] = 0;
   __syncthreads();
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kBinThreads * kItems);
-  uint32_t reg[kItems], lrank[kItems];
-  Key<A> k[kItems];
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kScatterThreads * kScatterItems);
+  uint32_t packed[kScatterItems];
+  constexpr int kHalf = kScatterItems / 2;
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int64_t p = base + it * kBinThreads + threadIdx.x;
-    if (p < n) {
-      k[it] = load_key<A>(keys, p, A);
-      uint32_t home;
-      reg[it] = region_of_key<A>(k[it], n_buckets, &home);
-      lrank[it] = static_cast<uint32_t>(atomicAdd(&s_hist[reg[it]], 1));
+  for (int h = 0; h < 2; ++h) {
+    Key<A> k[kHalf];
+#pragma unroll
+    for (int it = 0; it < kHalf; ++it) {
+      const int64_t p = base + (h * kHalf + it) * kScatterThreads + threadIdx.x;
+      if (p < n) k[it] = load_key<A>(keys, p, A);
+    }
+#pragma unroll
+    for (int it = 0; it < kHalf; ++it) {
+      const int64_t p = base + (h * kHalf + it) * kScatterThreads + threadIdx.x;
+      if (p < n) {
+        uint32_t home;
+        const uint32_t r = region_of_key<A>(k[it], n_buckets, &home);
+        packed[h * kHalf + it] = (r << 18) | static_cast<uint32_t>(atomicAdd(&s_hist[r], 1));
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n_regions; i += kBinThreads)
+  for (int i = threadIdx.x; i < n_regions; i += kScatterThreads)
     if (s_hist[i]) s_hist[i] = atomicAdd(&cursor[i], s_hist[i]);
   __syncthreads();
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int64_t p = base + it * kBinThreads + threadIdx.x;
-    if (p < n)
-      bins[s_hist[reg[it]] + lrank[it]] = make_uint4(k[it].w[0], k[it].w[1], k[it].w[2], static_cast<uint32_t>(p));
+  for (int it = 0; it < kScatterItems; ++it) {
+    const int64_t p = base + it * kScatterThreads + threadIdx.x;
+    if (p < n) {
+      const Key<A> k = load_key<A>(keys, p, A);
+      const uint32_t r = packed[it] >> 18, lr = packed[it] & 0x3FFFFu;
+      bins[s_hist[r] + lr] = make_uint4(k.w[0], k.w[1], k.w[2], static_cast<uint32_t>(p));
+    }
   }
-}
-
-__device__ __forceinline__ uint32_t smem_ld_volatile(const uint32_t* p) {
-  return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
 enum { kRegFound = 0, kRegClaimed = 1, kRegJoined = 2, kRegSpill = 3 };
-
-// Pass 1 of a record inside its region (shared-memory slots s, nb local
-// buckets).  EMPTY -> LOCK (CAS) -> key words -> PEND|pos, so a reader that
-// sees a state other than EMPTY / LOCK / TOMB may compare the key words.
-template <int A>
-__device__ int region_claim(uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3], uint32_t pos,
-                            uint32_t* dirty, int* tombs_used) {
-  const uint32_t me = PEND | pos;
-  int free_slot = -1;
-  uint32_t sl = 2 * lb;
-  while (sl < 2 * nb) {
-    uint32_t* stp = &s[sl].w;
-    uint32_t st = smem_ld_volatile(stp);
-    while (st == LOCK) {  // the writer may be in this warp: yield so it can finish
-      __nanosleep(32);
-      st = smem_ld_volatile(stp);
-    }
-    if (st == EMPTY) {
-      const int target = free_slot >= 0 ? free_slot : static_cast<int>(sl);
-      const uint32_t expect = free_slot >= 0 ? TOMB : EMPTY;
-      if (atomicCAS(&s[target].w, expect, LOCK) == expect) {
-        volatile uint32_t* vs = reinterpret_cast<volatile uint32_t*>(&s[target]);
-        vs[0] = w[0];
-        vs[1] = w[1];
-        vs[2] = w[2];
-        __threadfence_block();
-        vs[3] = me;
-        atomicOr(&dirty[target >> 6], 1u << ((target >> 1) & 31));
-        if (free_slot >= 0) ++*tombs_used;
-        return kRegClaimed;
-      }
-      if (free_slot >= 0) {  // the tombstone went to another key (maybe ours): rescan from it
-        sl = static_cast<uint32_t>(free_slot);
-        free_slot = -1;
-      }
-      continue;  // re-read this slot
-    }
-    if (st == TOMB) {
-      if (free_slot < 0) free_slot = static_cast<int>(sl);
-      ++sl;
-      continue;
-    }
-    __threadfence_block();
-    const volatile uint32_t* vs = reinterpret_cast<const volatile uint32_t*>(&s[sl]);
-    const bool match = vs[0] == w[0] && (A < 2 || vs[1] == w[1]) && (A < 3 || vs[2] == w[2]);
-    if (match) {
-      if (st < PEND) return kRegFound;
-      if (st > me) atomicMin(stp, me);
-      return kRegJoined;
-    }
-    ++sl;
-  }
-  return kRegSpill;
-}
 
 // Pass 2 (read-only, after every claim of the region): where did pos end up?
 template <int A>
@@ -850,14 +882,95 @@ __device__ __forceinline__ int region_lookup(const uint4* s, uint32_t nb, uint32
   return kRegSpill;
 }
 
+__device__ __forceinline__ uint4 lds128_volatile(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p))
+               : "memory");
+  return r;
+}
+
+// 128-bit CAS on a shared-memory slot; returns the previous contents
+__device__ __forceinline__ uint4 cas128_shared(uint4* addr, uint4 cmp, uint4 val) {
+  unsigned long long clo = ((unsigned long long)cmp.y << 32) | cmp.x;
+  unsigned long long chi = ((unsigned long long)cmp.w << 32) | cmp.z;
+  unsigned long long vlo = ((unsigned long long)val.y << 32) | val.x;
+  unsigned long long vhi = ((unsigned long long)val.w << 32) | val.z;
+  unsigned long long olo, ohi;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.shared::cta.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(olo), "=l"(ohi)
+      : "l"(clo), "l"(chi), "l"(vlo), "l"(vhi), "r"(smem_u32(addr))
+      : "memory");
+  return make_uint4(static_cast<uint32_t>(olo), static_cast<uint32_t>(olo >> 32), static_cast<uint32_t>(ohi),
+                    static_cast<uint32_t>(ohi >> 32));
+}
+
+// Pass 1 of a record inside its region (shared-memory slots s, nb local
+// buckets): the global claim protocol on shared memory — a 128-bit CAS takes
+// an EMPTY (or the first TOMB) slot with {key, PEND|pos} in one step, a
+// pending match joins with atomicMin.  Returns where the record landed:
+// bit 31 found (low bits = buffer index), bit 30 spill, else the local slot.
+constexpr uint32_t kOutFound = 0x80000000u, kOutSpill = 0x40000000u;
+
+template <int A>
+__device__ __forceinline__ uint32_t region_claim_out(uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3],
+                                                     uint32_t pos, uint32_t* dirty, int* tombs) {
+  const uint32_t me = PEND | pos;
+  int free_slot = -1;
+  uint4 free_val = make_uint4(0, 0, 0, 0);
+  uint32_t sl = 2 * lb;
+  while (sl < 2 * nb) {
+    const uint4 v = lds128_volatile(&s[sl]);
+    if (v.w == EMPTY) {
+      const bool use_tomb = free_slot >= 0;
+      const uint32_t target = use_tomb ? static_cast<uint32_t>(free_slot) : sl;
+      const uint4 expect = use_tomb ? free_val : v;
+      const uint4 old = cas128_shared(&s[target], expect, make_uint4(w[0], w[1], w[2], me));
+      if (old.x == expect.x && old.y == expect.y && old.z == expect.z && old.w == expect.w) {
+        atomicOr(&dirty[target >> 6], 1u << ((target >> 1) & 31));
+        if (use_tomb) ++*tombs;
+        return target;
+      }
+      if (use_tomb) {  // the tombstone went to another key (maybe ours): rescan from it
+        sl = target;
+        free_slot = -1;
+      }
+      continue;  // re-read the slot
+    }
+    if (v.w == TOMB) {
+      if (free_slot < 0) {
+        free_slot = static_cast<int>(sl);
+        free_val = v;
+      }
+      ++sl;
+      continue;
+    }
+    if (v.x == w[0] && (A < 2 || v.y == w[1]) && (A < 3 || v.z == w[2])) {
+      if (v.w < PEND) return kOutFound | v.w;
+      if (v.w > me) atomicMin(&s[sl].w, me);
+      return sl;
+    }
+    ++sl;
+  }
+  return kOutSpill;
+}
+
 template <int A>
 __global__ void __launch_bounds__(kRegionThreads)
     k_region_claim(Table t, const uint4* __restrict__ bins, const int32_t* __restrict__ region_off,
                    int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, int32_t* counters,
                    int32_t* __restrict__ spill, int32_t* spill_cnt) {
-  extern __shared__ __align__(16) uint4 s_slots[];
+  extern __shared__ __align__(128) uint4 s_slots[];
   __shared__ uint32_t s_dirty[kRegionBuckets / 32];
   __shared__ int s_tombs;
+  __shared__ int32_t s_base;
+  __shared__ __align__(8) uint64_t s_bar;
   const int r = blockIdx.x;
   const uint32_t b0 = static_cast<uint32_t>(r) * kRegionBuckets;
   const uint32_t nb = min(static_cast<uint32_t>(kRegionBuckets), t.n_buckets - b0);
@@ -866,7 +979,6 @@ __global__ void __launch_bounds__(kRegionThreads)
   const int lane = threadIdx.x & 31;
   if (cnt == 0) return;
   if (cnt > kRegionMaxRecords) {  // heavy duplication: the global claim handles it
-    __shared__ int32_t s_base;
     if (threadIdx.x == 0) s_base = atomicAdd(spill_cnt, cnt);
     __syncthreads();
     for (int32_t i = threadIdx.x; i < cnt; i += kRegionThreads) {
@@ -876,57 +988,123 @@ __global__ void __launch_bounds__(kRegionThreads)
     }
     return;
   }
-  const uint4* src = t.slots + 2 * static_cast<size_t>(b0);
-  for (uint32_t i = threadIdx.x; i < 2 * nb; i += kRegionThreads) s_slots[i] = src[i];
-  for (int i = threadIdx.x; i < kRegionBuckets / 32; i += kRegionThreads) s_dirty[i] = 0;
-  if (threadIdx.x == 0) s_tombs = 0;
-  __syncthreads();
-  int tombs = 0;
-  for (int32_t i = lo + threadIdx.x; i < hi; i += kRegionThreads) {
-    const uint4 rec = bins[i];
-    const uint32_t w[3] = {rec.x, rec.y, rec.z};
-    Key<A> k;
-    k.row = nullptr;
-    k.w[0] = rec.x, k.w[1] = rec.y, k.w[2] = rec.z;
-    const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
-    region_claim<A>(s_slots, nb, lb, w, rec.w, s_dirty, &tombs);
+  // the region's slots through the bulk-copy engine while the threads load
+  // their records
+  const uint32_t bytes = 2 * nb * 16;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(&s_bar, bytes);
+    bulk_g2s(s_slots, t.slots + 2 * static_cast<size_t>(b0), bytes, &s_bar, stream_policy(0));
+    s_tombs = 0;
   }
-  if (tombs) atomicAdd(&s_tombs, tombs);
+  for (int i = threadIdx.x; i < kRegionBuckets / 32; i += kRegionThreads) s_dirty[i] = 0;
+  const bool fast = cnt <= kRegionThreads * kRegionItems;
+  uint4 rec[kRegionItems];
+  if (fast) {
+#pragma unroll
+    for (int it = 0; it < kRegionItems; ++it) {
+      const int32_t i = lo + it * kRegionThreads + threadIdx.x;
+      if (i < hi) rec[it] = bins[i];
+    }
+  }
   __syncthreads();
-  for (int32_t i0 = lo; i0 < hi; i0 += kRegionThreads) {
-    const int32_t i = i0 + threadIdx.x;
-    bool spilled = false;
-    uint32_t pos = 0;
-    if (i < hi) {
-      const uint4 rec = bins[i];
-      pos = rec.w;
-      const uint32_t w[3] = {rec.x, rec.y, rec.z};
+  mbar_wait(&s_bar, 0);
+  int tombs = 0;
+  if (fast) {
+    uint32_t out[kRegionItems];
+#pragma unroll
+    for (int it = 0; it < kRegionItems; ++it) {
+      const int32_t i = lo + it * kRegionThreads + threadIdx.x;
+      if (i >= hi) continue;
+      const uint32_t w[3] = {rec[it].x, rec[it].y, rec[it].z};
       Key<A> k;
       k.row = nullptr;
-      k.w[0] = rec.x, k.w[1] = rec.y, k.w[2] = rec.z;
+      k.w[0] = w[0], k.w[1] = w[1], k.w[2] = w[2];
       const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
-      uint32_t sl = 0, st = 0;
-      const int res = region_lookup<A>(s_slots, nb, lb, w, &sl, &st);
-      if (res == kRegFound) {
-        tmp[pos] = static_cast<int32_t>(st);
-        mask[pos] = 0;
-      } else if (res == kRegJoined && st == (PEND | pos)) {
-        tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + sl));
-        mask[pos] = 0;
-      } else if (res == kRegJoined) {
-        tmp[pos] = static_cast<int32_t>(PEND);
-        mask[pos] = DEMOTED;
-      } else {
-        spilled = true;
-        mask[pos] = 0;
+      out[it] = region_claim_out<A>(s_slots, nb, lb, w, rec[it].w, s_dirty, &tombs);
+    }
+    if (tombs) atomicAdd(&s_tombs, tombs);
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kRegionItems; ++it) {
+      const int32_t i0 = lo + it * kRegionThreads;
+      if (i0 >= hi) break;  // uniform
+      const int32_t i = i0 + threadIdx.x;
+      bool spilled = false;
+      uint32_t pos = 0;
+      if (i < hi) {
+        pos = rec[it].w;
+        const uint32_t o = out[it];
+        if (o & kOutFound) {
+          tmp[pos] = static_cast<int32_t>(o & ~kOutFound);
+          mask[pos] = 0;
+        } else if (o & kOutSpill) {
+          spilled = true;
+          mask[pos] = 0;
+        } else if (s_slots[o].w == (PEND | pos)) {
+          tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + o));
+          mask[pos] = 0;
+        } else {
+          tmp[pos] = static_cast<int32_t>(PEND);
+          mask[pos] = DEMOTED;
+        }
+      }
+      const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
+      if (sp) {
+        int32_t base = 0;
+        if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
+        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
+        if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
       }
     }
-    const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
-    if (sp) {
-      int32_t base = 0;
-      if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
-      base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
-      if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
+  } else {
+    for (int32_t i = lo + threadIdx.x; i < hi; i += kRegionThreads) {
+      const uint4 rc = bins[i];
+      const uint32_t w[3] = {rc.x, rc.y, rc.z};
+      Key<A> k;
+      k.row = nullptr;
+      k.w[0] = rc.x, k.w[1] = rc.y, k.w[2] = rc.z;
+      const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
+      region_claim_out<A>(s_slots, nb, lb, w, rc.w, s_dirty, &tombs);
+    }
+    if (tombs) atomicAdd(&s_tombs, tombs);
+    __syncthreads();
+    for (int32_t i0 = lo; i0 < hi; i0 += kRegionThreads) {
+      const int32_t i = i0 + threadIdx.x;
+      bool spilled = false;
+      uint32_t pos = 0;
+      if (i < hi) {
+        const uint4 rc = bins[i];
+        pos = rc.w;
+        const uint32_t w[3] = {rc.x, rc.y, rc.z};
+        Key<A> k;
+        k.row = nullptr;
+        k.w[0] = rc.x, k.w[1] = rc.y, k.w[2] = rc.z;
+        const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
+        uint32_t sl = 0, st = 0;
+        const int res = region_lookup<A>(s_slots, nb, lb, w, &sl, &st);
+        if (res == kRegFound) {
+          tmp[pos] = static_cast<int32_t>(st);
+          mask[pos] = 0;
+        } else if (res == kRegJoined && st == (PEND | pos)) {
+          tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + sl));
+          mask[pos] = 0;
+        } else if (res == kRegJoined) {
+          tmp[pos] = static_cast<int32_t>(PEND);
+          mask[pos] = DEMOTED;
+        } else {
+          spilled = true;
+          mask[pos] = 0;
+        }
+      }
+      const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
+      if (sp) {
+        int32_t base = 0;
+        if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
+        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
+        if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
+      }
     }
   }
   // dirty buckets back to the table (32 bytes each)
@@ -987,20 +1165,30 @@ __global__ void __launch_bounds__(kBlock) k_claim_spill(Table t, const int32_t* 
 __global__ void __launch_bounds__(kBlock) k_tile_count(const int32_t* __restrict__ tmp,
                                                        const uint8_t* __restrict__ mask, int64_t n,
                                                        int32_t* __restrict__ tile_cnt) {
-  __shared__ int32_t s_cnt;
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+  __shared__ int32_t s_cnt[kBlock / 32];
+  const int64_t p0 = blockIdx.x * static_cast<int64_t>(kTile) + threadIdx.x * kItems;  // 8 consecutive
   int c = 0;
+  if (p0 + kItems <= n) {
+    const int4 a = *reinterpret_cast<const int4*>(tmp + p0);
+    const int4 b = *reinterpret_cast<const int4*>(tmp + p0 + 4);
+    const uint2 mk = *reinterpret_cast<const uint2*>(mask + p0);
+    const int32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int64_t p = base + it * kBlock + threadIdx.x;
-    if (p < n && tmp[p] < 0 && !(mask[p] & DEMOTED)) ++c;
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m8 = ((i < 4 ? mk.x : mk.y) >> (8 * (i & 3))) & 0xFF;
+      c += v[i] < 0 && !(m8 & DEMOTED);
+    }
+  } else {
+    for (int64_t p = p0; p < n && p < p0 + kItems; ++p) c += tmp[p] < 0 && !(mask[p] & DEMOTED);
   }
   c = __reduce_add_sync(0xFFFFFFFFu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_cnt, c);
+  if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = c;
   __syncthreads();
-  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_cnt;
+  if (threadIdx.x < 32) {
+    int x = threadIdx.x < kBlock / 32 ? s_cnt[threadIdx.x] : 0;
+    x = __reduce_add_sync(0xFFFFFFFFu, x);
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = x;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1408,65 +1596,6 @@ __global__ void k_heap_dirty(int32_t* counters, int64_t n) {
 // heap[top + pre[t] .. top + pre[t+1]).  A producer warp streams them into
 // shared memory with cp.async.bulk (TMA 1-D) two tiles ahead, completion on an
 // mbarrier; eight consumer warps rank the winners and issue only stores.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// global -> shared bulk copy of `bytes` (multiple of 16, both ends 16-byte
-// aligned), completion counted on `bar`; L2 evict-first (read-once stream)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-
-__device__ __forceinline__ void named_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-// Copy `bytes` from src to dst: the 16-byte multiple through the bulk engine,
-// the tail (< 16 bytes) by the calling thread.  Returns the bulk byte count.
-__device__ __forceinline__ uint32_t stage_range(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                                uint64_t pol) {
-  const uint32_t main = bytes & ~15u;
-  if (main) bulk_g2s(dst, src, main, bar, pol);
-  if ((bytes & 3) == 0) {
-    for (uint32_t b = main; b < bytes; b += 4)
-      *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dst) + b) =
-          __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(src) + b));
-  } else {
-    for (uint32_t b = main; b < bytes; ++b)
-      static_cast<uint8_t*>(dst)[b] = __ldg(static_cast<const uint8_t*>(src) + b);
-  }
-  return main;
-}
 
 constexpr int kCommitConsumers = kBlock;             // 8 consumer warps
 constexpr int kCommitThreads = kBlock + 32;          // + 1 producer warp
@@ -2344,7 +2473,7 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   if (int rc = check_tiles(m, n)) return rc;
   const int64_t n_regions = (t.n_buckets + kRegionBuckets - 1) / kRegionBuckets;
   if (g_bin_div > 0 && m->arity <= 3 && n >= kMinBinned && n * g_bin_div >= m->n_slots && n_regions <= kMaxRegions &&
-      m->bin_ws && m->bin_ws_bytes >= ash_bin_ws_bytes(n, m->n_slots)) {
+      m->bin_ws && m->bin_ws_bytes >= ash_bin_ws_bytes(n, m->n_slots) && aligned16(out_idx) && aligned16(out_mask)) {
     uint8_t* ws = static_cast<uint8_t*>(m->bin_ws);
     uint4* bins = reinterpret_cast<uint4*>(ws);
     ws += align256(n * 16);
@@ -2378,8 +2507,8 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   k_bin_count<A_><<<grid_for(n, kBinThreads * kBinItems), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr,      \
                                                                                    region_cnt);                  \
   k_excl_scan<<<1, 1024, 0, s>>>(region_cnt, nr, region_off, cursor);                                            \
-  k_bin_scatter<A_><<<grid_for(n, kBinThreads * kBinItems / 2), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr, \
-                                                                                       cursor, bins);             \
+  k_bin_scatter<A_><<<grid_for(n, kScatterThreads * kScatterItems), kScatterThreads, hist, s>>>(                 \
+      keys, n, t.n_buckets, nr, cursor, bins);                                                                     \
   k_region_claim<A_><<<nr, kRegionThreads, kRegionSlots * 16, s>>>(t, bins, region_off, out_idx, out_mask,         \
                                                                    m->counters, spill, spill_cnt);               \
   k_claim_spill<A_><<<sms * 4, kBlock, 0, s>>>(t, keys, spill, spill_cnt, out_idx, out_mask, m->counters,         \
@@ -2394,8 +2523,8 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
     return check_launch("ash_insert_claim (binned)");
   }
   cudaMemsetAsync(out_mask, 0, n, s);
-  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
-                                                                                 m->counters, m->tile_counts)));
+  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(
+                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts)));
   return check_launch("ash_insert_claim");
 }
 
