@@ -97,6 +97,9 @@ int ash_device_setup(int32_t l2_fetch_bytes);
  * table keeps the L2 (default on; process-wide). */
 int ash_set_stream_hints(int32_t on);
 
+/* Kernels launched by this library so far (process-wide counter). */
+int64_t ash_launch_count(void);
+
 /* Insert commit strategy (process-wide; same results in every mode).
  *   bulk = 1: TMA-staged persistent commit where the batch qualifies (arity
  *             <= 3, one register-sized value buffer or none, 16-byte aligned

@@ -43,6 +43,7 @@ _SIGNATURES = {
     "ash_last_error": (c_char_p, []),
     "ash_device_setup": (c_int32, [c_int32]),
     "ash_set_stream_hints": (c_int32, [c_int32]),
+    "ash_launch_count": (c_int64, []),
     "ash_set_commit_mode": (c_int32, [c_int32, c_int32]),
     "ash_set_claim_mode": (c_int32, [c_int32]),
     "ash_bin_ws_bytes": (c_int64, [c_int64, c_int64]),

@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include "../../include/ash.h"
+#include "launch_count.h"
 
 namespace {
 
@@ -2250,7 +2251,7 @@ int32_t* split_prefix(const ash_map_t* m, int64_t n) {
 
 void launch_tile_scan(const ash_map_t* m, int64_t n, int top_slot, int total_slot, cudaStream_t s,
                       int32_t* pre_out = nullptr) {
-  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot, pre_out);
+  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot, pre_out); note_launch();
 }
 
 int check_scan(const ash_map_t* m, int64_t n) {
@@ -2300,7 +2301,7 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
   }
   unsigned g = grid_for(t.n_buckets, kBlock);
   const unsigned cap = static_cast<unsigned>(sms) * 8;
-  k_commit_sweep<<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min);
+  k_commit_sweep<<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min); note_launch();
 }
 
 template <int A, int VW>
@@ -2323,26 +2324,26 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
   const unsigned grid = static_cast<unsigned>(T < cap ? T : cap);
   k_commit_bulk<A, VW><<<grid, kCommitThreads, smem, s>>>(t, keys, n, va, assoc, out_idx, out_mask, m->heap,
                                                           m->capacity, m->active, m->key_buf, m->counters, pre, T,
-                                                          sweep_min, rank_words);
+                                                          sweep_min, rank_words); note_launch();
   return ASH_OK;
 }
 
 #define ASH_DISPATCH_ARITY(arity, KERNEL_CALL) \
   switch (arity_class(arity)) {                \
-    case 1: { constexpr int A = 1; KERNEL_CALL; break; } \
-    case 2: { constexpr int A = 2; KERNEL_CALL; break; } \
-    case 3: { constexpr int A = 3; KERNEL_CALL; break; } \
-    default: { constexpr int A = 0; KERNEL_CALL; break; } \
+    case 1: { constexpr int A = 1; KERNEL_CALL; note_launch(); break; } \
+    case 2: { constexpr int A = 2; KERNEL_CALL; note_launch(); break; } \
+    case 3: { constexpr int A = 3; KERNEL_CALL; note_launch(); break; } \
+    default: { constexpr int A = 0; KERNEL_CALL; note_launch(); break; } \
   }
 
 template <typename Src>
 void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
                       int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s) {
   k_voxel_claim<Src><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, src, n, scratch_idx, scratch_mask, ws->counters,
-                                                            ws->tile_counts);
+                                                            ws->tile_counts); note_launch();
   launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
   k_voxel_select<Src><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask, out_coords,
-                                                             out_sel, ws->tile_counts);
+                                                             out_sel, ws->tile_counts); note_launch();
 }
 
 int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t width, const double* cam,
@@ -2380,6 +2381,8 @@ int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t wid
 extern "C" {
 
 int ash_abi_version(void) { return ASH_ABI_VERSION; }
+
+int64_t ash_launch_count(void) { return ash_launch_counter().load(std::memory_order_relaxed); }
 
 int ash_set_commit_mode(int32_t bulk, int32_t sweep_div) {
   if (sweep_div < 0) return fail(ASH_ERR_INVALID, "sweep divisor must be >= 0");
@@ -2422,7 +2425,7 @@ int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream) {
   unsigned g = grid_for(work, kBlock);
   if (g > 148 * 16) g = 148 * 16;
   k_reset<<<g, kBlock, 0, s>>>(static_cast<uint4*>(m->slots), m->n_slots, m->heap, m->active,
-                               m->erase_claim, m->freed, m->capacity, m->counters);
+                               m->erase_claim, m->freed, m->capacity, m->counters); note_launch();
   if (zero_rows) {
     cudaMemsetAsync(m->key_buf, 0, sizeof(int32_t) * m->capacity * m->arity, s);
     for (int b = 0; b < m->n_values; ++b)
@@ -2453,7 +2456,7 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
   if (n > (int64_t(1) << 38) / K) return fail(ASH_ERR_INVALID, "too many lattice queries");
   if (!coords || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
   Table t = make_table(m);
-  k_find_lattice<<<grid_for(n * K, kBlock), kBlock, 0, as_stream(stream)>>>(t, coords, n, r, out_idx, out_mask);
+  k_find_lattice<<<grid_for(n * K, kBlock), kBlock, 0, as_stream(stream)>>>(t, coords, n, r, out_idx, out_mask); note_launch();
   return check_launch("ash_find_lattice");
 }
 
@@ -2505,21 +2508,21 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
     }
 #define ASH_BINNED(A_)                                                                                             \
   k_bin_count<A_><<<grid_for(n, kBinThreads * kBinItems), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr,      \
-                                                                                   region_cnt);                  \
-  k_excl_scan<<<1, 1024, 0, s>>>(region_cnt, nr, region_off, cursor);                                            \
+                                                                                   region_cnt); note_launch();                  \
+  k_excl_scan<<<1, 1024, 0, s>>>(region_cnt, nr, region_off, cursor); note_launch();                                            \
   k_bin_scatter<A_><<<grid_for(n, kScatterThreads * kScatterItems), kScatterThreads, hist, s>>>(                 \
-      keys, n, t.n_buckets, nr, cursor, bins);                                                                     \
+      keys, n, t.n_buckets, nr, cursor, bins); note_launch();                                                                     \
   k_region_claim<A_><<<nr, kRegionThreads, kRegionSlots * 16, s>>>(t, bins, region_off, out_idx, out_mask,         \
-                                                                   m->counters, spill, spill_cnt);               \
+                                                                   m->counters, spill, spill_cnt); note_launch();               \
   k_claim_spill<A_><<<sms * 4, kBlock, 0, s>>>(t, keys, spill, spill_cnt, out_idx, out_mask, m->counters,         \
-                                               m->tile_counts);
+                                               m->tile_counts); note_launch();
     switch (m->arity) {
       case 1: ASH_BINNED(1); break;
       case 2: ASH_BINNED(2); break;
       default: ASH_BINNED(3); break;
     }
 #undef ASH_BINNED
-    k_tile_count<<<grid_for(n, kTile), kBlock, 0, s>>>(out_idx, out_mask, n, m->tile_counts);
+    k_tile_count<<<grid_for(n, kTile), kBlock, 0, s>>>(out_idx, out_mask, n, m->tile_counts); note_launch();
     return check_launch("ash_insert_claim (binned)");
   }
   cudaMemsetAsync(out_mask, 0, n, s);
@@ -2626,8 +2629,8 @@ int ash_heap_put_losers(ash_map_t* m, const int32_t* sorted_losers, int64_t n, v
   if (int rc = check_map(m)) return rc;
   if (n < 0) return fail(ASH_ERR_INVALID, "negative batch length");
   if (n == 0) return ASH_OK;
-  k_heap_put_losers<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(m->heap, sorted_losers, n, m->counters);
-  k_heap_dirty<<<1, 1, 0, as_stream(stream)>>>(m->counters, n);  // heap above top is no longer the identity
+  k_heap_put_losers<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(m->heap, sorted_losers, n, m->counters); note_launch();
+  k_heap_dirty<<<1, 1, 0, as_stream(stream)>>>(m->counters, n); note_launch();  // heap above top is no longer the identity
   return check_launch("ash_heap_put_losers");
 }
 
@@ -2644,7 +2647,7 @@ int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* s
   if (n == 0) return ASH_OK;
   if (int rc = check_tiles(m, n)) return rc;
   k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n,
-                                                                    m->counters, m->tile_counts);
+                                                                    m->counters, m->tile_counts); note_launch();
   return check_launch("ash_insert_rollback");
 }
 
@@ -2659,10 +2662,10 @@ int ash_erase(ash_map_t* m, const int32_t* keys, int64_t n, uint8_t* out_mask, i
   ASH_DISPATCH_ARITY(m->arity, (k_erase_probe<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(
                                    t, keys, n, scratch, m->erase_claim, m->counters)));
   k_erase_commit<<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<uint4*>(m->slots), n, scratch, m->erase_claim,
-                                                         m->active, m->freed, out_mask, m->counters);
+                                                         m->active, m->freed, out_mask, m->counters); note_launch();
   uint32_t ep = next_epoch(m);
   k_free_compact<<<grid_for(m->capacity, kTile), kBlock, 0, s>>>(m->freed, m->capacity, m->heap, m->counters,
-                                                                  m->scan_status, ep);
+                                                                  m->scan_status, ep); note_launch();
   return check_launch("ash_erase");
 }
 
@@ -2671,7 +2674,7 @@ int ash_active_indices(ash_map_t* m, int32_t* out, void* stream) {
   if (int rc = check_scan(m, m->capacity)) return rc;
   uint32_t ep = next_epoch(m);
   k_active_compact<<<grid_for(m->capacity, kTile), kBlock, 0, as_stream(stream)>>>(
-      m->active, m->capacity, out, m->counters, m->scan_status, ep);
+      m->active, m->capacity, out, m->counters, m->scan_status, ep); note_launch();
   return check_launch("ash_active_indices");
 }
 
@@ -2704,7 +2707,7 @@ int ash_rebuild_table(ash_map_t* m, void* new_slots, int64_t new_n_slots, void* 
   cudaStream_t s = as_stream(stream);
   unsigned g = grid_for(new_n_slots, kBlock);
   if (g > 148 * 16) g = 148 * 16;
-  k_fill_empty<<<g, kBlock, 0, s>>>(static_cast<uint4*>(new_slots), new_n_slots);
+  k_fill_empty<<<g, kBlock, 0, s>>>(static_cast<uint4*>(new_slots), new_n_slots); note_launch();
   ash_map_t nm = *m;
   nm.slots = new_slots;
   nm.n_slots = new_n_slots;
@@ -2719,7 +2722,7 @@ int ash_table_clear(void* slots, int64_t n_slots, void* stream) {
   if (n_slots == 0) return ASH_OK;
   unsigned g = grid_for(n_slots, kBlock);
   if (g > 148 * 16) g = 148 * 16;
-  k_fill_empty<<<g, kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(slots), n_slots);
+  k_fill_empty<<<g, kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(slots), n_slots); note_launch();
   return check_launch("ash_table_clear");
 }
 
@@ -2730,9 +2733,12 @@ int ash_quantize(const void* points, int32_t points_are_f64, int64_t n, double c
   if (n == 0) return ASH_OK;
   cudaStream_t s = as_stream(stream);
   if (points_are_f64)
-    k_quantize<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const double*>(points), n, cell, out_coords, flags);
+    k_quantize<double><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const double*>(points), n, cell, out_coords,
+                                                              flags);
   else
-    k_quantize<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const float*>(points), n, cell, out_coords, flags);
+    k_quantize<float><<<grid_for(n, kBlock), kBlock, 0, s>>>(static_cast<const float*>(points), n, cell, out_coords,
+                                                             flags);
+  note_launch();
   return check_launch("ash_quantize");
 }
 
@@ -2782,7 +2788,7 @@ int ash_frame_candidates(const double* depth, int64_t height, int64_t width, con
   int64_t n = 0;
   if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
   if (!out_coords || !out_valid || !flags) return fail(ASH_ERR_INVALID, "null output pointer");
-  k_frame_candidates<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(f, n, out_coords, out_valid, flags);
+  k_frame_candidates<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(f, n, out_coords, out_valid, flags); note_launch();
   return check_launch("ash_frame_candidates");
 }
 

@@ -17,6 +17,7 @@
 #include <stdio.h>
 
 #include "../../include/ash.h"
+#include "launch_count.h"
 
 namespace {
 
@@ -257,7 +258,7 @@ int ash_route_owner(const int32_t* keys, int64_t n, int32_t arity, int32_t world
   if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
   if (n == 0) return ASH_OK;
   k_owner_of<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(keys, n, arity,
-                                                                                 static_cast<uint32_t>(world), out);
+                                                                                 static_cast<uint32_t>(world), out); note_launch();
   return rcheck("ash_route_owner");
 }
 
@@ -279,11 +280,11 @@ int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t w
   const int64_t n_tiles = (n + kTile - 1) / kTile;
   if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
   const uint32_t w = static_cast<uint32_t>(world);
-  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, owners, scratch, n_tiles);
-  k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts);
+  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, owners, scratch, n_tiles); note_launch();
+  k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts); note_launch();
   k_route_scatter<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(
       keys, n, arity, w, owners, scratch, n_tiles, perm, keys_out, static_cast<const uint8_t*>(payload),
-      payload_row_bytes, static_cast<uint8_t*>(payload_out));
+      payload_row_bytes, static_cast<uint8_t*>(payload_out)); note_launch();
   return rcheck("ash_route_partition");
 }
 
@@ -291,7 +292,7 @@ int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_
   if (n < 0 || row_bytes < 0) return rfail("bad gather arguments");
   if (n == 0 || row_bytes == 0) return ASH_OK;
   k_gather_rows<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst));
+      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst)); note_launch();
   return rcheck("ash_gather_rows");
 }
 
@@ -300,11 +301,11 @@ int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row
   if (n == 0 || row_bytes == 0) return ASH_OK;
   if (row_bytes == 4 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3) == 0) {
     k_scatter_words<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint32_t*>(src), idx, n, static_cast<uint32_t*>(dst));
+        static_cast<const uint32_t*>(src), idx, n, static_cast<uint32_t*>(dst)); note_launch();
     return rcheck("ash_scatter_rows");
   }
   k_scatter_rows<<<blocks(n, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst));
+      static_cast<const uint8_t*>(src), idx, n, row_bytes, static_cast<uint8_t*>(dst)); note_launch();
   return rcheck("ash_scatter_rows");
 }
 
