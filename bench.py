@@ -63,6 +63,17 @@ def _profiled_traffic(kernel: str):
     return None, None
 
 
+def _random_access(kms):
+    files = sorted((ROOT / "profiles").glob("*_random_access.json"))
+    if not files:
+        return None
+    ra = json.loads(files[-1].read_text())
+    ceil = ra["probe_32B_gps"]
+    find_gps = N_KEYS / (kms["find"] / 1e3) / 1e9
+    return {"probe_ceiling_gps": ceil, "source": files[-1].name,
+            "find_gprobes_per_s": round(find_gps, 1), "find_frac_of_ceiling": round(find_gps / ceil, 3)}
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -570,6 +581,9 @@ def main():
             "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS /
                                  ((kms["claim"] + kms["tile_scan"] + kms["commit"]) / 1e3) / 1e9 / bw, 4),
             "find_frac": round(per_kernel_bytes["find"] / (kms["find"] / 1e3) / 1e9 / bw, 4)},
+        # the bound that actually binds a random probe: DRAM bandwidth at the
+        # ~85 B the memory system moves per 32-byte probe (profiles/*_random_access.json)
+        "random_access": _random_access(kms),
         "e2e": {"value": round(2 * N_KEYS / (res["e2e_ms"] / 1e3) / 1e6, 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
         "gpu_launches": res["launches"],  # libash kernels in the timed region (ash_launch_count)
