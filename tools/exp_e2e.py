@@ -43,3 +43,36 @@ for chunk in [int(c) for c in (sys.argv[1:] or ["2097152", "1048576", "524288", 
     ms = 1e3 * sum(ts) / len(ts)
     print(f"chunk={chunk}: step {ms:.3f} ms  insert {1e3*sum(ti)/len(ti):.3f}  find {1e3*sum(tf)/len(tf):.3f}"
           f"  e2e {2*N/ms/1e3:.1f} Mops/s")
+
+# floor: the same chunked copies with no kernels (H2D keys+vals, D2H idx+mask)
+def copies_only(with_vals):
+    c = 1 << 20
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    kd = torch.empty((N, 3), dtype=torch.int32, device=dev)
+    vd = torch.empty((N, 1), dtype=torch.float32, device=dev)
+    ih = torch.empty(N, dtype=torch.int32, pin_memory=True)
+    mh = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+    idd = torch.zeros(N, dtype=torch.int32, device=dev)
+    md = torch.zeros(N, dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream()
+    for a in range(0, N, c):
+        b = min(N, a + c)
+        with torch.cuda.stream(h2d):
+            kd[a:b].copy_(keys_h[a:b], non_blocking=True)
+            if with_vals:
+                vd[a:b].copy_(vals_h[a:b], non_blocking=True)
+        d2h.wait_stream(h2d)
+        with torch.cuda.stream(d2h):
+            ih[a:b].copy_(idd[a:b], non_blocking=True)
+            mh[a:b].copy_(md[a:b], non_blocking=True)
+    d2h.synchronize()
+
+for _ in range(3):
+    copies_only(True); copies_only(False)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5):
+    copies_only(True)
+    copies_only(False)
+torch.cuda.synchronize()
+print(f"copies only (insert-like + find-like): {(time.perf_counter() - t0) / 5 * 1e3:.3f} ms per step")
