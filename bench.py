@@ -14,7 +14,7 @@ Arms:
   --impl reference   the reference algorithm on the host CPU (the numpy
                      oracle port, oracle/ash_oracle.py, since the reference is
                      pure Python and cannot travel to the GPU box).
-Multi-GPU (torchrun, N>1): hash-partitioned map, NCCL all-to-all routing,
+Multi-GPU (torchrun, N>1): hash-partitioned map, peer-memory routing (NCCL all-to-all with --transport nccl),
 10M insert + 10M find keys per rank per step (weak scaling).
 """
 from __future__ import annotations
@@ -526,6 +526,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true",
                     help="force the hash-partitioned (torch.distributed) path even at N=1")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="partitioned routing: peer-memory put/pull (symmetric memory) or NCCL all-to-all")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
     args = ap.parse_args()

@@ -276,6 +276,25 @@ int ash_insert_commit_delegate(ash_map_t* m, const int32_t* keys, int64_t n,
  * index_heap.py:38-47), W / top_base from the device counters. */
 int ash_heap_put_losers(ash_map_t* m, const int32_t* sorted_losers, int64_t n, void* stream);
 
+/* Peer-memory dispatch / combine for the hash-partitioned map (no NCCL
+ * payload collective).  ash_route_count: owners + per-owner counts (device
+ * int64[world]) with the tile offsets in scratch.  ash_route_put: the stable
+ * owner partition stores every key row (and payload row) directly into owner
+ * o's receive buffers peer_keys[o] / peer_payload[o] (symmetric allocations
+ * mapped on this rank; host arrays of world device pointers) at row
+ * row_off[o] + j, j = index within this rank's owner-o segment (-> jdx).
+ * ash_route_pull: out[p] = peer_ret[owner(p)][row_off[owner(p)] + jdx[p]].
+ * The caller orders put -> (peer barrier) -> shard op -> (peer barrier) -> pull. */
+int ash_route_count(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int64_t* counts,
+                    uint8_t* owners, int32_t* scratch, int64_t scratch_len, void* stream);
+int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, const uint8_t* owners,
+                  const int32_t* scratch, int64_t scratch_len, const int64_t* row_off,
+                  void* const* peer_keys, const void* payload, int64_t payload_row_bytes,
+                  void* const* peer_payload, int32_t* jdx, void* stream);
+int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world,
+                   const int64_t* row_off, const void* const* peer_ret, int32_t* out,
+                   uint8_t* out_mask /* optional: out >= 0 */, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

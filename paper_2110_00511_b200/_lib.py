@@ -78,10 +78,17 @@ _SIGNATURES = {
     "ash_route_partition": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                       c_void_p, c_int64, c_void_p]),
+    "ash_route_count": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_int64,
+                                  c_void_p]),
+    "ash_route_put": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p,
+                                c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ash_route_pull": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
     "ash_gather_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ash_scatter_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
 }
-_ROUTE_FUNCS = ("ash_route_owner", "ash_route_partition", "ash_gather_rows", "ash_scatter_rows")
+_ROUTE_FUNCS = ("ash_route_owner", "ash_route_partition", "ash_gather_rows", "ash_scatter_rows",
+                "ash_route_count", "ash_route_put", "ash_route_pull")
 
 EXPORTED = tuple(_SIGNATURES)
 

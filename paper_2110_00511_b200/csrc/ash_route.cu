@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "../../include/ash.h"
 #include "launch_count.h"
@@ -51,11 +52,21 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
   return x;
 }
 
-__device__ __forceinline__ uint32_t owner_of(const int32_t* row, int arity, uint32_t world) {
+// row: global key row (read-only path) or registers
+template <typename Row>
+__device__ __forceinline__ uint32_t owner_of(const Row& row, int arity, uint32_t world) {
   uint64_t x = 0x243F6A8885A308D3ull ^ static_cast<uint64_t>(arity);
   for (int d = 0; d < arity; ++d)
-    x = fmix64(x ^ (static_cast<uint64_t>(static_cast<uint32_t>(__ldg(row + d))) + 0x9E3779B97F4A7C15ull * (d + 1)));
+    x = fmix64(x ^ (static_cast<uint64_t>(static_cast<uint32_t>(row[d])) + 0x9E3779B97F4A7C15ull * (d + 1)));
   return static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * world) >> 32);
+}
+
+__device__ __forceinline__ uint32_t owner_of(const int32_t* row, int arity, uint32_t world) {
+  struct Ldg {
+    const int32_t* r;
+    __device__ int32_t operator[](int d) const { return __ldg(r + d); }
+  };
+  return owner_of(Ldg{row}, arity, world);
 }
 
 // pass 1: owner of every key (uint8) and per-tile, per-owner counts ->
@@ -70,10 +81,25 @@ __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restric
   // every item's owner first (all key loads of the tile in flight), then the
   // warp-aggregated shared-memory counts
   uint32_t own[kItems];
+  if (arity == 3) {  // int3 keys: all 24 key words of the thread in flight first
+    int32_t kw[kItems][3];
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int64_t p = base + it * kBlock + threadIdx.x;
-    own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) kw[it][d] = p < n ? __ldg(keys + p * 3 + d) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      own[it] = p < n ? owner_of(kw[it], 3, world) : 0xFFFFFFFFu;
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+    }
   }
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
@@ -213,6 +239,139 @@ __global__ void __launch_bounds__(kBlock) k_route_scatter(const int32_t* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Peer-memory dispatch / combine (the all-to-all fused into the partition).
+//
+// Every rank's receive buffers are symmetric allocations (torch symmetric
+// memory: each rank maps every peer's buffer over NVLink).  The owner's
+// receive buffer holds its sources' segments in source-rank order, so the
+// shard sees its keys in global batch order (first-occurrence exactness).
+// k_route_put computes the stable owner partition exactly like
+// k_route_scatter and stores each key row (+ payload row) straight into the
+// owner's buffer at row_off[owner] + j, j = the position's index within its
+// owner segment (kept in jdx for the combine).  k_route_pull reads each
+// position's result back from its owner's result buffer.  No staging copy,
+// no NCCL payload collective: the only collective is the N x N count exchange.
+
+struct PeerArgs {
+  int64_t row_off[kMaxWorld];     // this rank's first row in owner o's receive buffers
+  int32_t* keys[kMaxWorld];       // owner o's receive key rows
+  uint8_t* pay[kMaxWorld];        // owner o's receive payload rows (or null)
+  const int32_t* ret[kMaxWorld];  // owner o's result buffer
+};
+
+__global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict__ keys, int64_t n, int arity,
+                                                      uint32_t world, const uint8_t* __restrict__ owners,
+                                                      const int32_t* __restrict__ off, int64_t n_tiles,
+                                                      const uint8_t* __restrict__ pay, int64_t pay_rb, PeerArgs pa,
+                                                      int32_t* __restrict__ jdx) {
+  constexpr int kW = kBlock / 32;
+  __shared__ int32_t s_pre[kItems][kW][kMaxWorld];
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < kItems * kW * kMaxWorld; e += kBlock) (&s_pre[0][0][0])[e] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t own[kItems], rank_in_warp[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    own[it] = p < n ? owners[p] : 0xFFFFFFFFu;
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, own[it]);
+    rank_in_warp[it] = __popc(same & lt);
+    if (p < n && (same & lt) == 0) s_pre[it][warp][own[it]] = __popc(same);
+  }
+  __syncthreads();
+  // index within the owner's segment: global owner-major offset minus the
+  // segment start off[o * n_tiles]
+  for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
+    int32_t run = off[o * n_tiles + blockIdx.x] - off[o * n_tiles];
+    for (int it = 0; it < kItems; ++it)
+      for (int w = 0; w < kW; ++w) {
+        const int32_t c = s_pre[it][w][o];
+        s_pre[it][w][o] = run;
+        run += c;
+      }
+  }
+  __syncthreads();
+  if (arity == 3 && (pay_rb == 0 || (pay_rb == 4 && (reinterpret_cast<uintptr_t>(pay) & 3) == 0))) {
+    // int3 keys + at most one 4-byte value: every load first, then the
+    // (peer) stores
+    uint32_t kw[kItems][3], pw[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      if (p >= n) continue;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) kw[it][d] = static_cast<uint32_t>(__ldg(keys + p * 3 + d));
+      if (pay_rb) pw[it] = __ldg(reinterpret_cast<const uint32_t*>(pay) + p);
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      if (p >= n) continue;
+      const uint32_t o = own[it];
+      const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
+      const int64_t row = pa.row_off[o] + j;
+      jdx[p] = j;
+      int32_t* kd = pa.keys[o] + row * 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) kd[d] = static_cast<int32_t>(kw[it][d]);
+      if (pay_rb) reinterpret_cast<uint32_t*>(pa.pay[o])[row] = pw[it];
+    }
+    return;
+  }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t p = base + it * kBlock + threadIdx.x;
+    if (p >= n) continue;
+    const uint32_t o = own[it];
+    const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
+    const int64_t row = pa.row_off[o] + j;
+    jdx[p] = j;
+    int32_t* kd = pa.keys[o] + row * arity;
+    for (int d = 0; d < arity; ++d) kd[d] = __ldg(keys + p * arity + d);
+    if (pay_rb) copy_row_words(pa.pay[o] + row * pay_rb, pay + p * pay_rb, pay_rb);
+  }
+}
+
+// out[p] = the owner's result; out_mask[p] = (out[p] >= 0) when given (the
+// partitioned result's mask, so no separate compare pass)
+// 4 positions per thread (vector loads of owners / jdx, vector stores); the
+// per-owner base pointers are staged in shared memory
+__global__ void __launch_bounds__(kBlock) k_route_pull(const uint8_t* __restrict__ owners,
+                                                       const int32_t* __restrict__ jdx, int64_t n, PeerArgs pa,
+                                                       uint32_t world, int32_t* __restrict__ out,
+                                                       uint8_t* __restrict__ out_mask) {
+  __shared__ const int32_t* s_base[kMaxWorld];
+  for (uint32_t o = threadIdx.x; o < world; o += kBlock) s_base[o] = pa.ret[o] + pa.row_off[o];
+  __syncthreads();
+  const int64_t p0 = (blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x) * 4;
+  if (p0 >= n) return;
+  const bool vec = p0 + 4 <= n && ((reinterpret_cast<uintptr_t>(owners) | reinterpret_cast<uintptr_t>(jdx) |
+                                    reinterpret_cast<uintptr_t>(out) |
+                                    reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0 && (p0 & 3) == 0;
+  if (vec) {
+    const uint32_t ow = *reinterpret_cast<const uint32_t*>(owners + p0);
+    const int4 j = *reinterpret_cast<const int4*>(jdx + p0);
+    const int32_t jj[4] = {j.x, j.y, j.z, j.w};
+    int32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = s_base[(ow >> (8 * i)) & 0xFF][jj[i]];
+    *reinterpret_cast<int4*>(out + p0) = make_int4(v[0], v[1], v[2], v[3]);
+    if (out_mask)
+      *reinterpret_cast<uint32_t*>(out_mask + p0) =
+          (v[0] >= 0) | ((v[1] >= 0) << 8) | ((v[2] >= 0) << 16) | ((v[3] >= 0) << 24);
+    return;
+  }
+  for (int64_t p = p0; p < n && p < p0 + 4; ++p) {
+    const int32_t v = s_base[owners[p]][jdx[p]];
+    out[p] = v;
+    if (out_mask) out_mask[p] = v >= 0;
+  }
+}
+
 // dst[i] = src[idx[i]] (gather) / dst[idx[i]] = src[i] (scatter): thread per row
 __global__ void k_gather_rows(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                               int64_t rb, uint8_t* __restrict__ dst) {
@@ -286,6 +445,67 @@ int ash_route_partition(const int32_t* keys, int64_t n, int32_t arity, int32_t w
       keys, n, arity, w, owners, scratch, n_tiles, perm, keys_out, static_cast<const uint8_t*>(payload),
       payload_row_bytes, static_cast<uint8_t*>(payload_out)); note_launch();
   return rcheck("ash_route_partition");
+}
+
+int ash_route_count(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int64_t* counts, uint8_t* owners,
+                    int32_t* scratch, int64_t scratch_len, void* stream) {
+  if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
+  if (n >= (int64_t(1) << 31)) return rfail("routing batch too long");
+  if (!counts) return rfail("null routing output");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n == 0) {
+    cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, s);
+    return rcheck("ash_route_count");
+  }
+  if (!keys || !owners || !scratch) return rfail("null routing buffer");
+  const int64_t n_tiles = (n + kTile - 1) / kTile;
+  if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
+  const uint32_t w = static_cast<uint32_t>(world);
+  k_route_count<<<static_cast<unsigned>(n_tiles), kBlock, 0, s>>>(keys, n, arity, w, owners, scratch, n_tiles); note_launch();
+  k_route_scan<<<1, 1024, 0, s>>>(scratch, n_tiles * world, n_tiles, w, counts); note_launch();
+  return rcheck("ash_route_count");
+}
+
+int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, const uint8_t* owners,
+                  const int32_t* scratch, int64_t scratch_len, const int64_t* row_off, void* const* peer_keys,
+                  const void* payload, int64_t payload_row_bytes, void* const* peer_payload, int32_t* jdx,
+                  void* stream) {
+  if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
+  if (n == 0) return ASH_OK;
+  if (!keys || !owners || !scratch || !row_off || !peer_keys || !jdx) return rfail("null routing buffer");
+  if (payload_row_bytes < 0 || (payload_row_bytes && (!payload || !peer_payload)))
+    return rfail("payload and peer payload buffers must both be given");
+  const int64_t n_tiles = (n + kTile - 1) / kTile;
+  if (scratch_len < n_tiles * world) return rfail("routing scratch too small");
+  PeerArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  for (int o = 0; o < world; ++o) {
+    if (!peer_keys[o]) return rfail("null peer key buffer");
+    pa.row_off[o] = row_off[o];
+    pa.keys[o] = static_cast<int32_t*>(peer_keys[o]);
+    pa.pay[o] = payload_row_bytes ? static_cast<uint8_t*>(peer_payload[o]) : nullptr;
+  }
+  k_route_put<<<static_cast<unsigned>(n_tiles), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      keys, n, arity, static_cast<uint32_t>(world), owners, scratch, n_tiles,
+      static_cast<const uint8_t*>(payload), payload_row_bytes, pa, jdx); note_launch();
+  return rcheck("ash_route_put");
+}
+
+int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world, const int64_t* row_off,
+                   const void* const* peer_ret, int32_t* out, uint8_t* out_mask, void* stream) {
+  if (n < 0 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
+  if (n == 0) return ASH_OK;
+  if (!owners || !jdx || !row_off || !peer_ret || !out) return rfail("null routing buffer");
+  PeerArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  for (int o = 0; o < world; ++o) {
+    if (!peer_ret[o]) return rfail("null peer result buffer");
+    pa.row_off[o] = row_off[o];
+    pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
+  }
+  k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask); note_launch();
+  return rcheck("ash_route_pull");
 }
 
 int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {

@@ -98,12 +98,148 @@ class CudaRouter:
         return out
 
 
+class PeerExchange:
+    """Dispatch / combine over NVLink peer memory (torch symmetric memory).
+
+    Each rank owns symmetric receive buffers (key rows, one payload buffer)
+    and a symmetric result buffer, every peer's copy mapped locally.  A batch
+    op is: owner count + N x N count exchange (the only collective, a few
+    bytes) -> ``ash_route_put`` stores each key (+ value) row straight into
+    its owner's receive buffer, segments in source-rank order -> peer barrier
+    -> the shard op on the received rows -> results into the symmetric result
+    buffer -> peer barrier -> ``ash_route_pull`` reads every position's result
+    from its owner -> peer barrier (buffers free for the next op).  Compared
+    with the NCCL transport this removes the send-buffer gather, both payload
+    all-to-alls and the un-permute pass."""
+
+    def __init__(self, group, world: int, rank: int, device: torch.device, arity: int,
+                 payload=None, capacity: int = 1 << 20, mapping: str = "symmetric"):
+        from . import _lib
+        self._lib = _lib
+        self.group = group if group is not None else dist.group.WORLD
+        self.group_name = self.group.group_name
+        if mapping not in ("symmetric", "ipc"):
+            raise ValueError("mapping must be 'symmetric' or 'ipc'")
+        # "symmetric": torch symmetric memory (NVLink peer mappings, device-side
+        # barriers) — the multi-GPU product path.  "ipc": CUDA IPC mappings of
+        # ordinary allocations with host barriers — lets ranks that share one
+        # GPU (tests) run the same put / pull kernels across processes.
+        self.mapping = mapping
+        if mapping == "symmetric":
+            import torch.distributed._symmetric_memory as symm
+            self._symm = symm
+        self.world, self.rank, self.device, self.arity = world, rank, device, arity
+        self.payload = payload  # (row shape, torch dtype) of the single value buffer, or None
+        self.pay_rb = 0
+        if payload is not None:
+            shape, dt = payload
+            self.pay_rb = int(np.prod(shape)) * torch.empty(0, dtype=dt).element_size()
+        self._scratch = torch.empty(0, dtype=torch.int32, device=device)
+        self.capacity = 0
+        self._alloc(capacity)
+
+    def _alloc(self, cap: int) -> None:
+        cap = max(int(cap), 1)
+        sizes = [(cap * self.arity, torch.int32), (cap, torch.int32)]
+        if self.pay_rb:
+            sizes.append((cap * self.pay_rb, torch.uint8))
+        if self.mapping == "symmetric":
+            symm = self._symm
+            bufs = [symm.empty(n, dtype=dt, device=self.device) for n, dt in sizes]
+            self._handles = [symm.rendezvous(b, self.group_name) for b in bufs]
+            ptrs = [list(h.buffer_ptrs) for h in self._handles]
+        else:
+            from torch.multiprocessing.reductions import reduce_tensor
+            bufs = [torch.empty(n, dtype=dt, device=self.device) for n, dt in sizes]
+            shared = [None] * self.world
+            dist.all_gather_object(shared, [reduce_tensor(b) for b in bufs], group=self.group)
+            self._peer_views = [[fn(*args) if r != self.rank else bufs[i]
+                                 for r, (fn, args) in ((r, shared[r][i]) for r in range(self.world))]
+                                for i in range(len(bufs))]
+            ptrs = [[t.data_ptr() for t in views] for views in self._peer_views]
+        self.recv_keys, self.ret = bufs[0], bufs[1]
+        self.recv_pay = bufs[2] if self.pay_rb else None
+        self.capacity = cap
+        c_void_p = self._lib.c_void_p
+        self._p_keys = (c_void_p * self.world)(*ptrs[0])
+        self._p_ret = (c_void_p * self.world)(*ptrs[1])
+        self._p_pay = (c_void_p * self.world)(*ptrs[2]) if self.pay_rb else None
+
+    def _barrier(self) -> None:
+        """All ranks' device work issued so far is complete and visible."""
+        if self.mapping == "symmetric":
+            self._handles[0].barrier(channel=0)  # stream-ordered device barrier
+        else:
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=self.group)
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def dispatch(self, keys: torch.Tensor, payload: torch.Tensor = None):
+        """Route keys (+ payload rows) to their owners.  Returns this rank's
+        shard batch (keys, payload views into the receive buffers) and the
+        context the combine needs."""
+        lib = self._lib
+        n = keys.shape[0]
+        need = int(lib.lib.ash_route_scratch_len(n, self.world))
+        if self._scratch.numel() < need:
+            self._scratch = torch.empty(max(need, 1), dtype=torch.int32, device=self.device)
+        counts = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        owners = torch.empty(n, dtype=torch.uint8, device=self.device)
+        lib.call("ash_route_count", keys.data_ptr(), n, self.arity, self.world, counts.data_ptr(),
+                 owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), self._stream())
+        if dist.get_backend(self.group) == "gloo":  # CPU control plane (tests: ranks sharing a GPU)
+            parts = [torch.empty(self.world, dtype=torch.int64) for _ in range(self.world)]
+            dist.all_gather(parts, counts.cpu(), group=self.group)
+            C = torch.stack(parts)
+        else:
+            mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
+            dist.all_gather_into_tensor(mat, counts, group=self.group)
+            C = mat.cpu()  # C[src][owner]; the one host read of the op
+        row_off = torch.cumsum(C, 0) - C  # rows of earlier sources at every owner
+        m = int(C[:, self.rank].sum())
+        peak = int(C.sum(0).max())
+        if peak > self.capacity:  # every rank sees the same C: grow together
+            self._alloc(int(peak * 1.25))
+        offs = (lib.ctypes.c_int64 * self.world)(*row_off[self.rank].tolist())
+        jdx = torch.empty(n, dtype=torch.int32, device=self.device)
+        rb = self.pay_rb if (payload is not None and n) else 0
+        if rb:
+            payload = payload.contiguous()
+        lib.call("ash_route_put", keys.data_ptr(), n, self.arity, self.world, owners.data_ptr(),
+                 self._scratch.data_ptr(), self._scratch.numel(), offs, self._p_keys,
+                 payload.data_ptr() if rb else None, rb, self._p_pay if rb else None,
+                 jdx.data_ptr(), self._stream())
+        self._barrier()  # every source's rows have landed
+        rkeys = self.recv_keys[:m * self.arity].view(m, self.arity)
+        rpay = None
+        if self.pay_rb and payload is not None:
+            shape, dt = self.payload
+            rpay = self.recv_pay[:m * self.pay_rb].view(dt).view(m, *shape)
+        return rkeys, rpay, (n, owners, jdx, offs)
+
+    def combine(self, local_idx: torch.Tensor, ctx) -> torch.Tensor:
+        n, owners, jdx, offs = ctx
+        m = local_idx.shape[0]
+        if m:
+            self.ret[:m].copy_(local_idx.reshape(-1))
+        self._barrier()  # every owner's results are in place
+        out = torch.empty(n, dtype=torch.int32, device=self.device)
+        msk = torch.empty(n, dtype=torch.uint8, device=self.device)
+        self._lib.call("ash_route_pull", owners.data_ptr(), jdx.data_ptr(), n, self.world, offs,
+                       self._p_ret, out.data_ptr(), msk.data_ptr(), self._stream())
+        self._barrier()  # all pulls done: buffers reusable
+        return out, msk.view(torch.bool)
+
+
 class PartitionedHashMap:
     """One shard per rank; batch ops are collective (every rank calls them
     with its own slice of the global batch, possibly empty)."""
 
     def __init__(self, capacity_per_rank: int, key_arity: int, value_specs=(), group=None,
-                 device=None, auto_rehash: bool = True, local_map=None, router=None):
+                 device=None, auto_rehash: bool = True, local_map=None, router=None,
+                 transport: str = "nccl", peer_mapping: str = "symmetric"):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -115,6 +251,17 @@ class PartitionedHashMap:
         self.local = local_map
         self.device = getattr(local_map, "device", torch.device("cpu"))
         self.router = router if router is not None else CudaRouter(self.world, self.device)
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport must be 'nccl' or 'peer'")
+        self.transport = transport
+        self.peer = None
+        if transport == "peer":
+            specs = getattr(local_map, "value_specs", ())
+            if len(specs) > 1:
+                raise ValueError("the peer transport carries at most one value buffer")
+            payload = (specs[0].shape, local_map._torch_dtypes[0]) if specs else None
+            self.peer = PeerExchange(group, self.world, self.rank, self.device, self.key_arity, payload,
+                                     capacity=max(int(capacity_per_rank), 1), mapping=peer_mapping)
 
     # -- routing ---------------------------------------------------------
 
@@ -162,27 +309,48 @@ class PartitionedHashMap:
 
     # -- operations --------------------------------------------------------
 
+    def _peer_op(self, op: str, keys, vals=()):
+        """One batch op over the peer transport (PeerExchange)."""
+        rkeys, rpay, ctx = self.peer.dispatch(keys, vals[0] if vals else None)
+        if op == "insert":
+            res = self.local.insert(rkeys, *([rpay] if rpay is not None else []))
+        elif op == "erase":
+            out, _ = self.peer.combine(torch.as_tensor(self.local.erase(rkeys)).to(torch.int32), ctx)
+            return out.to(torch.bool)
+        else:
+            res = getattr(self.local, op)(rkeys)
+        out, msk = self.peer.combine(torch.as_tensor(res.indices), ctx)
+        return PartitionedResult(out, msk, ctx[1])
+
     def insert(self, keys, *values) -> PartitionedResult:
         keys = self._keys(keys)
         vals = self._values(keys.shape[0], values)
+        if self.peer is not None:
+            return self._peer_op("insert", keys, vals)
         rkeys, rvals, ctx = self._forward(keys, vals)
         res = self.local.insert(rkeys, *rvals)  # the shard reshapes (n, -1) rows itself
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def activate(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
+        if self.peer is not None:
+            return self._peer_op("activate", keys)
         rkeys, _, ctx = self._forward(keys)
         res = self.local.activate(rkeys)
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def find(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
+        if self.peer is not None:
+            return self._peer_op("find", keys)
         rkeys, _, ctx = self._forward(keys)
         res = self.local.find(rkeys)
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
     def erase(self, keys) -> torch.Tensor:
         keys = self._keys(keys)
+        if self.peer is not None:
+            return self._peer_op("erase", keys)
         rkeys, _, ctx = self._forward(keys)
         m = torch.as_tensor(self.local.erase(rkeys)).to(torch.uint8)
         return self._backward(m, ctx).to(torch.bool)
@@ -205,6 +373,7 @@ def bench_main(args, rank: int, world: int) -> None:
     import json
     import os
     import statistics
+    import sys
 
     from .workloads import int3_batch
 
@@ -226,7 +395,15 @@ def bench_main(args, rank: int, world: int) -> None:
     vals = torch.rand((per_rank, 1), dtype=torch.float32, device=dev)
     # a shard receives ~per_rank keys per batch (hash-uniform owners): 5%
     # headroom keeps every insert on the no-sync path (batch <= free slots)
-    pm = PartitionedHashMap(int(per_rank * 1.05), 3, [np.float32], device=dev)
+    transport = getattr(args, "transport", "nccl")
+    try:
+        pm = PartitionedHashMap(int(per_rank * 1.05), 3, [np.float32], device=dev, transport=transport)
+    except Exception as exc:  # no symmetric memory on this node: NCCL all-to-all instead
+        if transport != "peer":
+            raise
+        print(f"peer transport unavailable ({exc!r}); using NCCL all-to-all", file=sys.stderr)
+        transport = "nccl"
+        pm = PartitionedHashMap(int(per_rank * 1.05), 3, [np.float32], device=dev, transport=transport)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -267,8 +444,9 @@ def bench_main(args, rank: int, world: int) -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": f"hash-partitioned map, {per_rank:,} insert + {per_rank:,} find "
-                                   f"int3 keys per rank per step (uniqueness {rho}), NCCL all-to-all "
-                                   f"routing; step time = max over ranks",
+                                   f"int3 keys per rank per step (uniqueness {rho}); step time = max over ranks",
+                       "routing": "peer-memory put/pull (symmetric memory)" if transport == "peer"
+                                  else "NCCL all-to-all",
                        "parallelism": f"hash-partitioned x{world}"},
             "gpu_launches": launches,  # libash kernels in the timed region (ash_launch_count)
         }), flush=True)

@@ -68,3 +68,87 @@ def test_partitioned_world1_nccl(cuda_ok):
         assert pm.size == om.size
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+@pytest.mark.parametrize("n", [0, 5000, 200_003])
+def test_peer_put_pull_kernels(cuda_ok, world, n):
+    """ash_route_put / ash_route_pull with `world` owner buffers on one GPU:
+    owner o's buffer holds this rank's owner-o keys and payload rows in batch
+    order at row_off[o]; the pull returns owner-buffer values per position."""
+    from paper_2110_00511_b200 import _lib
+    rng = np.random.default_rng(n + 7 * world)
+    k = rng.integers(-2 ** 31, 2 ** 31, size=(n, 3)).astype(np.int32)
+    pay = rng.integers(0, 2 ** 31, size=(n, 2)).astype(np.int32)
+    own = owner_of_np(k, world)
+    dev = torch.device("cuda")
+    kt, pt = torch.from_numpy(k).to(dev), torch.from_numpy(pay).to(dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    owners = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    scratch = torch.empty(max(int(_lib.lib.ash_route_scratch_len(n, world)), 1), dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("ash_route_count", kt.data_ptr(), n, 3, world, counts.data_ptr(), owners.data_ptr(),
+              scratch.data_ptr(), scratch.numel(), st)
+    cnt = np.bincount(own, minlength=world)
+    assert np.array_equal(counts.cpu().numpy(), cnt)
+    row_off = rng.integers(0, 100, size=world)
+    bufk = [torch.full((int(row_off[o] + cnt[o]) + 1, 3), -7, dtype=torch.int32, device=dev) for o in range(world)]
+    bufp = [torch.zeros((int(row_off[o] + cnt[o]) + 1, 2), dtype=torch.int32, device=dev) for o in range(world)]
+    P = _lib.c_void_p * world
+    offs = (_lib.ctypes.c_int64 * world)(*row_off.tolist())
+    jdx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _lib.call("ash_route_put", kt.data_ptr(), n, 3, world, owners.data_ptr(), scratch.data_ptr(), scratch.numel(),
+              offs, P(*[b.data_ptr() for b in bufk]), pt.data_ptr(), 8, P(*[b.data_ptr() for b in bufp]),
+              jdx.data_ptr(), st)
+    for o in range(world):
+        sel = own == o
+        got = bufk[o].cpu().numpy()
+        assert np.array_equal(got[row_off[o]:row_off[o] + cnt[o]], k[sel])
+        assert np.all(got[:row_off[o]] == -7)
+        assert np.array_equal(bufp[o].cpu().numpy()[row_off[o]:row_off[o] + cnt[o]], pay[sel])
+    ret = [torch.arange(b.shape[0], dtype=torch.int32, device=dev) * 10 + o for o, b in enumerate(bufk)]
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    msk = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    _lib.call("ash_route_pull", owners.data_ptr(), jdx.data_ptr(), n, world, offs,
+              P(*[r.data_ptr() for r in ret]), out.data_ptr(), msk.data_ptr(), st)
+    if n:
+        j = np.zeros(n, np.int64)
+        for o in range(world):
+            j[own == o] = np.arange(cnt[o])
+        expect = (row_off[own] + j) * 10 + own
+        assert np.array_equal(out[:n].cpu().numpy(), expect.astype(np.int32))
+        assert np.array_equal(msk[:n].cpu().numpy(), (expect >= 0).astype(np.uint8))
+
+
+def test_partitioned_world1_peer_transport(cuda_ok):
+    """The symmetric-memory transport end to end at world size 1 (the put /
+    barrier / pull path with this rank as its own peer)."""
+    import torch.distributed as dist
+    from oracle.ash_oracle import OracleMap
+    from paper_2110_00511_b200.partitioned import PartitionedHashMap
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(4)
+        pm = PartitionedHashMap(30_000, 3, [np.float32], device=torch.device("cuda", 0), transport="peer")
+        om = OracleMap(30_000, 3, [np.float32])
+        for step in range(3):
+            keys = rng.integers(-60, 60, size=(40_000, 3)).astype(np.int32)
+            vals = rng.random((40_000, 1), dtype=np.float32)
+            r, o = pm.insert(keys, vals), om.insert(keys, vals)
+            assert np.array_equal(r.indices.cpu().numpy(), o.indices)
+            assert np.array_equal(r.masks.cpu().numpy(), o.masks)
+            e, oe = pm.erase(keys[::5].copy()), om.erase(keys[::5].copy())
+            assert np.array_equal(e.cpu().numpy(), oe)
+            a, oa = pm.activate(keys[::-3].copy()), om.activate(keys[::-3].copy())
+            assert np.array_equal(a.indices.cpu().numpy(), oa.indices)
+            f, of = pm.find(keys[::-1].copy()), om.find(keys[::-1].copy())
+            assert np.array_equal(f.indices.cpu().numpy(), of.indices)
+        assert pm.size == om.size
+        assert pm.local.value_buffer(0).cpu().numpy().tobytes() == om.value_buffer(0).tobytes()
+    finally:
+        dist.destroy_process_group()
