@@ -528,6 +528,8 @@ def main():
                     help="force the hash-partitioned (torch.distributed) path even at N=1")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="partitioned routing: peer-memory put/pull (symmetric memory) or NCCL all-to-all")
+    ap.add_argument("--c5", action="store_true",
+                    help="configs[4]: the 400M-key partitioned map built by the mixed stream (strong scaling)")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
     args = ap.parse_args()
@@ -541,7 +543,7 @@ def main():
         return
 
     import torch
-    if world > 1 or args.partitioned:
+    if world > 1 or args.partitioned or args.c5:
         from paper_2110_00511_b200 import partitioned
         partitioned.bench_main(args, rank, world)
         return

@@ -369,14 +369,8 @@ class PartitionedHashMap:
 # ---------------------------------------------------------------------------
 # bench.py entry for N > 1 (torchrun; NCCL)
 
-def bench_main(args, rank: int, world: int) -> None:
-    import json
+def _bench_init():
     import os
-    import statistics
-    import sys
-
-    from .workloads import int3_batch
-
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -387,6 +381,90 @@ def bench_main(args, rank: int, world: int) -> None:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]),
                               RANK="0", WORLD_SIZE="1")
     dist.init_process_group("nccl", device_id=dev)
+    return dev
+
+
+def _make_pm(args, capacity: int, dev):
+    import sys
+    transport = getattr(args, "transport", "nccl")
+    try:
+        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport=transport), transport
+    except Exception as exc:  # no symmetric memory on this node: NCCL all-to-all instead
+        if transport != "peer":
+            raise
+        print(f"peer transport unavailable ({exc!r}); using NCCL all-to-all", file=sys.stderr)
+        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport="nccl"), "nccl"
+
+
+def bench_c5(args, rank: int, world: int) -> None:
+    """configs[4]: the 400M-key map built across the ranks by the mixed
+    stream — each step inserts 2^25 new keys and finds 2^25 keys (half
+    present), every rank holding a contiguous 1/N slice of both global
+    batches; total work fixed (strong scaling).  Step time = max over ranks."""
+    import json
+
+    from .workloads import c5_step_batches
+    dev = _bench_init()
+    total, batch = 400_000_000, 1 << 25
+    pm, transport = _make_pm(args, int(total / world * 1.05) + (1 << 20), dev)
+    stream = torch.cuda.current_stream(dev)
+    steps = -(-total // batch)
+    ms = 0.0
+    ops = 0
+    launches0 = None
+    for s in range(steps):
+        size = min(batch, total - s * batch)
+        ins, q = c5_step_batches(s * batch, size, total, device=dev)
+        lo, hi = size * rank // world, size * (rank + 1) // world
+        ins, q = ins[lo:hi].contiguous(), q[lo:hi].contiguous()
+        vals = torch.rand((hi - lo, 1), dtype=torch.float32, device=dev)
+        dist.barrier()
+        torch.cuda.synchronize()
+        if launches0 is None:
+            from . import _lib
+            launches0 = _lib.lib.ash_launch_count()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        pm.insert(ins, vals)
+        f = pm.find(q)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms += float(t.item())
+        ops += 2 * size
+        hits = torch.tensor([int(f.masks.sum())], dtype=torch.int64, device=dev)
+        dist.all_reduce(hits)
+        assert int(hits.item()) == size // 2, (s, int(hits.item()))
+    from . import _lib
+    launches = _lib.lib.ash_launch_count() - launches0
+    assert pm.size == total
+    if rank == 0:
+        print(json.dumps({
+            "metric": "insert & find Mops/s (int3 keys)", "value": round(ops / ms / 1e3, 2), "unit": "Mops/s",
+            "n_gpus": world, "steps": steps, "warmup": 0, "ms_per_step": round(ms / steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (counter-based keys generated on the device)",
+            "config": {"workload": "configs[4]: 400M-key hash-partitioned map built by the mixed stream "
+                                   "(12 steps of 2^25 inserts + 2^25 finds, half present); every rank holds "
+                                   "a contiguous 1/N slice of each global batch; time = max over ranks",
+                       "routing": "peer-memory put/pull (symmetric memory)" if transport == "peer"
+                                  else "NCCL all-to-all",
+                       "parallelism": f"hash-partitioned x{world}"},
+            "gpu_launches": launches,
+        }), flush=True)
+    dist.destroy_process_group()
+
+
+def bench_main(args, rank: int, world: int) -> None:
+    import json
+    import statistics
+
+    from .workloads import int3_batch
+
+    if getattr(args, "c5", False):
+        return bench_c5(args, rank, world)
+    dev = _bench_init()
     per_rank = 10_000_000
     rho = 0.5
     # this rank's contiguous slice of the global batch (counter-based keys:
@@ -395,15 +473,7 @@ def bench_main(args, rank: int, world: int) -> None:
     vals = torch.rand((per_rank, 1), dtype=torch.float32, device=dev)
     # a shard receives ~per_rank keys per batch (hash-uniform owners): 5%
     # headroom keeps every insert on the no-sync path (batch <= free slots)
-    transport = getattr(args, "transport", "nccl")
-    try:
-        pm = PartitionedHashMap(int(per_rank * 1.05), 3, [np.float32], device=dev, transport=transport)
-    except Exception as exc:  # no symmetric memory on this node: NCCL all-to-all instead
-        if transport != "peer":
-            raise
-        print(f"peer transport unavailable ({exc!r}); using NCCL all-to-all", file=sys.stderr)
-        transport = "nccl"
-        pm = PartitionedHashMap(int(per_rank * 1.05), 3, [np.float32], device=dev, transport=transport)
+    pm, transport = _make_pm(args, int(per_rank * 1.05), dev)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
