@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ASH_ABI_VERSION 3
+#define ASH_ABI_VERSION 4
 
 #define ASH_OK 0
 #define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
@@ -47,7 +47,7 @@ extern "C" {
 #define ASH_CTR_HEAP_DIRTY 7 /* heap[i] == i for every i >= this value     */
 #define ASH_N_COUNTERS 8
 
-#define ASH_FLAG_TABLE_FULL 1  /* a probe wrapped the whole table */
+#define ASH_FLAG_TABLE_FULL 1  /* a claim probe wrapped the table (or hit max_probe) */
 #define ASH_FLAG_RANGE 2       /* quantized coordinate outside int32 */
 
 /*
@@ -78,7 +78,8 @@ typedef struct ash_map {
                             /* keep the tile prefixes in [H, 2H]               */
   int64_t capacity;         /* <= 2^31 - 1                                     */
   uint32_t epoch;           /* scan epoch; the library bumps it per launch     */
-  uint32_t reserved;
+  uint32_t max_probe;       /* claim probe limit in buckets (0: whole table); */
+                            /* a claim that hits it sets ASH_FLAG_TABLE_FULL */
   int32_t* rank_words;      /* optional: 2 x ceil(n / 32) int32, lets the     */
   int64_t rank_words_len;   /* table-sweep commit rank winners without tmp    */
   void* bin_ws;             /* optional: >= ash_bin_ws_bytes(n, n_slots) bytes */
@@ -195,10 +196,14 @@ int ash_quantize(const void* points, int32_t points_are_f64, int64_t n,
                  double cell, int32_t* out_coords, int32_t* flags, void* stream);
 
 /* geometry.voxel_downsample (geometry.py:59-76), fused quantize + set insert
- * + first-occurrence select.  `ws` supplies an all-EMPTY workspace table
- * (slots, n_slots >= 2n), counters and scan status; the table is left EMPTY
- * again.  Writes count voxels to out_coords (count x 3) / out_sel (int64)
- * in ascending point order; count in ws->counters[COUNT].
+ * + first-occurrence select.  `ws` supplies an all-EMPTY workspace table,
+ * counters and scan status; the slots claimed are left EMPTY again.  Writes
+ * count voxels to out_coords (count x 3) / out_sel (int64) in ascending
+ * point order; count in ws->counters[COUNT].  The table must hold every
+ * distinct voxel: with n_slots >= 2n it always does; a smaller table (sized
+ * from an estimate, ws->max_probe bounding the probes) may overflow, which
+ * sets ASH_FLAG_TABLE_FULL: the results are then invalid, the table must be
+ * refilled with EMPTY and the call repeated with a larger one.
  * scratch_idx: n int32, scratch_mask: n bytes. */
 int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64,
                  int64_t n, double voxel, int32_t* out_coords, int64_t* out_sel,

@@ -31,7 +31,7 @@ class AshMap(ctypes.Structure):
         ("freed", c_void_p), ("counters", c_void_p), ("scan_status", c_void_p),
         ("scan_status_len", c_int64), ("tile_counts", c_void_p), ("tile_counts_len", c_int64),
         ("capacity", c_int64),
-        ("epoch", c_uint32), ("reserved", c_uint32),
+        ("epoch", c_uint32), ("max_probe", c_uint32),
         ("rank_words", c_void_p), ("rank_words_len", c_int64),
         ("bin_ws", c_void_p), ("bin_ws_bytes", c_int64),
     ]
@@ -103,7 +103,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ash_abi_version() != 3:
+    if lib.ash_abi_version() != 4:
         raise ImportError("libash.so ABI version mismatch; rebuild")
     return lib
 

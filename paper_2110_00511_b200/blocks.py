@@ -149,10 +149,10 @@ def frame_blocks(depth, intrinsics, pose, block_size: float, trunc: float,
         coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
         scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
-        call("ash_frame_blocks", ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c,
-             float(block_size), float(trunc), nb, coords.data_ptr(), scratch_idx.data_ptr(),
-             scratch_mask.data_ptr(), _stream_handle(dev))
-        count, flags = ws.counters[[_lib.CTR_COUNT, _lib.CTR_FLAGS]].tolist()
+        count, flags = ws.run(lambda: call(
+            "ash_frame_blocks", ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c, float(block_size),
+            float(trunc), nb, coords.data_ptr(), scratch_idx.data_ptr(), scratch_mask.data_ptr(),
+            _stream_handle(dev)))
     if flags & _lib.FLAG_RANGE:
         raise ValueError("block coordinates exceed int32 range")
     return coords[:count]

@@ -134,6 +134,23 @@ __device__ __forceinline__ uint32_t ld_stream(const void* p, uint64_t pol) {
   return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T ld_stream_t(const T* p, uint64_t pol);
+
+template <>
+__device__ __forceinline__ float ld_stream_t<float>(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+template <>
+__device__ __forceinline__ double ld_stream_t<double>(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ uint8_t ld_stream_u8(const void* p, uint64_t pol) {
   uint16_t v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
@@ -345,6 +362,7 @@ struct Table {
   uint32_t n_buckets;    // n_slots / 2 (bucket = 2 slots = one 32-byte sector)
   uint32_t n_slots;
   uint32_t hints;        // 1: streaming traffic marked L2 evict-first
+  uint32_t max_scan;     // claim probe limit in buckets (n_buckets, or ash_map_t.max_probe)
   const int32_t* key_buf;
   int arity;
 };
@@ -355,6 +373,7 @@ Table make_table(const ash_map_t* m) {
   t.n_buckets = static_cast<uint32_t>(m->n_slots / 2);
   t.n_slots = static_cast<uint32_t>(m->n_slots);
   t.hints = g_stream_hints;
+  t.max_scan = (m->max_probe > 0 && m->max_probe < t.n_buckets) ? m->max_probe : t.n_buckets;
   t.key_buf = m->key_buf;
   t.arity = m->arity;
   return t;
@@ -451,7 +470,7 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
     }
     first = 0;
     b = next_bucket(b, t.n_buckets);
-    if (++scanned >= t.n_buckets) {
+    if (++scanned >= t.max_scan) {
       if (free_slot != EMPTY) goto claim;
       atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_TABLE_FULL);
       mask[j] = DEMOTED;
@@ -2056,8 +2075,11 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
   const T* pts;
   double cell;
   __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
+    // the cloud streams through once: L2 evict-first keeps the (small) set
+    // of hot voxel slots resident
+    const uint64_t pol = stream_policy(1);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(pts[3 * p + d], cell, bad));
+    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(ld_stream_t<T>(pts + 3 * p + d, pol), cell, bad));
     return true;
   }
 };
@@ -2747,7 +2769,7 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
   if (int rc = check_batch(n)) return rc;
   if (!(voxel > 0)) return fail(ASH_ERR_INVALID, "voxel size must be > 0");
-  if (ws->n_slots < n + n / 4 + 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
@@ -2771,7 +2793,7 @@ int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t
   FrameSrc f;
   int64_t n = 0;
   if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
-  if (ws->n_slots < n + n / 4 + 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
   if (!out_coords || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null output pointer");
   cudaStream_t s = as_stream(stream);
