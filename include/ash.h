@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ASH_ABI_VERSION 4
+#define ASH_ABI_VERSION 5
 
 #define ASH_OK 0
 #define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
@@ -82,8 +82,6 @@ typedef struct ash_map {
                             /* a claim that hits it sets ASH_FLAG_TABLE_FULL */
   int32_t* rank_words;      /* optional: 2 x ceil(n / 32) int32, lets the     */
   int64_t rank_words_len;   /* table-sweep commit rank winners without tmp    */
-  void* bin_ws;             /* optional: >= ash_bin_ws_bytes(n, n_slots) bytes */
-  int64_t bin_ws_bytes;     /* enables the binned claim for dense batches      */
 } ash_map_t;
 
 int ash_abi_version(void);
@@ -110,14 +108,6 @@ int64_t ash_launch_count(void);
  *             stores; 0: never.  Defaults: 1, 5. */
 int ash_set_commit_mode(int32_t bulk, int32_t sweep_div);
 
-/* Workspace bytes the binned claim needs for a batch of n positions. */
-int64_t ash_bin_ws_bytes(int64_t n, int64_t n_slots);
-
-/* Insert claim strategy (process-wide; same results either way): batches
- * with n * bin_div >= n_slots (and arity <= 3, n >= 65536, a big enough
- * bin_ws) are binned by table region and claimed in shared memory;
- * 0 = always the plain per-position claim.  Default 2. */
-int ash_set_claim_mode(int32_t bin_div);
 
 /* Scan-status words needed for a single-pass scan over n items. */
 int64_t ash_scan_tiles(int64_t n);

@@ -33,7 +33,6 @@ class AshMap(ctypes.Structure):
         ("capacity", c_int64),
         ("epoch", c_uint32), ("max_probe", c_uint32),
         ("rank_words", c_void_p), ("rank_words_len", c_int64),
-        ("bin_ws", c_void_p), ("bin_ws_bytes", c_int64),
     ]
 
 
@@ -45,8 +44,6 @@ _SIGNATURES = {
     "ash_set_stream_hints": (c_int32, [c_int32]),
     "ash_launch_count": (c_int64, []),
     "ash_set_commit_mode": (c_int32, [c_int32, c_int32]),
-    "ash_set_claim_mode": (c_int32, [c_int32]),
-    "ash_bin_ws_bytes": (c_int64, [c_int64, c_int64]),
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -103,7 +100,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ash_abi_version() != 4:
+    if lib.ash_abi_version() != 5:
         raise ImportError("libash.so ABI version mismatch; rebuild")
     return lib
 
@@ -112,7 +109,6 @@ lib = _load()
 lib.ash_set_stream_hints(int(_os.environ.get("ASH_STREAM_HINTS", "1")))
 lib.ash_set_commit_mode(int(_os.environ.get("ASH_COMMIT_BULK", "1")),
                         int(_os.environ.get("ASH_SWEEP_DIV", "5")))
-lib.ash_set_claim_mode(int(_os.environ.get("ASH_BIN_DIV", "0")))
 
 
 class AshError(RuntimeError):

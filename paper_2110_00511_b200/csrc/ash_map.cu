@@ -729,489 +729,6 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Binned claim (insert / activate phase 1 for dense batches).
-//
-// The plain claim makes every position a random 32-byte probe plus, for new
-// keys, a random 128-bit CAS: ~20 M random L2 misses for a 10M batch, bound
-// by the random-access rate.  When the batch is dense relative to
-// the table (n >= n_slots / kBinDensity), the positions are first binned by
-// the table region of their home bucket (regions of kRegionBuckets buckets,
-// 64 KB of slots): two streaming passes (count, scatter of {key, pos}
-// records).  One CTA per region then loads the region's slots into shared
-// memory, claims / finds / joins every record with shared-memory atomics,
-// writes the dirty buckets back and the per-position results (same scratch
-// encoding as k_claim).  The table layout is unchanged (global linear
-// probing): a record whose probe would run past the region's last bucket
-// "spills" and is claimed afterwards on the global table by k_claim_spill,
-// together with every record of an oversized (heavily duplicated) region.
-// All records of one key share a home bucket, so they resolve in the same
-// place, and the lowest position still wins (atomicMin on the pending state).
-
-constexpr int kRegionBuckets = 1024;
-constexpr int kRegionSlots = 2 * kRegionBuckets;
-constexpr int kRegionMaxRecords = 1 << 16;  // beyond: the region's records spill
-constexpr int kMaxRegions = 8192;           // 18-bit packing, 32 KB shared histogram
-constexpr int kBinThreads = 512;
-constexpr int kBinItems = 16;
-constexpr int kRegionThreads = 256;
-constexpr int kRegionItems = 8;  // records cached in registers per thread (fast path)
-
-template <int A>
-__device__ __forceinline__ uint32_t region_of_key(const Key<A>& k, uint32_t n_buckets, uint32_t* home) {
-  *home = home_bucket(hash_key<A>(k, A), n_buckets);
-  return *home / kRegionBuckets;
-}
-
-template <int A>
-__global__ void __launch_bounds__(kBinThreads) k_bin_count(const int32_t* __restrict__ keys, int64_t n,
-                                                           uint32_t n_buckets, int n_regions,
-                                                           int32_t* __restrict__ region_cnt) {
-  extern __shared__ int32_t s_hist[];
-  for (int i = threadIdx.x; i < n_regions; i += kBinThreads) s_hist[i] = 0;
-  __syncthreads();
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kBinThreads * kBinItems);
-  constexpr int kHalf = kBinItems / 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    Key<A> k[kHalf];
-#pragma unroll
-    for (int it = 0; it < kHalf; ++it) {  // all loads of the half first
-      const int64_t p = base + (h * kHalf + it) * kBinThreads + threadIdx.x;
-      if (p < n) k[it] = load_key<A>(keys, p, A);
-    }
-#pragma unroll
-    for (int it = 0; it < kHalf; ++it) {
-      const int64_t p = base + (h * kHalf + it) * kBinThreads + threadIdx.x;
-      if (p < n) {
-        uint32_t home;
-        atomicAdd(&s_hist[region_of_key<A>(k[it], n_buckets, &home)], 1);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n_regions; i += kBinThreads)
-    if (s_hist[i]) atomicAdd(&region_cnt[i], s_hist[i]);
-}
-
-// exclusive prefix of n counts (one block); out[n] = total; cursor = copy
-__global__ void __launch_bounds__(1024) k_excl_scan(const int32_t* __restrict__ cnt, int n, int32_t* __restrict__ out,
-                                                    int32_t* __restrict__ cursor) {
-  __shared__ int32_t warp_tot[32];
-  __shared__ int32_t carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int32_t x = i < n ? cnt[i] : 0;
-    int32_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const int32_t w = warp_tot[lane];
-      int32_t wi = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-        if (lane >= o) wi += y;
-      }
-      warp_tot[lane] = wi - w;
-    }
-    __syncthreads();
-    const int32_t c = carry;
-    if (i < n) out[i] = cursor[i] = c + warp_tot[warp] + incl - x;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = c + warp_tot[warp] + incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[n] = carry;
-}
-
-constexpr int kScatterThreads = 1024;
-constexpr int kScatterItems = 16;
-
-template <int A>
-__global__ void __launch_bounds__(kScatterThreads) k_bin_scatter(const int32_t* __restrict__ keys, int64_t n,
-                                                                 uint32_t n_buckets, int n_regions,
-                                                                 int32_t* __restrict__ cursor,
-                                                                 uint4* __restrict__ bins) {
-  // 16K positions per block, so each region's cursor is reserved once per
-  // block for a run of ~n / (blocks x regions) records; (region, rank in
-  // block) packed in one register per item, key words re-read (L2-hot) for
-  // the record writes
-  extern __shared__ int32_t s_hist[];
-  for (int i = threadIdx.x; i < n_regions; i += kScatterThreads) s_hist[i] = 0;
-  __syncthreads();
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kScatterThreads * kScatterItems);
-  uint32_t packed[kScatterItems];
-  constexpr int kHalf = kScatterItems / 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    Key<A> k[kHalf];
-#pragma unroll
-    for (int it = 0; it < kHalf; ++it) {
-      const int64_t p = base + (h * kHalf + it) * kScatterThreads + threadIdx.x;
-      if (p < n) k[it] = load_key<A>(keys, p, A);
-    }
-#pragma unroll
-    for (int it = 0; it < kHalf; ++it) {
-      const int64_t p = base + (h * kHalf + it) * kScatterThreads + threadIdx.x;
-      if (p < n) {
-        uint32_t home;
-        const uint32_t r = region_of_key<A>(k[it], n_buckets, &home);
-        packed[h * kHalf + it] = (r << 18) | static_cast<uint32_t>(atomicAdd(&s_hist[r], 1));
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n_regions; i += kScatterThreads)
-    if (s_hist[i]) s_hist[i] = atomicAdd(&cursor[i], s_hist[i]);
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < kScatterItems; ++it) {
-    const int64_t p = base + it * kScatterThreads + threadIdx.x;
-    if (p < n) {
-      const Key<A> k = load_key<A>(keys, p, A);
-      const uint32_t r = packed[it] >> 18, lr = packed[it] & 0x3FFFFu;
-      bins[s_hist[r] + lr] = make_uint4(k.w[0], k.w[1], k.w[2], static_cast<uint32_t>(p));
-    }
-  }
-}
-
-enum { kRegFound = 0, kRegClaimed = 1, kRegJoined = 2, kRegSpill = 3 };
-
-// Pass 2 (read-only, after every claim of the region): where did pos end up?
-template <int A>
-__device__ __forceinline__ int region_lookup(const uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3],
-                                             uint32_t* slot, uint32_t* state) {
-  for (uint32_t sl = 2 * lb; sl < 2 * nb; ++sl) {
-    const uint4 v = s[sl];
-    if (v.w == EMPTY) return kRegSpill;  // cannot happen: pass 1 would have claimed it
-    if (v.w == TOMB) continue;
-    if (v.x == w[0] && (A < 2 || v.y == w[1]) && (A < 3 || v.z == w[2])) {
-      *slot = sl;
-      *state = v.w;
-      return v.w < PEND ? kRegFound : kRegJoined;
-    }
-  }
-  return kRegSpill;
-}
-
-__device__ __forceinline__ uint4 lds128_volatile(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "r"(smem_u32(p))
-               : "memory");
-  return r;
-}
-
-// 128-bit CAS on a shared-memory slot; returns the previous contents
-__device__ __forceinline__ uint4 cas128_shared(uint4* addr, uint4 cmp, uint4 val) {
-  unsigned long long clo = ((unsigned long long)cmp.y << 32) | cmp.x;
-  unsigned long long chi = ((unsigned long long)cmp.w << 32) | cmp.z;
-  unsigned long long vlo = ((unsigned long long)val.y << 32) | val.x;
-  unsigned long long vhi = ((unsigned long long)val.w << 32) | val.z;
-  unsigned long long olo, ohi;
-  asm volatile(
-      "{\n\t.reg .b128 c, v, o;\n\t"
-      "mov.b128 c, {%2, %3};\n\t"
-      "mov.b128 v, {%4, %5};\n\t"
-      "atom.shared::cta.cas.b128 o, [%6], c, v;\n\t"
-      "mov.b128 {%0, %1}, o;\n\t}"
-      : "=l"(olo), "=l"(ohi)
-      : "l"(clo), "l"(chi), "l"(vlo), "l"(vhi), "r"(smem_u32(addr))
-      : "memory");
-  return make_uint4(static_cast<uint32_t>(olo), static_cast<uint32_t>(olo >> 32), static_cast<uint32_t>(ohi),
-                    static_cast<uint32_t>(ohi >> 32));
-}
-
-// Pass 1 of a record inside its region (shared-memory slots s, nb local
-// buckets): the global claim protocol on shared memory — a 128-bit CAS takes
-// an EMPTY (or the first TOMB) slot with {key, PEND|pos} in one step, a
-// pending match joins with atomicMin.  Returns where the record landed:
-// bit 31 found (low bits = buffer index), bit 30 spill, else the local slot.
-constexpr uint32_t kOutFound = 0x80000000u, kOutSpill = 0x40000000u;
-
-template <int A>
-__device__ __forceinline__ uint32_t region_claim_out(uint4* s, uint32_t nb, uint32_t lb, const uint32_t (&w)[3],
-                                                     uint32_t pos, uint32_t* dirty, int* tombs) {
-  const uint32_t me = PEND | pos;
-  int free_slot = -1;
-  uint4 free_val = make_uint4(0, 0, 0, 0);
-  uint32_t sl = 2 * lb;
-  while (sl < 2 * nb) {
-    const uint4 v = lds128_volatile(&s[sl]);
-    if (v.w == EMPTY) {
-      const bool use_tomb = free_slot >= 0;
-      const uint32_t target = use_tomb ? static_cast<uint32_t>(free_slot) : sl;
-      const uint4 expect = use_tomb ? free_val : v;
-      const uint4 old = cas128_shared(&s[target], expect, make_uint4(w[0], w[1], w[2], me));
-      if (old.x == expect.x && old.y == expect.y && old.z == expect.z && old.w == expect.w) {
-        atomicOr(&dirty[target >> 6], 1u << ((target >> 1) & 31));
-        if (use_tomb) ++*tombs;
-        return target;
-      }
-      if (use_tomb) {  // the tombstone went to another key (maybe ours): rescan from it
-        sl = target;
-        free_slot = -1;
-      }
-      continue;  // re-read the slot
-    }
-    if (v.w == TOMB) {
-      if (free_slot < 0) {
-        free_slot = static_cast<int>(sl);
-        free_val = v;
-      }
-      ++sl;
-      continue;
-    }
-    if (v.x == w[0] && (A < 2 || v.y == w[1]) && (A < 3 || v.z == w[2])) {
-      if (v.w < PEND) return kOutFound | v.w;
-      if (v.w > me) atomicMin(&s[sl].w, me);
-      return sl;
-    }
-    ++sl;
-  }
-  return kOutSpill;
-}
-
-template <int A>
-__global__ void __launch_bounds__(kRegionThreads)
-    k_region_claim(Table t, const uint4* __restrict__ bins, const int32_t* __restrict__ region_off,
-                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, int32_t* counters,
-                   int32_t* __restrict__ spill, int32_t* spill_cnt) {
-  extern __shared__ __align__(128) uint4 s_slots[];
-  __shared__ uint32_t s_dirty[kRegionBuckets / 32];
-  __shared__ int s_tombs;
-  __shared__ int32_t s_base;
-  __shared__ __align__(8) uint64_t s_bar;
-  const int r = blockIdx.x;
-  const uint32_t b0 = static_cast<uint32_t>(r) * kRegionBuckets;
-  const uint32_t nb = min(static_cast<uint32_t>(kRegionBuckets), t.n_buckets - b0);
-  const int32_t lo = region_off[r], hi = region_off[r + 1];
-  const int32_t cnt = hi - lo;
-  const int lane = threadIdx.x & 31;
-  if (cnt == 0) return;
-  if (cnt > kRegionMaxRecords) {  // heavy duplication: the global claim handles it
-    if (threadIdx.x == 0) s_base = atomicAdd(spill_cnt, cnt);
-    __syncthreads();
-    for (int32_t i = threadIdx.x; i < cnt; i += kRegionThreads) {
-      const uint32_t pos = bins[lo + i].w;
-      spill[s_base + i] = static_cast<int32_t>(pos);
-      mask[pos] = 0;
-    }
-    return;
-  }
-  // the region's slots through the bulk-copy engine while the threads load
-  // their records
-  const uint32_t bytes = 2 * nb * 16;
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arrive_expect_tx(&s_bar, bytes);
-    bulk_g2s(s_slots, t.slots + 2 * static_cast<size_t>(b0), bytes, &s_bar, stream_policy(0));
-    s_tombs = 0;
-  }
-  for (int i = threadIdx.x; i < kRegionBuckets / 32; i += kRegionThreads) s_dirty[i] = 0;
-  const bool fast = cnt <= kRegionThreads * kRegionItems;
-  uint4 rec[kRegionItems];
-  if (fast) {
-#pragma unroll
-    for (int it = 0; it < kRegionItems; ++it) {
-      const int32_t i = lo + it * kRegionThreads + threadIdx.x;
-      if (i < hi) rec[it] = bins[i];
-    }
-  }
-  __syncthreads();
-  mbar_wait(&s_bar, 0);
-  int tombs = 0;
-  if (fast) {
-    uint32_t out[kRegionItems];
-#pragma unroll
-    for (int it = 0; it < kRegionItems; ++it) {
-      const int32_t i = lo + it * kRegionThreads + threadIdx.x;
-      if (i >= hi) continue;
-      const uint32_t w[3] = {rec[it].x, rec[it].y, rec[it].z};
-      Key<A> k;
-      k.row = nullptr;
-      k.w[0] = w[0], k.w[1] = w[1], k.w[2] = w[2];
-      const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
-      out[it] = region_claim_out<A>(s_slots, nb, lb, w, rec[it].w, s_dirty, &tombs);
-    }
-    if (tombs) atomicAdd(&s_tombs, tombs);
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < kRegionItems; ++it) {
-      const int32_t i0 = lo + it * kRegionThreads;
-      if (i0 >= hi) break;  // uniform
-      const int32_t i = i0 + threadIdx.x;
-      bool spilled = false;
-      uint32_t pos = 0;
-      if (i < hi) {
-        pos = rec[it].w;
-        const uint32_t o = out[it];
-        if (o & kOutFound) {
-          tmp[pos] = static_cast<int32_t>(o & ~kOutFound);
-          mask[pos] = 0;
-        } else if (o & kOutSpill) {
-          spilled = true;
-          mask[pos] = 0;
-        } else if (s_slots[o].w == (PEND | pos)) {
-          tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + o));
-          mask[pos] = 0;
-        } else {
-          tmp[pos] = static_cast<int32_t>(PEND);
-          mask[pos] = DEMOTED;
-        }
-      }
-      const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
-      if (sp) {
-        int32_t base = 0;
-        if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
-        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
-        if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
-      }
-    }
-  } else {
-    for (int32_t i = lo + threadIdx.x; i < hi; i += kRegionThreads) {
-      const uint4 rc = bins[i];
-      const uint32_t w[3] = {rc.x, rc.y, rc.z};
-      Key<A> k;
-      k.row = nullptr;
-      k.w[0] = rc.x, k.w[1] = rc.y, k.w[2] = rc.z;
-      const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
-      region_claim_out<A>(s_slots, nb, lb, w, rc.w, s_dirty, &tombs);
-    }
-    if (tombs) atomicAdd(&s_tombs, tombs);
-    __syncthreads();
-    for (int32_t i0 = lo; i0 < hi; i0 += kRegionThreads) {
-      const int32_t i = i0 + threadIdx.x;
-      bool spilled = false;
-      uint32_t pos = 0;
-      if (i < hi) {
-        const uint4 rc = bins[i];
-        pos = rc.w;
-        const uint32_t w[3] = {rc.x, rc.y, rc.z};
-        Key<A> k;
-        k.row = nullptr;
-        k.w[0] = rc.x, k.w[1] = rc.y, k.w[2] = rc.z;
-        const uint32_t lb = home_bucket(hash_key<A>(k, A), t.n_buckets) - b0;
-        uint32_t sl = 0, st = 0;
-        const int res = region_lookup<A>(s_slots, nb, lb, w, &sl, &st);
-        if (res == kRegFound) {
-          tmp[pos] = static_cast<int32_t>(st);
-          mask[pos] = 0;
-        } else if (res == kRegJoined && st == (PEND | pos)) {
-          tmp[pos] = static_cast<int32_t>(PEND | CLAIMER | (2 * b0 + sl));
-          mask[pos] = 0;
-        } else if (res == kRegJoined) {
-          tmp[pos] = static_cast<int32_t>(PEND);
-          mask[pos] = DEMOTED;
-        } else {
-          spilled = true;
-          mask[pos] = 0;
-        }
-      }
-      const unsigned sp = __ballot_sync(0xFFFFFFFFu, spilled);
-      if (sp) {
-        int32_t base = 0;
-        if (lane == __ffs(sp) - 1) base = atomicAdd(spill_cnt, __popc(sp));
-        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(sp) - 1);
-        if (spilled) spill[base + __popc(sp & lanemask_lt())] = static_cast<int32_t>(pos);
-      }
-    }
-  }
-  // dirty buckets back to the table (32 bytes each)
-  uint4* dst = t.slots + 2 * static_cast<size_t>(b0);
-  for (uint32_t b = threadIdx.x; b < nb; b += kRegionThreads) {
-    if (s_dirty[b >> 5] & (1u << (b & 31))) {
-      dst[2 * b] = s_slots[2 * b];
-      dst[2 * b + 1] = s_slots[2 * b + 1];
-    }
-  }
-  if (threadIdx.x == 0 && s_tombs) atomicSub(&counters[ASH_CTR_TOMBS], s_tombs);
-}
-
-// Spilled records on the global table (k_claim's probe); the list is in no
-// particular order, so a group of equal keys in a warp resolves through its
-// lowest batch position, not its lowest lane.
-template <int A>
-__global__ void __launch_bounds__(kBlock) k_claim_spill(Table t, const int32_t* __restrict__ keys,
-                                                        const int32_t* __restrict__ spill, const int32_t* spill_cnt,
-                                                        int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                                        int32_t* counters, int32_t* tile_cnt) {
-  const int32_t n = *spill_cnt;
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kBlock;
-  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(kBlock) + (threadIdx.x & ~31); i0 < n; i0 += stride) {
-    const int64_t i = i0 + lane;
-    const bool valid = i < n;
-    const unsigned live = __ballot_sync(0xFFFFFFFFu, valid);
-    if (!valid) continue;
-    const uint32_t pos = static_cast<uint32_t>(spill[i]);
-    Key<A> k = load_key<A>(keys, pos, A);
-    const uint32_t h = hash_key<A>(k, A);
-    unsigned grp = __match_any_sync(live, h);
-    unsigned g2;
-    same_key_in_warp<A>(k, live, &g2);
-    grp &= g2;
-    const uint32_t minpos = __reduce_min_sync(grp, pos);
-    const int leader = __ffs(__ballot_sync(grp, pos == minpos)) - 1;
-    uint32_t res = 0;
-    bool tomb = false, cand = false;
-    if (lane == leader)
-      res = probe_claim<A>(t, k, h, pos, keys, mask, counters, tile_cnt, &tomb, &cand);
-    if (tomb) atomicSub(&counters[ASH_CTR_TOMBS], 1);
-    const uint32_t lres = __shfl_sync(grp, res, leader);
-    if (lane == leader) {
-      tmp[pos] = static_cast<int32_t>(res);
-    } else if (lres < PEND) {
-      tmp[pos] = static_cast<int32_t>(lres);
-    } else {
-      tmp[pos] = static_cast<int32_t>(PEND);
-      mask[pos] = DEMOTED;
-    }
-  }
-}
-
-// Winners per 2048-position tile from the scratch encoding (overwrites the
-// counts; the binned claim does not keep them incrementally)
-__global__ void __launch_bounds__(kBlock) k_tile_count(const int32_t* __restrict__ tmp,
-                                                       const uint8_t* __restrict__ mask, int64_t n,
-                                                       int32_t* __restrict__ tile_cnt) {
-  __shared__ int32_t s_cnt[kBlock / 32];
-  const int64_t p0 = blockIdx.x * static_cast<int64_t>(kTile) + threadIdx.x * kItems;  // 8 consecutive
-  int c = 0;
-  if (p0 + kItems <= n) {
-    const int4 a = *reinterpret_cast<const int4*>(tmp + p0);
-    const int4 b = *reinterpret_cast<const int4*>(tmp + p0 + 4);
-    const uint2 mk = *reinterpret_cast<const uint2*>(mask + p0);
-    const int32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t m8 = ((i < 4 ? mk.x : mk.y) >> (8 * (i & 3))) & 0xFF;
-      c += v[i] < 0 && !(m8 & DEMOTED);
-    }
-  } else {
-    for (int64_t p = p0; p < n && p < p0 + kItems; ++p) c += tmp[p] < 0 && !(mask[p] & DEMOTED);
-  }
-  c = __reduce_add_sync(0xFFFFFFFFu, c);
-  if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int x = threadIdx.x < kBlock / 32 ? s_cnt[threadIdx.x] : 0;
-    x = __reduce_add_sync(0xFFFFFFFFu, x);
-    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = x;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // single-pass (decoupled look-back) tile scan over a 0/1 predicate
 
 constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
@@ -2306,10 +1823,7 @@ int arity_class(int arity) { return arity <= 3 ? arity : 0; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int g_commit_bulk = -1;  // ASH_COMMIT_BULK=0 selects the plain commit (A/B runs)
-int g_bin_div = 0;       // binned claim when n * g_bin_div >= n_slots (0: never)
-constexpr int64_t kMinBinned = 1 << 16;
 
-inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 int g_sweep_div = 5;     // table sweep when winners >= n_buckets / g_sweep_div (0: never)
 
 void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words, const ash_map_t* m, int64_t sweep_min,
@@ -2413,11 +1927,6 @@ int ash_set_commit_mode(int32_t bulk, int32_t sweep_div) {
   return ASH_OK;
 }
 
-int ash_set_claim_mode(int32_t bin_div) {
-  if (bin_div < 0) return fail(ASH_ERR_INVALID, "bin divisor must be >= 0");
-  g_bin_div = bin_div;
-  return ASH_OK;
-}
 
 int ash_set_stream_hints(int32_t on) {
   g_stream_hints = on ? 1u : 0u;
@@ -2482,11 +1991,6 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
   return check_launch("ash_find_lattice");
 }
 
-int64_t ash_bin_ws_bytes(int64_t n, int64_t n_slots) {
-  const int64_t regions = (n_slots / 2 + kRegionBuckets - 1) / kRegionBuckets;
-  return align256(n * 16) + align256(n * 4) + 3 * align256((regions + 1) * 4) + 256;
-}
-
 int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
                      void* stream) {
   if (int rc = check_map(m)) return rc;
@@ -2496,57 +2000,6 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   Table t = make_table(m);
   cudaStream_t s = as_stream(stream);
   if (int rc = check_tiles(m, n)) return rc;
-  const int64_t n_regions = (t.n_buckets + kRegionBuckets - 1) / kRegionBuckets;
-  if (g_bin_div > 0 && m->arity <= 3 && n >= kMinBinned && n * g_bin_div >= m->n_slots && n_regions <= kMaxRegions &&
-      m->bin_ws && m->bin_ws_bytes >= ash_bin_ws_bytes(n, m->n_slots) && aligned16(out_idx) && aligned16(out_mask)) {
-    uint8_t* ws = static_cast<uint8_t*>(m->bin_ws);
-    uint4* bins = reinterpret_cast<uint4*>(ws);
-    ws += align256(n * 16);
-    int32_t* spill = reinterpret_cast<int32_t*>(ws);
-    ws += align256(n * 4);
-    int32_t* region_cnt = reinterpret_cast<int32_t*>(ws);
-    ws += align256((n_regions + 1) * 4);
-    int32_t* region_off = reinterpret_cast<int32_t*>(ws);
-    ws += align256((n_regions + 1) * 4);
-    int32_t* cursor = reinterpret_cast<int32_t*>(ws);
-    ws += align256((n_regions + 1) * 4);
-    int32_t* spill_cnt = reinterpret_cast<int32_t*>(ws);
-    cudaMemsetAsync(region_cnt, 0, sizeof(int32_t) * n_regions, s);
-    cudaMemsetAsync(spill_cnt, 0, sizeof(int32_t), s);
-    const int nr = static_cast<int>(n_regions);
-    const size_t hist = sizeof(int32_t) * nr;
-    static bool attr_done = false;
-    if (!attr_done) {
-      cudaFuncSetAttribute(k_region_claim<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
-      cudaFuncSetAttribute(k_region_claim<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
-      cudaFuncSetAttribute(k_region_claim<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRegionSlots * 16);
-      attr_done = true;
-    }
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-#define ASH_BINNED(A_)                                                                                             \
-  k_bin_count<A_><<<grid_for(n, kBinThreads * kBinItems), kBinThreads, hist, s>>>(keys, n, t.n_buckets, nr,      \
-                                                                                   region_cnt); note_launch();                  \
-  k_excl_scan<<<1, 1024, 0, s>>>(region_cnt, nr, region_off, cursor); note_launch();                                            \
-  k_bin_scatter<A_><<<grid_for(n, kScatterThreads * kScatterItems), kScatterThreads, hist, s>>>(                 \
-      keys, n, t.n_buckets, nr, cursor, bins); note_launch();                                                                     \
-  k_region_claim<A_><<<nr, kRegionThreads, kRegionSlots * 16, s>>>(t, bins, region_off, out_idx, out_mask,         \
-                                                                   m->counters, spill, spill_cnt); note_launch();               \
-  k_claim_spill<A_><<<sms * 4, kBlock, 0, s>>>(t, keys, spill, spill_cnt, out_idx, out_mask, m->counters,         \
-                                               m->tile_counts); note_launch();
-    switch (m->arity) {
-      case 1: ASH_BINNED(1); break;
-      case 2: ASH_BINNED(2); break;
-      default: ASH_BINNED(3); break;
-    }
-#undef ASH_BINNED
-    k_tile_count<<<grid_for(n, kTile), kBlock, 0, s>>>(out_idx, out_mask, n, m->tile_counts); note_launch();
-    return check_launch("ash_insert_claim (binned)");
-  }
   cudaMemsetAsync(out_mask, 0, n, s);
   ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(
                                    t, keys, n, out_idx, out_mask, m->counters, m->tile_counts)));

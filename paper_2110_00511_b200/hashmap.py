@@ -206,8 +206,6 @@ _SLOT_LIMIT = 0.75  # rebuild the table when non-EMPTY slots would pass this
 # device insert batches run as sequential chunks of this many positions
 # (0 = one batch); exact for insert, see HashMap._pipelined
 INSERT_CHUNK = int(os.environ.get("ASH_INSERT_CHUNK", "0"))
-# binned claim for dense batches (libash ash_set_claim_mode; ASH_BIN_DIV=0 disables)
-BIN_CLAIM = int(os.environ.get("ASH_BIN_DIV", "0")) > 0
 
 
 class HashMap:
@@ -307,17 +305,6 @@ class HashMap:
             self._struct.rank_words = self._rank_words.data_ptr()
             self._struct.rank_words_len = self._rank_words.numel()
 
-    def _ensure_bin_ws(self, n: int) -> None:
-        """Binned-claim workspace (records, spill list, region counts) for a
-        dense batch of n positions; sized on demand, kept across batches."""
-        if not (BIN_CLAIM and n >= (1 << 16) and 2 * n >= self._n_slots):
-            return
-        need = int(_lib.lib.ash_bin_ws_bytes(n, self._n_slots))
-        ws = getattr(self, "_bin_ws", None)
-        if ws is None or ws.numel() < need:
-            ws = self._bin_ws = torch.empty(need, dtype=torch.uint8, device=self._device)
-        self._struct.bin_ws = ws.data_ptr()
-        self._struct.bin_ws_bytes = ws.numel()
 
     def _ptr(self):
         return _lib.ctypes.byref(self._struct)
@@ -617,7 +604,6 @@ class HashMap:
         while True:
             self._reserve_slots(m)
             self._ensure_scan(m)
-            self._ensure_bin_ws(m)
             if m > self._capacity - self._top_ub:
                 self._sync_size()
             free = self._capacity - self._top_ub
@@ -665,7 +651,6 @@ class HashMap:
         while True:
             self._reserve_slots(m)
             self._ensure_scan(m)
-            self._ensure_bin_ws(m)
             if m > self._capacity - self._top_ub:
                 self._sync_size()
             free = self._capacity - self._top_ub
