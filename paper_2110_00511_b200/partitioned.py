@@ -361,7 +361,8 @@ class PartitionedHashMap:
 
     @property
     def size(self) -> int:
-        t = torch.tensor([self.local_size], dtype=torch.int64, device=self.device)
+        dev = "cpu" if dist.get_backend(self.group) == "gloo" else self.device
+        t = torch.tensor([self.local_size], dtype=torch.int64, device=dev)
         dist.all_reduce(t, group=self.group)
         return int(t.item())
 
@@ -369,9 +370,16 @@ class PartitionedHashMap:
 # ---------------------------------------------------------------------------
 # bench.py entry for N > 1 (torchrun; NCCL)
 
+def _shared_gpu() -> bool:
+    """ASH_SHARED_GPU=1: every rank on cuda:0 with a gloo control plane and
+    CUDA-IPC peer mappings, so the N-rank bench path can run on one GPU."""
+    import os
+    return os.environ.get("ASH_SHARED_GPU", "0") == "1"
+
+
 def _bench_init():
     import os
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if _shared_gpu() else int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     if "MASTER_ADDR" not in os.environ:  # plain `python bench.py --partitioned`
@@ -380,13 +388,27 @@ def _bench_init():
             s.bind(("127.0.0.1", 0))
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]),
                               RANK="0", WORLD_SIZE="1")
-    dist.init_process_group("nccl", device_id=dev)
+    if _shared_gpu():
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     return dev
+
+
+def _reduce(x, op=dist.ReduceOp.SUM, dev=None):
+    """All-reduce of a host scalar (CPU tensor under gloo, device under NCCL)."""
+    on_dev = dist.get_backend() != "gloo"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=op)
+    return float(t.item())
 
 
 def _make_pm(args, capacity: int, dev):
     import sys
     transport = getattr(args, "transport", "nccl")
+    if _shared_gpu():
+        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport="peer",
+                                  peer_mapping="ipc"), "peer"
     try:
         return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport=transport), transport
     except Exception as exc:  # no symmetric memory on this node: NCCL all-to-all instead
@@ -429,13 +451,10 @@ def bench_c5(args, rank: int, world: int) -> None:
         f = pm.find(q)
         b.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms += float(t.item())
+        ms += _reduce(a.elapsed_time(b), dist.ReduceOp.MAX, dev)
         ops += 2 * size
-        hits = torch.tensor([int(f.masks.sum())], dtype=torch.int64, device=dev)
-        dist.all_reduce(hits)
-        assert int(hits.item()) == size // 2, (s, int(hits.item()))
+        hits = int(_reduce(int(f.masks.sum()), dev=dev))
+        assert hits == size // 2, (s, hits)
     from . import _lib
     launches = _lib.lib.ash_launch_count() - launches0
     assert pm.size == total
@@ -448,9 +467,12 @@ def bench_c5(args, rank: int, world: int) -> None:
             "config": {"workload": "configs[4]: 400M-key hash-partitioned map built by the mixed stream "
                                    "(12 steps of 2^25 inserts + 2^25 finds, half present); every rank holds "
                                    "a contiguous 1/N slice of each global batch; time = max over ranks",
-                       "routing": "peer-memory put/pull (symmetric memory)" if transport == "peer"
+                       "routing": ("peer-memory put/pull (CUDA IPC, shared GPU)" if _shared_gpu() else
+                                   "peer-memory put/pull (symmetric memory)") if transport == "peer"
                                   else "NCCL all-to-all",
-                       "parallelism": f"hash-partitioned x{world}"},
+                       "parallelism": f"hash-partitioned x{world}",
+                       **({"note": "ASH_SHARED_GPU: all ranks on one GPU (functional run, not a scaling "
+                                   "number)"} if _shared_gpu() else {})},
             "gpu_launches": launches,
         }), flush=True)
     dist.destroy_process_group()
@@ -503,9 +525,7 @@ def bench_main(args, rank: int, world: int) -> None:
     torch.cuda.synchronize()
     launches = _lib.lib.ash_launch_count() - launches0
     dist.barrier()
-    ms = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    ms = _reduce(statistics.mean(times), dist.ReduceOp.MAX, dev)
     value = 2 * per_rank * world / (ms / 1e3) / 1e6
     if rank == 0:
         print(json.dumps({
@@ -515,9 +535,12 @@ def bench_main(args, rank: int, world: int) -> None:
             "data": "synthetic",
             "config": {"workload": f"hash-partitioned map, {per_rank:,} insert + {per_rank:,} find "
                                    f"int3 keys per rank per step (uniqueness {rho}); step time = max over ranks",
-                       "routing": "peer-memory put/pull (symmetric memory)" if transport == "peer"
+                       "routing": ("peer-memory put/pull (CUDA IPC, shared GPU)" if _shared_gpu() else
+                                   "peer-memory put/pull (symmetric memory)") if transport == "peer"
                                   else "NCCL all-to-all",
-                       "parallelism": f"hash-partitioned x{world}"},
+                       "parallelism": f"hash-partitioned x{world}",
+                       **({"note": "ASH_SHARED_GPU: all ranks on one GPU (functional run, not a scaling "
+                                   "number)"} if _shared_gpu() else {})},
             "gpu_launches": launches,  # libash kernels in the timed region (ash_launch_count)
         }), flush=True)
     dist.destroy_process_group()
