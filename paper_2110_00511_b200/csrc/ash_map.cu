@@ -14,6 +14,8 @@
 // Keys are int32 rows; arity <= 3 is compared inline, larger arities compare
 // the first three words inline and the rest against the key rows.
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -1826,15 +1828,32 @@ int g_commit_bulk = -1;  // ASH_COMMIT_BULK=0 selects the plain commit (A/B runs
 
 int g_sweep_div = 5;     // table sweep when winners >= n_buckets / g_sweep_div (0: never)
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
+// SM count of the current device (cached per device; a racing first call
+// just computes the same value twice)
+int device_sms() {
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v < 1) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words, const ash_map_t* m, int64_t sweep_min,
                   cudaStream_t s) {
   if (sweep_min == INT64_MAX) return;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   unsigned g = grid_for(t.n_buckets, kBlock);
   const unsigned cap = static_cast<unsigned>(sms) * 8;
   k_commit_sweep<<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min); note_launch();
@@ -1846,15 +1865,17 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
                        int64_t sweep_min, int32_t* rank_words, cudaStream_t s) {
   constexpr int SV = (VW > 0 && VW <= 4) ? VW : 0;
   constexpr size_t smem = kCommitStages * CommitStage<A, SV>::kBytes;
-  static int blocks_per_sm = 0, sms = 0;
+  // the >48 KB dynamic shared memory opt-in and the occupancy, per device
+  static std::atomic<int> bps_cache[kMaxDevices];
+  const int dev = current_device();
+  int blocks_per_sm = bps_cache[dev].load(std::memory_order_relaxed);
   if (!blocks_per_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaFuncSetAttribute(k_commit_bulk<A, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_commit_bulk<A, VW>, kCommitThreads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (blocks_per_sm < 1) return fail(ASH_ERR_CUDA, "k_commit_bulk does not fit on an SM");
+    bps_cache[dev].store(blocks_per_sm, std::memory_order_relaxed);
   }
+  const int sms = device_sms();
   const int64_t T = tiles_for(n);
   const int64_t cap = static_cast<int64_t>(blocks_per_sm) * sms;
   const unsigned grid = static_cast<unsigned>(T < cap ? T : cap);
@@ -1954,7 +1975,7 @@ int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream) {
   cudaStream_t s = as_stream(stream);
   int64_t work = m->n_slots > m->capacity ? m->n_slots : m->capacity;
   unsigned g = grid_for(work, kBlock);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > static_cast<unsigned>(device_sms()) * 16) g = device_sms() * 16;
   k_reset<<<g, kBlock, 0, s>>>(static_cast<uint4*>(m->slots), m->n_slots, m->heap, m->active,
                                m->erase_claim, m->freed, m->capacity, m->counters); note_launch();
   if (zero_rows) {
@@ -2181,7 +2202,7 @@ int ash_rebuild_table(ash_map_t* m, void* new_slots, int64_t new_n_slots, void* 
     return fail(ASH_ERR_INVALID, "bad new table");
   cudaStream_t s = as_stream(stream);
   unsigned g = grid_for(new_n_slots, kBlock);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > static_cast<unsigned>(device_sms()) * 16) g = device_sms() * 16;
   k_fill_empty<<<g, kBlock, 0, s>>>(static_cast<uint4*>(new_slots), new_n_slots); note_launch();
   ash_map_t nm = *m;
   nm.slots = new_slots;
@@ -2196,7 +2217,7 @@ int ash_table_clear(void* slots, int64_t n_slots, void* stream) {
   if (!slots || n_slots < 0) return fail(ASH_ERR_INVALID, "bad table");
   if (n_slots == 0) return ASH_OK;
   unsigned g = grid_for(n_slots, kBlock);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > static_cast<unsigned>(device_sms()) * 16) g = device_sms() * 16;
   k_fill_empty<<<g, kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(slots), n_slots); note_launch();
   return check_launch("ash_table_clear");
 }
