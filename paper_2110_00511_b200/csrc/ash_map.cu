@@ -1136,8 +1136,8 @@ __global__ void k_heap_dirty(int32_t* counters, int64_t n) {
 // shared memory with cp.async.bulk (TMA 1-D) two tiles ahead, completion on an
 // mbarrier; eight consumer warps rank the winners and issue only stores.
 
-constexpr int kCommitConsumers = kBlock;             // 8 consumer warps
-constexpr int kCommitThreads = kBlock + 32;          // + 1 producer warp
+constexpr int kCommitConsumers = kBlock;  // 8 consumer warps (512 measured: same time)
+constexpr int kCommitThreads = kCommitConsumers + 32;  // + 1 producer warp
 constexpr int kCommitStages = 2;
 
 __host__ __device__ constexpr uint32_t align128(uint32_t x) { return (x + 127u) & ~127u; }
@@ -1222,6 +1222,9 @@ __global__ void __launch_bounds__(kCommitThreads)
   }
 
   // ---------------- consumer warps ----------------
+  // kCT consumer threads, kCI positions each (kCI x kCW = 64 scan entries)
+  constexpr int kCT = kCommitConsumers, kCW = kCT / 32, kCI = kTile / kCT;
+  static_assert(kCI * kCW == 64, "tile scan expects 64 (item, warp) counts");
   const int arity = A;
   int i = 0;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++i) {
@@ -1237,27 +1240,27 @@ __global__ void __launch_bounds__(kCommitThreads)
     const int heap_off = info[s].heap_off;
     const int64_t base = tile * kTile;
 
-    int32_t v[kItems];
-    bool win[kItems];
+    int32_t v[kCI];
+    bool win[kCI];
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int r = it * kBlock + threadIdx.x;
+    for (int it = 0; it < kCI; ++it) {
+      const int r = it * kCT + threadIdx.x;
       v[it] = r < rows ? s_tmp[r] : 0;
       win[it] = r < rows && v[it] < 0 && !(s_mask[r] & DEMOTED);
     }
-    RowWords<(VW > 4 ? VW : 1)> grow[kItems];
+    RowWords<(VW > 4 ? VW : 1)> grow[kCI];
     if (VW > 4) {  // large rows: per-winner loads, in flight across the scan
 #pragma unroll
-      for (int it = 0; it < kItems; ++it)
+      for (int it = 0; it < kCI; ++it)
         if (win[it])
-          load_row<(VW > 4 ? VW : 1)>(grow[it], va.src[0] + (base + it * kBlock + threadIdx.x) * VW * 4, pol);
+          load_row<(VW > 4 ? VW : 1)>(grow[it], va.src[0] + (base + it * kCT + threadIdx.x) * VW * 4, pol);
     }
     // in-tile ranks (ballots + one warp scan; consumer-only named barrier)
-    uint32_t bal[kItems];
+    uint32_t bal[kCI];
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
+    for (int it = 0; it < kCI; ++it) {
       bal[it] = __ballot_sync(0xFFFFFFFFu, win[it]);
-      if (lane == 0) sm.cnt[it * kWarps + warp] = __popc(bal[it]);
+      if (lane == 0) sm.cnt[it * kCW + warp] = __popc(bal[it]);
     }
     named_sync(1, kCommitConsumers);
     if (warp == 0) {
@@ -1276,20 +1279,20 @@ __global__ void __launch_bounds__(kCommitThreads)
     if (defer && rank_words && lane == 0) {
       const uint32_t tpre = info[s].pre;
 #pragma unroll
-      for (int it = 0; it < kItems; ++it) {
-        const int r0 = it * kBlock + warp * 32;
+      for (int it = 0; it < kCI; ++it) {
+        const int r0 = it * kCT + warp * 32;
         if (r0 < rows)
           reinterpret_cast<uint2*>(rank_words)[(base + r0) >> 5] =
-              make_uint2(bal[it], tpre + sm.pre[it * kWarps + warp]);
+              make_uint2(bal[it], tpre + sm.pre[it * kCW + warp]);
       }
     }
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int r = it * kBlock + threadIdx.x;
+    for (int it = 0; it < kCI; ++it) {
+      const int r = it * kCT + threadIdx.x;
       if (r >= rows) continue;
       const int64_t p = base + r;
       if (win[it]) {
-        const uint32_t rank = sm.pre[it * kWarps + warp] + __popc(bal[it] & lanemask_lt());
+        const uint32_t rank = sm.pre[it * kCW + warp] + __popc(bal[it] & lanemask_lt());
         const int32_t idx = s_heap[heap_off + rank];
         const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
         if (!defer) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
