@@ -228,6 +228,13 @@ int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_
 int ash_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
                      void* dst, void* stream);
 
+/* Distinct int3 rows of a batch in first-occurrence order (the local
+ * activate + survivor gather of tsdf/grid.py:140-142 without a local map):
+ * out_keys[0 .. ws->counters[ASH_CTR_COUNT]) and, if out_first is given,
+ * their first positions (int64).  Workspace rules as for ash_voxelize. */
+int ash_unique_rows(ash_map_t* ws, const int32_t* keys, int64_t n, int32_t* out_keys,
+                    int64_t* out_first, int32_t* scratch_idx, uint8_t* scratch_mask, void* stream);
+
 /* Block candidates of one depth frame (tsdf/grid.py:98-125 _candidate_blocks
  * + block_of :24-27).  depth: height x width float64 (row-major, device);
  * cam = {fx, fy, cx, cy, depth_min, depth_max}; pose: 4x4 row-major float64

@@ -64,6 +64,7 @@ _SIGNATURES = {
     "ash_quantize": (c_int32, [c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p, c_void_p]),
     "ash_voxelize": (c_int32, [_M, c_void_p, c_int32, c_int64, c_double, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
+    "ash_unique_rows": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ash_frame_positions": (c_int64, [c_int64, c_int64, c_double, c_double, c_int32]),
     "ash_frame_candidates": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,
                                        c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),

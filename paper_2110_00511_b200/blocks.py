@@ -15,26 +15,47 @@ from ._lib import call
 from .hashmap import HashMap, ValueSpec, _stream_handle
 
 __all__ = ["allocate_blocks", "BlockGrid", "frame_candidates", "frame_blocks", "allocate_frame",
-           "LocalBlockMap"]
+           "LocalBlockMap", "unique_rows"]
+
+
+def unique_rows(keys: torch.Tensor) -> torch.Tensor:
+    """Distinct int3 rows of a device batch in first-occurrence order — the
+    survivors ``coords[local.activate(coords).masks]`` of tsdf/grid.py:140-142
+    — in one fused dedup pass on the shared workspace table (libash
+    ``ash_unique_rows``), no per-frame local map."""
+    from .geometry import _VoxelWorkspace
+    dev = keys.device
+    n = keys.shape[0]
+    if n == 0:
+        return keys[:0]
+    ws = _VoxelWorkspace.get(dev)
+    with _VoxelWorkspace._lock:
+        ws.reserve(n)
+        out = torch.empty((n, 3), dtype=torch.int32, device=dev)
+        scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
+        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        count, _ = ws.run(lambda: call(
+            "ash_unique_rows", ctypes.byref(ws.struct), keys.data_ptr(), n, out.data_ptr(), None,
+            scratch_idx.data_ptr(), scratch_mask.data_ptr(), _stream_handle(dev)))
+    return out[:count]
 
 
 def allocate_blocks(global_map: HashMap, coords, threads: int = 1):
     """grid.py:136-150 for a given candidate batch.
 
     Returns ``(gi, local_map)``: global indices of the frame's distinct blocks
-    (first-occurrence order) and the local dedup map whose value buffer 0
-    holds each block's global index."""
+    (first-occurrence order) and the local map (block -> global index).  The
+    distinct blocks come from one fused dedup pass; the local map — needed
+    only by frame-scoped queries (tsdf/raycast.py:32-35) — is built on first
+    use with the reference's indices (``LocalBlockMap``)."""
     coords = global_map._check_keys(coords)
     if coords.shape[0] == 0:
         return torch.zeros(0, dtype=torch.int32, device=global_map.device), None
-    local = HashMap(coords.shape[0], 3, value_specs=[np.int32], threads=threads,
-                    device=global_map.device)
-    li, lmask = local.activate(coords)
-    survivors = coords[lmask]
-    global_map.activate(survivors)
-    gi, gmask = global_map.find(survivors)
-    local.value_buffer(0)[li[lmask].long(), 0] = gi
-    return gi, local
+    if global_map.key_arity != 3:
+        raise ValueError("block coordinates must have key arity 3")
+    survivors = unique_rows(coords.contiguous())
+    gi, gmask = global_map.activate(survivors)
+    return gi, LocalBlockMap(survivors, gi, coords.shape[0], global_map.device)
 
 
 class BlockGrid:

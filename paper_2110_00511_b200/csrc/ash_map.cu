@@ -1606,6 +1606,16 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
   }
 };
 
+struct RowSrc {  // int3 key rows as given (the local activate of grid.py:140-142)
+  const int32_t* keys;
+  __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool*) const {
+    const uint64_t pol = stream_policy(1);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) k.w[d] = ld_stream(keys + 3 * p + d, pol);
+    return true;
+  }
+};
+
 // tsdf/grid.py:98-125 _candidate_blocks + grid.py:24-27 block_of, per depth
 // pixel (row-major) x per sample: ray mode samples the ray within +-trunc of
 // the surface at half-block spacing (tsdf/grid.py:115-125); neighbor mode is
@@ -2278,6 +2288,21 @@ int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t
   cudaMemsetAsync(scratch_mask, 0, n, s);
   run_dedup_select(make_table(ws), ws, f, n, out_coords, nullptr, scratch_idx, scratch_mask, s);
   return check_launch("ash_frame_blocks");
+}
+
+int ash_unique_rows(ash_map_t* ws, const int32_t* keys, int64_t n, int32_t* out_keys, int64_t* out_first,
+                    int32_t* scratch_idx, uint8_t* scratch_mask, void* stream) {
+  if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
+  if (int rc = check_batch(n)) return rc;
+  if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (int rc = check_tiles(ws, n)) return rc;
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
+  if (n == 0) return check_launch("ash_unique_rows");
+  if (!keys || !out_keys || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
+  cudaMemsetAsync(scratch_mask, 0, n, s);
+  run_dedup_select(make_table(ws), ws, RowSrc{keys}, n, out_keys, out_first, scratch_idx, scratch_mask, s);
+  return check_launch("ash_unique_rows");
 }
 
 int ash_frame_candidates(const double* depth, int64_t height, int64_t width, const double* cam, const double* pose,
