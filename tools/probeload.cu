@@ -4,6 +4,7 @@
 // many sectors each flavour pulls per probe.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/probeload tools/probeload.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -37,8 +38,10 @@ __global__ void k_probe(const uint4* __restrict__ tab, uint32_t n_buckets, int64
   out[i] = r[0] ^ r[3] ^ r[4] ^ r[7];
 }
 
-int main() {
-  const uint32_t n_buckets = 7500000;  // 15M 16-byte slots = 240 MB
+int main(int argc, char** argv) {
+  // table size in MB (default 240; e.g. 9600 for the configs[4] table)
+  const uint32_t n_buckets = (argc > 1 ? (uint32_t)(atof(argv[1]) * 1e6 / 32) : 7500000u);
+  printf("table %.0f MB\n", n_buckets * 32.0 / 1e6);
   const int64_t n = 10000000;
   uint4* tab; uint32_t* out;
   cudaMalloc(&tab, (size_t)n_buckets * 32);
