@@ -6,16 +6,22 @@ on): a fresh map of capacity 10M, one insert of 10M int3 keys (uniqueness
 that insert + find; value = (insert ops + find ops) / step time.  Map
 construction (HashMap.clear) is excluded from the step as in the reference
 timing loop (pkg/src/spatialhash/bench.py:110,123).  The working set (keys
-120 MB + values 40 MB + table 512 MB) exceeds the 126 MB L2, and L2 is also
-flushed between steps.
+120 MB + values 40 MB + table 240 MB) exceeds the 126 MB L2, and L2 is also
+flushed between steps.  The line also carries the e2e figure (host in / host
+out through the public API), the dominant kernel's roofline, the measured
+random-probe ceiling, the CPU baseline, clocks, the libash launch count, the
+configs[1] sweep and configs[2..4] in `other_configs`.
 
 Arms:
   default            this repo's CUDA path; one JSON line on rank 0.
-  --impl reference   the reference algorithm on the host CPU (the numpy
-                     oracle port, oracle/ash_oracle.py, since the reference is
-                     pure Python and cannot travel to the GPU box).
-Multi-GPU (torchrun, N>1): hash-partitioned map, peer-memory routing (NCCL all-to-all with --transport nccl),
-10M insert + 10M find keys per rank per step (weak scaling).
+  --impl reference   the reference algorithm on the host CPU: the numpy oracle
+                     port (oracle/ash_oracle.py; the reference is pure Python
+                     and cannot travel to the GPU box) on every host core, the
+                     sample sharded by key hash over one process per core.
+Multi-GPU (torchrun, N>1): hash-partitioned map, peer-memory routing (NCCL
+all-to-all with --transport nccl), 10M insert + 10M find keys per rank per
+step (weak scaling).  --c5: configs[4], the 400M-key partitioned map built by
+the mixed stream (strong scaling).
 """
 from __future__ import annotations
 
