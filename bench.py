@@ -42,7 +42,7 @@ sys.path.insert(0, str(ROOT))
 N_KEYS = 10_000_000
 RHO = 0.5
 CAPACITY = 10_000_000
-CPU_SAMPLE_KEYS = 1_000_000  # per host core (the CPU arm shards by key hash)
+CPU_SAMPLE_KEYS = int(os.environ.get("ASH_CPU_SAMPLE_KEYS", 1_000_000))  # per host core (sharded by key hash)
 METRIC = "insert & find Mops/s (int3 keys)"
 UNIT = "Mops/s"
 
