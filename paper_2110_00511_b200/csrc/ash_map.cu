@@ -1592,10 +1592,28 @@ __global__ void k_quantize(const T* __restrict__ pts, int64_t n, double cell, in
 // table, then the ascending select of first occurrences).  key() builds the
 // int3 key of virtual position p; false = no candidate at p.
 
-template <typename T>
+template <typename T, bool STAGED = true>
 struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
+  static constexpr bool kStaged = STAGED;  // full warps stage their 32 rows with 16-byte loads (aligned clouds)
+  static constexpr int kRowBytes = 3 * sizeof(T);
   const T* pts;
   double cell;
+  // warp-cooperative: the warp's 32 consecutive points (32 x 3 x sizeof(T)
+  // bytes, 16-byte aligned) come in as 16-byte vector loads through shared
+  // memory instead of three strided scalar loads per lane
+  __device__ __forceinline__ bool key_staged(int64_t warp_base, Key<3>& k, bool* bad, uint4* stage) const {
+    const int lane = threadIdx.x & 31;
+    constexpr int kChunks = 32 * kRowBytes / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(pts + 3 * warp_base);
+    const uint64_t pol = stream_policy(1);
+#pragma unroll
+    for (int c = lane; c < kChunks; c += 32) stage[c] = ld_stream_v4(src + c, pol);
+    __syncwarp();
+    const T* row = reinterpret_cast<const T*>(stage) + 3 * lane;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(row[d], cell, bad));
+    return true;
+  }
   __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
     // the cloud streams through once: L2 evict-first keeps the (small) set
     // of hot voxel slots resident
@@ -1607,6 +1625,9 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
 };
 
 struct RowSrc {  // int3 key rows as given (the local activate of grid.py:140-142)
+  static constexpr bool kStaged = false;
+  static constexpr int kRowBytes = 16;
+  __device__ __forceinline__ bool key_staged(int64_t, Key<3>&, bool*, uint4*) const { return false; }
   const int32_t* keys;
   __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool*) const {
     const uint64_t pol = stream_policy(1);
@@ -1625,6 +1646,9 @@ struct RowSrc {  // int3 key rows as given (the local activate of grid.py:140-14
 // product as numpy's OpenBLAS dgemm evaluates it (an FMA chain over k =
 // 0, 1, 2 from p0 * R[i][0]), then + trans, floor(x / block).
 struct FrameSrc {
+  static constexpr bool kStaged = false;
+  static constexpr int kRowBytes = 16;
+  __device__ __forceinline__ bool key_staged(int64_t, Key<3>&, bool*, uint4*) const { return false; }
   const double* depth;
   int64_t width;
   int per_pixel;  // n_steps (ray) or 27 (neighbor)
@@ -1668,12 +1692,18 @@ __global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, Src src, int64_
   const int lane = threadIdx.x & 31;
   const bool inside = p < n;
   const unsigned live = __ballot_sync(0xFFFFFFFFu, inside);
-  if (!inside) return;
+  __shared__ uint4 stage[Src::kStaged ? kBlock * Src::kRowBytes / 16 : 1];
   bool bad = false;
   Key<3> k;
   k.row = nullptr;
   k.w[0] = k.w[1] = k.w[2] = 0;
-  const bool has = src.key(p, k, &bad);
+  bool has;
+  if (Src::kStaged && live == 0xFFFFFFFFu) {
+    has = src.key_staged(p - lane, k, &bad, stage + (threadIdx.x >> 5) * (32 * Src::kRowBytes / 16));
+  } else {
+    if (!inside) return;
+    has = src.key(p, k, &bad);
+  }
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
   const bool skip = bad || !has;  // out-of-range points never claim; the host raises first
   const uint32_t h = hash_key<3>(k, 3);
@@ -1728,15 +1758,16 @@ __global__ void __launch_bounds__(kBlock)
     if (!win[it]) continue;
     const int64_t p = base + it * kBlock + threadIdx.x;
     const uint32_t r = item_rank(sm, bal, it);
-    bool bad = false;
-    Key<3> k;
-    k.row = nullptr;
-    src.key(p, k, &bad);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) out_coords[3 * static_cast<int64_t>(r) + d] = static_cast<int32_t>(k.w[d]);
+    // the winner's key words are in its claimed slot (L2-hot: the workspace
+    // is sized to stay resident), no need to regenerate them from the source
+    const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
+    const uint4 sv = slots[slot];
+    out_coords[3 * static_cast<int64_t>(r)] = static_cast<int32_t>(sv.x);
+    out_coords[3 * static_cast<int64_t>(r) + 1] = static_cast<int32_t>(sv.y);
+    out_coords[3 * static_cast<int64_t>(r) + 2] = static_cast<int32_t>(sv.z);
     if (out_sel) out_sel[r] = p;
     // leave the workspace table EMPTY for the next call
-    slots[static_cast<uint32_t>(v[it]) & SLOT_MASK] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+    slots[slot] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
   }
 }
 
@@ -2263,12 +2294,19 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   if (n == 0) return check_launch("ash_voxelize");
   cudaMemsetAsync(scratch_mask, 0, n, s);
   Table t = make_table(ws);
-  if (points_are_f64) {
+  const bool al = aligned16(points);
+  if (points_are_f64 && al) {
     run_dedup_select(t, ws, CloudSrc<double>{static_cast<const double*>(points), voxel}, n, out_coords, out_sel,
                      scratch_idx, scratch_mask, s);
-  } else {
+  } else if (points_are_f64) {
+    run_dedup_select(t, ws, CloudSrc<double, false>{static_cast<const double*>(points), voxel}, n, out_coords,
+                     out_sel, scratch_idx, scratch_mask, s);
+  } else if (al) {
     run_dedup_select(t, ws, CloudSrc<float>{static_cast<const float*>(points), voxel}, n, out_coords, out_sel,
                      scratch_idx, scratch_mask, s);
+  } else {
+    run_dedup_select(t, ws, CloudSrc<float, false>{static_cast<const float*>(points), voxel}, n, out_coords,
+                     out_sel, scratch_idx, scratch_mask, s);
   }
   return check_launch("ash_voxelize");
 }
