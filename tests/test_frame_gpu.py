@@ -129,3 +129,21 @@ def test_empty_and_invalid_frames(ash):
     with pytest.raises(ValueError):
         ash.frame_blocks(np.ones((24, 32)), cam, np.eye(4), BLOCK, TRUNC, allocation="cone",
                          device="cuda")
+
+
+def test_unique_rows_and_workspace_overflow_retry(ash):
+    """ash_unique_rows == first occurrences; a call after a much smaller one
+    overflows the estimate-sized workspace prefix (bounded probe) and must be
+    retried on the full table — results stay exact either way."""
+    import torch
+    from paper_2110_00511_b200.blocks import unique_rows
+    rng = np.random.default_rng(12)
+    small = torch.from_numpy(rng.integers(-3, 3, size=(100_000, 3)).astype(np.int32)).cuda()
+    got = unique_rows(small)
+    G.eq(got, _first_occurrence_rows(small.cpu().numpy()), "small")
+    big = rng.integers(-2 ** 30, 2 ** 30, size=(400_000, 3)).astype(np.int32)  # all distinct
+    big[::7] = big[3]  # a few repeats
+    got = unique_rows(torch.from_numpy(big).cuda())
+    G.eq(got, _first_occurrence_rows(big), "big after small (retried)")
+    got = unique_rows(small)
+    G.eq(got, _first_occurrence_rows(small.cpu().numpy()), "small again")
