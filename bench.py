@@ -633,8 +633,10 @@ def main():
     kms = res["kms"]
     # dominant kernel and its roofline (algorithmic bytes per launch)
     per_kernel_bytes = {
-        "claim": (12 + 32 + 5) * N_KEYS,                    # key, table sector, scratch idx+mask
-        "commit": (5 + 5) * N_KEYS + RHO * (12 + 2 * 4 + 32) * N_KEYS,  # scratch in, out; winner rows + slot
+        # key, probed sector, scratch idx+mask; each winner's CAS writes its slot sector
+        "claim": (12 + 32 + 5) * N_KEYS + RHO * 32 * N_KEYS,
+        # scratch in + out; winner key row, value read + write (the slot was written by the claim)
+        "commit": (5 + 5) * N_KEYS + RHO * (12 + 2 * 4) * N_KEYS,
         "find": algorithmic_bytes("find", RHO, 4) * N_KEYS,
         "tile_scan": 4 * 2 * (N_KEYS / 2048),
     }
