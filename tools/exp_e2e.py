@@ -76,3 +76,28 @@ for _ in range(5):
     copies_only(False)
 torch.cuda.synchronize()
 print(f"copies only (insert-like + find-like): {(time.perf_counter() - t0) / 5 * 1e3:.3f} ms per step")
+
+def h2d_only():
+    c = 1 << 20
+    h2d = torch.cuda.Stream()
+    kd = torch.empty((N, 3), dtype=torch.int32, device=dev)
+    vd = torch.empty((N, 1), dtype=torch.float32, device=dev)
+    for a in range(0, N, c):
+        b = min(N, a + c)
+        with torch.cuda.stream(h2d):
+            kd[a:b].copy_(keys_h[a:b], non_blocking=True)
+            vd[a:b].copy_(vals_h[a:b], non_blocking=True)
+    for a in range(0, N, c):
+        b = min(N, a + c)
+        with torch.cuda.stream(h2d):
+            kd[a:b].copy_(keys_h[a:b], non_blocking=True)
+    h2d.synchronize()
+
+for _ in range(3):
+    h2d_only()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5):
+    h2d_only()
+torch.cuda.synchronize()
+print(f"chunked H2D only (280 MB): {(time.perf_counter() - t0) / 5 * 1e3:.3f} ms per step")
