@@ -61,7 +61,8 @@ __device__ __forceinline__ uint32_t owner_of(const Row& row, int arity, uint32_t
   return static_cast<uint32_t>((static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * world) >> 32);
 }
 
-__device__ __forceinline__ uint32_t owner_of(const int32_t* row, int arity, uint32_t world) {
+// a key row in global memory (read-only path)
+__device__ __forceinline__ uint32_t owner_of_global(const int32_t* row, int arity, uint32_t world) {
   struct Ldg {
     const int32_t* r;
     __device__ int32_t operator[](int d) const { return __ldg(r + d); }
@@ -81,6 +82,37 @@ __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restric
   // every item's owner first (all key loads of the tile in flight), then the
   // warp-aggregated shared-memory counts
   uint32_t own[kItems];
+  const int64_t p8 = base + threadIdx.x * kItems;  // 8 consecutive positions
+  if (arity == 3 && base + kTile <= n && (reinterpret_cast<uintptr_t>(keys) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(owners) & 7) == 0) {  // block-uniform: full tile
+    // int3 keys, full octet: the thread's 8 rows (96 bytes) as six 16-byte
+    // loads, the 8 owner bytes as one 8-byte store; counts do not depend on
+    // the item layout (the scatter recomputes its ranks from `owners`)
+    int32_t kw[kItems * 3];
+    const int4* src = reinterpret_cast<const int4*>(keys + p8 * 3);
+#pragma unroll
+    for (int v = 0; v < kItems * 3 / 4; ++v) {
+      const int4 q = __ldg(src + v);
+      kw[4 * v] = q.x, kw[4 * v + 1] = q.y, kw[4 * v + 2] = q.z, kw[4 * v + 3] = q.w;
+    }
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int32_t row[3] = {kw[3 * it], kw[3 * it + 1], kw[3 * it + 2]};
+      own[it] = owner_of(row, 3, world);
+      if (it < 4) lo |= own[it] << (8 * it);
+      else hi |= own[it] << (8 * (it - 4));
+    }
+    *reinterpret_cast<uint2*>(owners + p8) = make_uint2(lo, hi);
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const unsigned same = __match_any_sync(0xFFFFFFFFu, own[it]);
+      if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s_cnt[own[it]], __popc(same));
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < static_cast<int>(world); o += kBlock) cnt[o * n_tiles + blockIdx.x] = s_cnt[o];
+    return;
+  }
   if (arity == 3) {  // int3 keys: all 24 key words of the thread in flight first
     int32_t kw[kItems][3];
 #pragma unroll
@@ -98,7 +130,7 @@ __global__ void __launch_bounds__(kBlock) k_route_count(const int32_t* __restric
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int64_t p = base + it * kBlock + threadIdx.x;
-      own[it] = p < n ? owner_of(keys + p * arity, arity, world) : 0xFFFFFFFFu;
+      own[it] = p < n ? owner_of_global(keys + p * arity, arity, world) : 0xFFFFFFFFu;
     }
   }
 #pragma unroll
@@ -395,7 +427,7 @@ __global__ void k_scatter_words(const uint32_t* __restrict__ src, const int32_t*
 __global__ void k_owner_of(const int32_t* __restrict__ keys, int64_t n, int arity, uint32_t world,
                            int32_t* __restrict__ out) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
-  if (p < n) out[p] = static_cast<int32_t>(owner_of(keys + p * arity, arity, world));
+  if (p < n) out[p] = static_cast<int32_t>(owner_of_global(keys + p * arity, arity, world));
 }
 
 inline unsigned blocks(int64_t work, int per) {
