@@ -29,7 +29,7 @@ def unique_rows(keys: torch.Tensor) -> torch.Tensor:
     if n == 0:
         return keys[:0]
     ws = _VoxelWorkspace.get(dev)
-    with _VoxelWorkspace._lock:
+    with _VoxelWorkspace._lock, torch.cuda.device(dev):
         ws.reserve(n)
         out = torch.empty((n, 3), dtype=torch.int32, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
@@ -143,8 +143,9 @@ def frame_candidates(depth, intrinsics, pose, block_size: float, trunc: float,
     valid = torch.empty(n, dtype=torch.uint8, device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     if n:
-        call("ash_frame_candidates", d.data_ptr(), h, w, cam, pose_c, float(block_size), float(trunc),
-             nb, out.data_ptr(), valid.data_ptr(), flags.data_ptr(), _stream_handle(dev))
+        with torch.cuda.device(dev):
+            call("ash_frame_candidates", d.data_ptr(), h, w, cam, pose_c, float(block_size), float(trunc),
+                 nb, out.data_ptr(), valid.data_ptr(), flags.data_ptr(), _stream_handle(dev))
     if int(flags.item()) & _lib.FLAG_RANGE:
         raise ValueError("block coordinates exceed int32 range")
     return out[valid.view(torch.bool)]
@@ -165,7 +166,7 @@ def frame_blocks(depth, intrinsics, pose, block_size: float, trunc: float,
     if n == 0:
         return torch.zeros((0, 3), dtype=torch.int32, device=dev)
     ws = _VoxelWorkspace.get(dev)
-    with _VoxelWorkspace._lock:
+    with _VoxelWorkspace._lock, torch.cuda.device(dev):
         ws.reserve(n)
         coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)

@@ -94,8 +94,9 @@ def quantize(positions, cell: float, device=None) -> torch.Tensor:
     if n == 0:
         return out.cpu() if host else out
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
-    call("ash_quantize", pts.data_ptr(), int(pts.dtype == torch.float64), n, float(cell),
-         out.data_ptr(), flags.data_ptr(), _stream_handle(dev))
+    with torch.cuda.device(dev):
+        call("ash_quantize", pts.data_ptr(), int(pts.dtype == torch.float64), n, float(cell),
+             out.data_ptr(), flags.data_ptr(), _stream_handle(dev))
     if int(flags.item()) & _lib.FLAG_RANGE:
         raise ValueError("quantized coordinates exceed int32 range")
     return out.cpu() if host else out
@@ -205,7 +206,7 @@ def voxel_downsample(points, voxel_size: float, backend: str = "generic", thread
         z = (torch.zeros((0, 3), dtype=torch.int32), torch.zeros(0, dtype=torch.int64))
         return z if host else (z[0].to(dev), z[1].to(dev))
     ws = _VoxelWorkspace.get(dev)
-    with _VoxelWorkspace._lock:
+    with _VoxelWorkspace._lock, torch.cuda.device(dev):
         ws.reserve(n)
         coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
         sel = torch.empty(n, dtype=torch.int64, device=dev)
@@ -249,7 +250,7 @@ def radius_neighbors(hashmap: HashMap, coords, r: int = 1) -> BatchResult:
     n, k = c.shape[0], (2 * r + 1) ** 3
     idx = torch.empty((n, k), dtype=torch.int32, device=hashmap.device)
     msk = torch.empty((n, k), dtype=torch.uint8, device=hashmap.device)
-    with hashmap._guard.reading():
+    with hashmap._guard.reading(), torch.cuda.device(hashmap.device):
         if n:
             call("ash_find_lattice", hashmap._ptr(), c.data_ptr(), n, int(r), idx.data_ptr(),
                  msk.data_ptr(), hashmap._stream())

@@ -23,6 +23,7 @@ Differences in mechanism (not in results):
 """
 from __future__ import annotations
 
+import functools
 import math
 import os
 import threading
@@ -186,6 +187,17 @@ def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def on_device(fn):
+    """Run a map method with the map's GPU as the current device: libash
+    launches on the calling thread's current device, and a stream handle of 0
+    (a device's default stream) does not name one."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with torch.cuda.device(self._device):
+            return fn(self, *args, **kwargs)
+    return wrapper
+
+
 # slots per unit of capacity (max live load 1/1.5); chosen by the r01 A/B
 # matrix (tools/exp_matrix.sh): 1.5 beat 2.0 and 1.25 on the C2 sweep
 TABLE_FACTOR = float(os.environ.get("ASH_TABLE_FACTOR", "1.5"))
@@ -243,6 +255,7 @@ class HashMap:
 
     # -- state ---------------------------------------------------------
 
+    @on_device
     def _init_state(self, capacity: int, zero_rows: bool = True) -> None:
         """hashmap.py:200-210: fresh table, heap = arange, zeroed buffers."""
         dev = self._device
@@ -369,6 +382,7 @@ class HashMap:
     def active_buf_indices(self) -> torch.Tensor:
         return self.active_indices()
 
+    @on_device
     def reserve(self, capacity: int) -> None:
         """Grow to at least ``capacity`` (no-op when already large enough)."""
         if int(capacity) > self._capacity:
@@ -551,6 +565,7 @@ class HashMap:
         return (isinstance(keys, torch.Tensor) and not keys.is_cuda and keys.is_pinned()
                 and keys.dim() == 2 and keys.shape[0] >= self.PIPELINE_MIN)
 
+    @on_device
     def insert(self, keys, *values) -> BatchResult:
         """Insert keys with one value batch per value buffer: the first
         occurrence of each absent key wins a fresh index; existing values are
@@ -577,6 +592,7 @@ class HashMap:
             res = self._insert_like(keys, vals, association=False)
         return self._to_host(res) if host else res
 
+    @on_device
     def activate(self, keys) -> BatchResult:
         """Ensure keys are present; values untouched; masks = found OR
         winner (hashmap.py:349-360)."""
@@ -670,6 +686,7 @@ class HashMap:
         call("ash_heap_put_losers", self._ptr(), srt.data_ptr(), m, self._stream())
         self._top_ub = min(self._capacity, self._top_ub + m)
 
+    @on_device
     def find(self, keys) -> BatchResult:
         """Look up keys; the map is not modified (hashmap.py:415-429)."""
         host = self._is_host(keys)
@@ -688,6 +705,7 @@ class HashMap:
             res = BatchResult(idx, msk.view(torch.bool))
         return self._to_host(res) if host else res
 
+    @on_device
     def erase(self, keys) -> torch.Tensor:
         """Remove keys; exactly one True per removed key, at its first batch
         position (hashmap.py:431-456)."""
@@ -705,6 +723,7 @@ class HashMap:
             res = out.view(torch.bool)
         return res.cpu() if host else res
 
+    @on_device
     def active_indices(self) -> torch.Tensor:
         """All buffer indices holding an entry, ascending (hashmap.py:458-460)."""
         with self._guard.reading():
@@ -714,6 +733,7 @@ class HashMap:
                 call("ash_active_indices", self._ptr(), out.data_ptr(), self._stream())
             return out
 
+    @on_device
     def rehash(self, new_capacity: int) -> None:
         """Rebuild at the given capacity; content preserved, indices become
         0..size-1 in ascending old-index order (hashmap.py:462-472)."""
@@ -726,6 +746,7 @@ class HashMap:
         with self._guard.writing():
             self._rehash_into(new_capacity)
 
+    @on_device
     def clear(self) -> None:
         """Remove every entry, keep the capacity (Open3D ``clear``); the map
         is then indistinguishable from a freshly constructed one."""
@@ -738,10 +759,12 @@ class HashMap:
 
     # -- content helpers (hashmap.py:476-496) ----------------------------
 
+    @on_device
     def items_arrays(self) -> tuple:
         act = self.active_indices().long()
         return (self._key_buf[act].clone(), *(b[act].clone() for b in self._value_bufs))
 
+    @on_device
     def validate(self) -> None:
         """Structural invariants (hashmap.py:483-496); raises AssertionError."""
         size = self._sync_size()
@@ -761,6 +784,7 @@ class HashMap:
         flags = int(self._counters[_lib.CTR_FLAGS].item())
         assert flags & _lib.FLAG_TABLE_FULL == 0, "a probe wrapped the whole table"
 
+    @on_device
     def save(self, path, metadata=None) -> None:
         """ASHL v1 snapshot, byte-compatible with the reference (hashmap.py:498-500)."""
         from .serialize import save_map

@@ -233,6 +233,19 @@ class PeerExchange:
         return out, msk.view(torch.bool)
 
 
+def _on_device(fn):
+    """Run a partitioned op with this rank's GPU as the current device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        if self.device.type != "cuda":
+            return fn(self, *args, **kwargs)
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+    return wrapper
+
+
 class PartitionedHashMap:
     """One shard per rank; batch ops are collective (every rank calls them
     with its own slice of the global batch, possibly empty)."""
@@ -322,6 +335,7 @@ class PartitionedHashMap:
         out, msk = self.peer.combine(torch.as_tensor(res.indices), ctx)
         return PartitionedResult(out, msk, ctx[1])
 
+    @_on_device
     def insert(self, keys, *values) -> PartitionedResult:
         keys = self._keys(keys)
         vals = self._values(keys.shape[0], values)
@@ -331,6 +345,7 @@ class PartitionedHashMap:
         res = self.local.insert(rkeys, *rvals)  # the shard reshapes (n, -1) rows itself
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
+    @_on_device
     def activate(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
         if self.peer is not None:
@@ -339,6 +354,7 @@ class PartitionedHashMap:
         res = self.local.activate(rkeys)
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
+    @_on_device
     def find(self, keys) -> PartitionedResult:
         keys = self._keys(keys)
         if self.peer is not None:
@@ -347,6 +363,7 @@ class PartitionedHashMap:
         res = self.local.find(rkeys)
         return self._result(self._backward(torch.as_tensor(res.indices), ctx), ctx)
 
+    @_on_device
     def erase(self, keys) -> torch.Tensor:
         keys = self._keys(keys)
         if self.peer is not None:
