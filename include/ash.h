@@ -293,6 +293,18 @@ int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, 
                   const int32_t* scratch, int64_t scratch_len, const int64_t* row_off,
                   void* const* peer_keys, const void* payload, int64_t payload_row_bytes,
                   void* const* peer_payload, int32_t* jdx, void* stream);
+/* ash_route_put with the row offsets taken on the device from the exchanged
+ * count matrix count_matrix[src * world + owner] (device int64, world x world):
+ * row_off[o] = sum over src < rank of count_matrix[src][o].  The put is
+ * launched before the host has read the matrix, so the host read overlaps
+ * it.  If any owner's total rows exceed recv_capacity (rows of each receive
+ * buffer) nothing is stored: every rank sees the same matrix and skips
+ * alike, and the caller grows the buffers and puts again. */
+int ash_route_put_counts(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int32_t rank,
+                         const uint8_t* owners, const int32_t* scratch, int64_t scratch_len,
+                         const int64_t* count_matrix, int64_t recv_capacity, void* const* peer_keys,
+                         const void* payload, int64_t payload_row_bytes, void* const* peer_payload,
+                         int32_t* jdx, void* stream);
 int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world,
                    const int64_t* row_off, const void* const* peer_ret, int32_t* out,
                    uint8_t* out_mask /* optional: out >= 0 */, void* stream);

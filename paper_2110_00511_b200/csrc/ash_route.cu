@@ -296,12 +296,36 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
                                                       uint32_t world, const uint8_t* __restrict__ owners,
                                                       const int32_t* __restrict__ off, int64_t n_tiles,
                                                       const uint8_t* __restrict__ pay, int64_t pay_rb, PeerArgs pa,
-                                                      int32_t* __restrict__ jdx) {
+                                                      int32_t* __restrict__ jdx, const int64_t* __restrict__ cmat,
+                                                      uint32_t rank, int64_t cap) {
   constexpr int kW = kBlock / 32;
   __shared__ int32_t s_pre[kItems][kW][kMaxWorld];
+  __shared__ int64_t s_off[kMaxWorld];
+  __shared__ int s_skip;
   const int warp = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < kItems * kW * kMaxWorld; e += kBlock) (&s_pre[0][0][0])[e] = 0;
+  if (threadIdx.x == 0) s_skip = 0;
   __syncthreads();
+  // row offsets: given, or from the exchanged count matrix cmat[src][owner]
+  // (rows of earlier sources at each owner); an owner whose rows would pass
+  // its receive capacity makes every rank skip the put (all see the same
+  // matrix), and the host re-puts after growing the buffers
+  for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
+    int64_t before = pa.row_off[o];
+    if (cmat) {
+      int64_t tot = 0;
+      before = 0;
+      for (uint32_t src = 0; src < world; ++src) {
+        const int64_t c = cmat[src * world + o];
+        if (src < rank) before += c;
+        tot += c;
+      }
+      if (tot > cap) s_skip = 1;
+    }
+    s_off[o] = before;
+  }
+  __syncthreads();
+  if (s_skip) return;
   const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
@@ -345,7 +369,7 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
       if (p >= n) continue;
       const uint32_t o = own[it];
       const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
-      const int64_t row = pa.row_off[o] + j;
+      const int64_t row = s_off[o] + j;
       jdx[p] = j;
       int32_t* kd = pa.keys[o] + row * 3;
 #pragma unroll
@@ -360,7 +384,7 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
     if (p >= n) continue;
     const uint32_t o = own[it];
     const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
-    const int64_t row = pa.row_off[o] + j;
+    const int64_t row = s_off[o] + j;
     jdx[p] = j;
     int32_t* kd = pa.keys[o] + row * arity;
     for (int d = 0; d < arity; ++d) kd[d] = __ldg(keys + p * arity + d);
@@ -498,13 +522,14 @@ int ash_route_count(const int32_t* keys, int64_t n, int32_t arity, int32_t world
   return rcheck("ash_route_count");
 }
 
-int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, const uint8_t* owners,
-                  const int32_t* scratch, int64_t scratch_len, const int64_t* row_off, void* const* peer_keys,
-                  const void* payload, int64_t payload_row_bytes, void* const* peer_payload, int32_t* jdx,
-                  void* stream) {
+static int route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, const uint8_t* owners,
+                     const int32_t* scratch, int64_t scratch_len, const int64_t* row_off, const int64_t* cmat,
+                     int32_t rank, int64_t cap, void* const* peer_keys, const void* payload,
+                     int64_t payload_row_bytes, void* const* peer_payload, int32_t* jdx, void* stream) {
   if (n < 0 || arity < 1 || world < 1 || world > kMaxWorld) return rfail("bad routing arguments");
   if (n == 0) return ASH_OK;
-  if (!keys || !owners || !scratch || !row_off || !peer_keys || !jdx) return rfail("null routing buffer");
+  if (!keys || !owners || !scratch || !(row_off || cmat) || !peer_keys || !jdx) return rfail("null routing buffer");
+  if (cmat && (rank < 0 || rank >= world || cap < 0)) return rfail("bad rank or receive capacity");
   if (payload_row_bytes < 0 || (payload_row_bytes && (!payload || !peer_payload)))
     return rfail("payload and peer payload buffers must both be given");
   const int64_t n_tiles = (n + kTile - 1) / kTile;
@@ -513,14 +538,34 @@ int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, 
   memset(&pa, 0, sizeof(pa));
   for (int o = 0; o < world; ++o) {
     if (!peer_keys[o]) return rfail("null peer key buffer");
-    pa.row_off[o] = row_off[o];
+    pa.row_off[o] = row_off ? row_off[o] : 0;
     pa.keys[o] = static_cast<int32_t*>(peer_keys[o]);
     pa.pay[o] = payload_row_bytes ? static_cast<uint8_t*>(peer_payload[o]) : nullptr;
   }
   k_route_put<<<static_cast<unsigned>(n_tiles), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
       keys, n, arity, static_cast<uint32_t>(world), owners, scratch, n_tiles,
-      static_cast<const uint8_t*>(payload), payload_row_bytes, pa, jdx); note_launch();
+      static_cast<const uint8_t*>(payload), payload_row_bytes, pa, jdx, cmat, static_cast<uint32_t>(rank),
+      cap); note_launch();
   return rcheck("ash_route_put");
+}
+
+int ash_route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t world, const uint8_t* owners,
+                  const int32_t* scratch, int64_t scratch_len, const int64_t* row_off, void* const* peer_keys,
+                  const void* payload, int64_t payload_row_bytes, void* const* peer_payload, int32_t* jdx,
+                  void* stream) {
+  if (!row_off) return rfail("null routing buffer");
+  return route_put(keys, n, arity, world, owners, scratch, scratch_len, row_off, nullptr, 0, 0, peer_keys,
+                   payload, payload_row_bytes, peer_payload, jdx, stream);
+}
+
+int ash_route_put_counts(const int32_t* keys, int64_t n, int32_t arity, int32_t world, int32_t rank,
+                         const uint8_t* owners, const int32_t* scratch, int64_t scratch_len,
+                         const int64_t* count_matrix, int64_t recv_capacity, void* const* peer_keys,
+                         const void* payload, int64_t payload_row_bytes, void* const* peer_payload, int32_t* jdx,
+                         void* stream) {
+  if (!count_matrix) return rfail("null count matrix");
+  return route_put(keys, n, arity, world, owners, scratch, scratch_len, nullptr, count_matrix, rank,
+                   recv_capacity, peer_keys, payload, payload_row_bytes, peer_payload, jdx, stream);
 }
 
 int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world, const int64_t* row_off,

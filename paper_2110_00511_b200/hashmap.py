@@ -602,10 +602,11 @@ class HashMap:
             res = self._insert_like(keys, None, association=True)
         return self._to_host(res) if host else res
 
-    def _insert_like(self, keys: torch.Tensor, vals, association: bool) -> BatchResult:
+    def _insert_like(self, keys: torch.Tensor, vals, association: bool, idx=None) -> BatchResult:
         m = keys.shape[0]
         dev = self._device
-        idx = torch.empty(m, dtype=torch.int32, device=dev)
+        if idx is None:
+            idx = torch.empty(m, dtype=torch.int32, device=dev)
         msk = torch.empty(m, dtype=torch.uint8, device=dev)
         if m == 0:
             return BatchResult(idx, msk.view(torch.bool))
@@ -685,6 +686,25 @@ class HashMap:
         srt = torch.sort(losers).values  # the sorted free of index_heap.py:46
         call("ash_heap_put_losers", self._ptr(), srt.data_ptr(), m, self._stream())
         self._top_ub = min(self._capacity, self._top_ub + m)
+
+    @on_device
+    def _op_into(self, op: str, keys: torch.Tensor, vals, out_idx: torch.Tensor) -> None:
+        """insert / activate / find of a CUDA batch (already checked) with the
+        indices written straight into out_idx, e.g. a view of the peer
+        transport's result buffer (no copy); masks are derived by the caller
+        (index >= 0)."""
+        m = keys.shape[0]
+        if op == "find":
+            with self._guard.reading():
+                if m:
+                    msk = torch.empty(m, dtype=torch.uint8, device=self._device)
+                    call("ash_find", self._ptr(), keys.data_ptr(), m, out_idx.data_ptr(),
+                         msk.data_ptr(), self._stream())
+            return
+        if op not in ("insert", "activate"):
+            raise ValueError(f"unknown op {op!r}")
+        with self._guard.writing():
+            self._insert_like(keys, vals if op == "insert" else None, op == "activate", idx=out_idx)
 
     @on_device
     def find(self, keys) -> BatchResult:

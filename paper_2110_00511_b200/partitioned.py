@@ -135,6 +135,7 @@ class PeerExchange:
             shape, dt = payload
             self.pay_rb = int(np.prod(shape)) * torch.empty(0, dtype=dt).element_size()
         self._scratch = torch.empty(0, dtype=torch.int32, device=device)
+        self._mat_h = self._mat_ev = None
         self.capacity = 0
         self._alloc(capacity)
 
@@ -189,6 +190,13 @@ class PeerExchange:
         owners = torch.empty(n, dtype=torch.uint8, device=self.device)
         lib.call("ash_route_count", keys.data_ptr(), n, self.arity, self.world, counts.data_ptr(),
                  owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), self._stream())
+        jdx = torch.empty(n, dtype=torch.int32, device=self.device)
+        rb = self.pay_rb if (payload is not None and n) else 0
+        if rb:
+            payload = payload.contiguous()
+        def pay_args():  # evaluated per put: a grow replaces the peer buffers
+            return (payload.data_ptr() if rb else None, rb, self._p_pay if rb else None)
+        put_done = False
         if dist.get_backend(self.group) == "gloo":  # CPU control plane (tests: ranks sharing a GPU)
             parts = [torch.empty(self.world, dtype=torch.int64) for _ in range(self.world)]
             dist.all_gather(parts, counts.cpu(), group=self.group)
@@ -196,21 +204,32 @@ class PeerExchange:
         else:
             mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
             dist.all_gather_into_tensor(mat, counts, group=self.group)
-            C = mat.cpu()  # C[src][owner]; the one host read of the op
+            # the put takes its row offsets from the matrix on the device, so
+            # it runs while the host reads the matrix (the one host read of the op)
+            if self._mat_h is None or self._mat_h.shape[0] != self.world:
+                self._mat_h = torch.empty((self.world, self.world), dtype=torch.int64, pin_memory=True)
+                self._mat_ev = torch.cuda.Event()
+            self._mat_h.copy_(mat, non_blocking=True)
+            self._mat_ev.record(torch.cuda.current_stream(self.device))
+            lib.call("ash_route_put_counts", keys.data_ptr(), n, self.arity, self.world, self.rank,
+                     owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), mat.data_ptr(),
+                     self.capacity, self._p_keys, *pay_args(), jdx.data_ptr(), self._stream())
+            self._mat_ev.synchronize()
+            C = self._mat_h.clone()
+            put_done = int(C.sum(0).max()) <= self.capacity  # else the kernel stored nothing
         row_off = torch.cumsum(C, 0) - C  # rows of earlier sources at every owner
         m = int(C[:, self.rank].sum())
         peak = int(C.sum(0).max())
         if peak > self.capacity:  # every rank sees the same C: grow together
+            # (the skipped put may still be in flight: drain before the old
+            # buffers are released)
+            torch.cuda.current_stream(self.device).synchronize()
             self._alloc(int(peak * 1.25))
         offs = (lib.ctypes.c_int64 * self.world)(*row_off[self.rank].tolist())
-        jdx = torch.empty(n, dtype=torch.int32, device=self.device)
-        rb = self.pay_rb if (payload is not None and n) else 0
-        if rb:
-            payload = payload.contiguous()
-        lib.call("ash_route_put", keys.data_ptr(), n, self.arity, self.world, owners.data_ptr(),
-                 self._scratch.data_ptr(), self._scratch.numel(), offs, self._p_keys,
-                 payload.data_ptr() if rb else None, rb, self._p_pay if rb else None,
-                 jdx.data_ptr(), self._stream())
+        if not put_done:
+            lib.call("ash_route_put", keys.data_ptr(), n, self.arity, self.world, owners.data_ptr(),
+                     self._scratch.data_ptr(), self._scratch.numel(), offs, self._p_keys, *pay_args(),
+                     jdx.data_ptr(), self._stream())
         self._barrier()  # every source's rows have landed
         rkeys = self.recv_keys[:m * self.arity].view(m, self.arity)
         rpay = None
@@ -219,11 +238,12 @@ class PeerExchange:
             rpay = self.recv_pay[:m * self.pay_rb].view(dt).view(m, *shape)
         return rkeys, rpay, (n, owners, jdx, offs)
 
-    def combine(self, local_idx: torch.Tensor, ctx) -> torch.Tensor:
+    def combine(self, local_idx, ctx) -> torch.Tensor:
+        """local_idx: this owner's results, or None when the shard op wrote
+        them into ``self.ret`` itself."""
         n, owners, jdx, offs = ctx
-        m = local_idx.shape[0]
-        if m:
-            self.ret[:m].copy_(local_idx.reshape(-1))
+        if local_idx is not None and local_idx.shape[0]:
+            self.ret[:local_idx.shape[0]].copy_(local_idx.reshape(-1))
         self._barrier()  # every owner's results are in place
         out = torch.empty(n, dtype=torch.int32, device=self.device)
         msk = torch.empty(n, dtype=torch.uint8, device=self.device)
@@ -324,7 +344,24 @@ class PartitionedHashMap:
 
     def _peer_op(self, op: str, keys, vals=()):
         """One batch op over the peer transport (PeerExchange)."""
+        if op == "insert":
+            # checked before the collective starts: every rank fails alike
+            specs = getattr(self.local, "value_specs", ())
+            if len(vals) != len(specs):
+                raise ValueError(f"expected {len(specs)} value batches, got {len(vals)}")
+            if vals:  # the put moves raw rows: the map's dtype and row size
+                v = vals[0].to(self.local._torch_dtypes[0])
+                if v.numel() != keys.shape[0] * int(np.prod(specs[0].shape)):
+                    raise ValueError(f"value batch has shape {tuple(vals[0].shape)}, expected "
+                                     f"({keys.shape[0]}, {', '.join(map(str, specs[0].shape))})")
+                vals = [v]
         rkeys, rpay, ctx = self.peer.dispatch(keys, vals[0] if vals else None)
+        if op != "erase" and hasattr(self.local, "_op_into"):
+            # the shard op writes its indices straight into the result buffer
+            self.local._op_into(op, rkeys, [rpay] if rpay is not None else [],
+                                self.peer.ret[:rkeys.shape[0]])
+            out, msk = self.peer.combine(None, ctx)
+            return PartitionedResult(out, msk, ctx[1])
         if op == "insert":
             res = self.local.insert(rkeys, *([rpay] if rpay is not None else []))
         elif op == "erase":

@@ -152,3 +152,49 @@ def test_partitioned_world1_peer_transport(cuda_ok):
         assert pm.local.value_buffer(0).cpu().numpy().tobytes() == om.value_buffer(0).tobytes()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rank", [(1, 0), (3, 1), (8, 7)])
+def test_peer_put_with_device_count_matrix(cuda_ok, world, rank):
+    """ash_route_put_counts: row offsets from the exchanged count matrix on
+    the device (rows of earlier sources at each owner); when some owner's
+    total passes the receive capacity nothing is stored."""
+    from paper_2110_00511_b200 import _lib
+    n = 100_003
+    rng = np.random.default_rng(world * 10 + rank)
+    k = rng.integers(-2 ** 31, 2 ** 31, size=(n, 3)).astype(np.int32)
+    pay = rng.integers(0, 2 ** 31, size=(n, 1)).astype(np.int32)
+    own = owner_of_np(k, world)
+    cnt = np.bincount(own, minlength=world)
+    C = rng.integers(0, 5000, size=(world, world)).astype(np.int64)
+    C[rank] = cnt
+    before = C[:rank].sum(0)
+    tot = C.sum(0)
+    dev = torch.device("cuda")
+    kt, pt = torch.from_numpy(k).to(dev), torch.from_numpy(pay).to(dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    owners = torch.empty(n, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(int(_lib.lib.ash_route_scratch_len(n, world)), dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("ash_route_count", kt.data_ptr(), n, 3, world, counts.data_ptr(), owners.data_ptr(),
+              scratch.data_ptr(), scratch.numel(), st)
+    cap = int(tot.max())
+    P = _lib.c_void_p * world
+    mat = torch.from_numpy(C).to(dev)
+    for capacity, stored in ((cap, True), (cap - 1, False)):
+        bufk = [torch.full((cap, 3), -7, dtype=torch.int32, device=dev) for _ in range(world)]
+        bufp = [torch.full((cap, 1), -7, dtype=torch.int32, device=dev) for _ in range(world)]
+        jdx = torch.empty(n, dtype=torch.int32, device=dev)
+        _lib.call("ash_route_put_counts", kt.data_ptr(), n, 3, world, rank, owners.data_ptr(),
+                  scratch.data_ptr(), scratch.numel(), mat.data_ptr(), capacity,
+                  P(*[b.data_ptr() for b in bufk]), pt.data_ptr(), 4, P(*[b.data_ptr() for b in bufp]),
+                  jdx.data_ptr(), st)
+        for o in range(world):
+            got, gp = bufk[o].cpu().numpy(), bufp[o].cpu().numpy()
+            if not stored:
+                assert np.all(got == -7) and np.all(gp == -7)
+                continue
+            sel = own == o
+            a, b = int(before[o]), int(before[o] + cnt[o])
+            assert np.array_equal(got[a:b], k[sel]) and np.array_equal(gp[a:b], pay[sel])
+            assert np.all(got[:a] == -7) and np.all(got[b:] == -7)

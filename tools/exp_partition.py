@@ -1,6 +1,9 @@
-"""Phase breakdown of the hash-partitioned insert/find at N=1 (GPU box):
-route plan, count exchange (+ host read of the split sizes), key/value
-all-to-all, shard op, result all-to-all, un-permute."""
+"""Phase breakdown of the hash-partitioned insert/find at N=1 (GPU box).
+NCCL transport: route plan, count exchange (+ host read of the split sizes),
+key/value all-to-all, shard op, result all-to-all, un-permute.  Peer
+transport (``peer`` argument): dispatch (owner count, count exchange, put
+overlapping the host read of the counts, barrier), shard op writing into the
+result buffer, combine (barrier, pull, barrier)."""
 import os, socket, sys, time
 sys.path.insert(0, ".")
 import numpy as np
@@ -19,7 +22,9 @@ from paper_2110_00511_b200.workloads import int3_batch
 N = 10_000_000
 keys = torch.from_numpy(int3_batch(N, 0.5, seed=1000)).to(dev)
 vals = torch.rand((N, 1), device=dev)
-pm = PartitionedHashMap(int(N * 1.05), 3, [np.float32], device=dev)
+PEER = "peer" in sys.argv[1:]
+pm = PartitionedHashMap(int(N * 1.05), 3, [np.float32], device=dev,
+                        transport="peer" if PEER else "nccl")
 st = torch.cuda.current_stream()
 marks = []
 
@@ -57,8 +62,28 @@ def run():
     torch.cuda.synchronize()
 
 
+def run_peer():
+    marks.clear()
+    pm.local.clear()
+    torch.cuda.synchronize()
+    mark("start")
+    rk, rv, ctx = pm.peer.dispatch(keys, vals)
+    mark("dispatch")
+    pm.local._op_into("insert", rk, [rv], pm.peer.ret[:rk.shape[0]])
+    mark("shard insert")
+    pm.peer.combine(None, ctx)
+    mark("combine")
+    rk, _, ctx = pm.peer.dispatch(keys)
+    mark("dispatch")
+    pm.local._op_into("find", rk, [], pm.peer.ret[:rk.shape[0]])
+    mark("shard find")
+    pm.peer.combine(None, ctx)
+    mark("combine")
+    torch.cuda.synchronize()
+
+
 for i in range(5):
-    run()
+    (run_peer if PEER else run)()
 t = [(n, marks[0][1].elapsed_time(e), 1e3 * (w - marks[0][2])) for n, e, w in marks]
 prev = 0
 for n, g, h in t[1:]:
