@@ -18,6 +18,7 @@
 #include <atomic>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/ash.h"
@@ -1343,6 +1344,7 @@ __global__ void __launch_bounds__(kCommitThreads)
 // touched the heap above top), the rank from the per-32-position winner bits
 // and prefixes the commit wrote to rank_words (2.5 MB at 10M positions, L2
 // resident); without rank_words, the index the commit wrote to tmp[pos].
+template <int U>  // buckets per thread per round; all loads of a round issued together
 __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t* __restrict__ tmp,
                                                          const int32_t* __restrict__ rank_words,
                                                          const int32_t* __restrict__ heap,
@@ -1352,7 +1354,6 @@ __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t*
   const uint32_t top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
   // fresh heap region (no frees at or above top): index = top + rank
   const bool ident = ld_volatile_i32(counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(top);
-  constexpr int U = 2;  // buckets per thread per round; all loads of a round issued together
   for (uint32_t b0 = blockIdx.x * kBlock + threadIdx.x; b0 < t.n_buckets; b0 += U * stride) {
     uint32_t w[U][8];
 #pragma unroll
@@ -1900,7 +1901,10 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
   const int sms = device_sms();
   unsigned g = grid_for(t.n_buckets, kBlock);
   const unsigned cap = static_cast<unsigned>(sms) * 8;
-  k_commit_sweep<<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min); note_launch();
+  // one bucket per thread per round: U = 2 / 4 measured 1% / 6% slower
+  // (tools/ab_sweep_u.sh history; DRAM read/write mix, not latency, bounds it)
+  k_commit_sweep<1><<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min);
+  note_launch();
 }
 
 template <int A, int VW>
