@@ -1902,7 +1902,7 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
   unsigned g = grid_for(t.n_buckets, kBlock);
   const unsigned cap = static_cast<unsigned>(sms) * 8;
   // one bucket per thread per round: U = 2 / 4 measured 1% / 6% slower
-  // (tools/ab_sweep_u.sh history; DRAM read/write mix, not latency, bounds it)
+  // (bench A/B in r01l: the DRAM read/write mix, not load latency, bounds it)
   k_commit_sweep<1><<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min);
   note_launch();
 }
