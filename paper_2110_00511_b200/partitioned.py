@@ -13,6 +13,11 @@ batch.  A batch op:
   4. owner-local indices travel back (``-1`` encodes a False mask, so one
      int32 per key suffices) and are scattered to the original positions.
 
+That is the ``transport="nccl"`` path.  ``transport="peer"`` (``PeerExchange``,
+the bench default) replaces steps 2 and 4 with stores into / loads from the
+owners' receive and result buffers over NVLink peer memory; the N x N count
+exchange is its only collective.
+
 A global buffer index is the pair ``(owner rank, local index)``; results
 carry the owner of every key.  Capacity and auto-rehash are per shard.
 """
