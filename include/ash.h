@@ -59,7 +59,7 @@ extern "C" {
  */
 typedef struct ash_map {
   void* slots;              /* n_slots x 16 B                                  */
-  int64_t n_slots;          /* power of two, 64 <= n_slots <= 2^30             */
+  int64_t n_slots;          /* even, 64 <= n_slots <= 2^30                     */
   int32_t* key_buf;         /* capacity x arity int32  (hashmap.py:203)        */
   int32_t arity;            /* >= 1                                            */
   int32_t n_values;         /* number of value buffers, <= 8                   */

@@ -56,3 +56,22 @@ def test_no_oracle_import_in_product():
     pkg = ROOT / "paper_2110_00511_b200"
     for f in pkg.rglob("*.py"):
         assert "oracle" not in f.read_text().replace("oracle/", ""), f"{f} references the oracle"
+
+
+def build_c_client(out_dir: Path) -> Path:
+    """Compile tests/c_abi/ash_c_client.c (a plain C caller of ash.h) against
+    libash.so and the CUDA runtime; warnings are errors."""
+    cuda = Path("/usr/local/cuda")
+    lib_dir = ROOT / "paper_2110_00511_b200" / "lib"
+    exe = out_dir / "ash_c_client"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", str(ROOT / "include"),
+                    "-I", str(cuda / "include"), str(ROOT / "tests" / "c_abi" / "ash_c_client.c"),
+                    "-L", str(lib_dir), "-lash", "-L", str(cuda / "lib64"), "-lcudart",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_plain_c_client_compiles_and_links(tmp_path):
+    """The header is plain C and a C caller links against the exports (the
+    client itself runs in tests/test_c_abi_gpu.py)."""
+    assert build_c_client(tmp_path).exists()
