@@ -35,6 +35,7 @@ __global__ void k_probe(const uint4* __restrict__ tab, uint32_t n_buckets, int64
   if (MODE == 5) { LD4("ld.global.cg.v4.u32", p, 0); LD4("ld.global.cg.v4.u32", p + 1, 4); }
   if (MODE == 6) LD4("ld.global.cg.v4.u32", p, 0);
   if (MODE == 7) LD8("ld.global.cv.v8.u32");
+  if (MODE == 8) LD8("ld.global.nc.L1::no_allocate.L2::64B.v8.u32");
   out[i] = r[0] ^ r[3] ^ r[4] ^ r[7];
 }
 
@@ -42,6 +43,13 @@ int main(int argc, char** argv) {
   // table size in MB (default 240; e.g. 9600 for the configs[4] table)
   const uint32_t n_buckets = (argc > 1 ? (uint32_t)(atof(argv[1]) * 1e6 / 32) : 7500000u);
   printf("table %.0f MB\n", n_buckets * 32.0 / 1e6);
+  // optional second argument: cudaLimitMaxL2FetchGranularity in bytes
+  if (argc > 2) {
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[2]));
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity limit %zu\n", v);
+  }
   const int64_t n = 10000000;
   uint4* tab; uint32_t* out;
   cudaMalloc(&tab, (size_t)n_buckets * 32);
@@ -50,8 +58,8 @@ int main(int argc, char** argv) {
   void* flush; size_t fb = size_t(256) << 20; cudaMalloc(&flush, fb);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const char* names[] = {"nc.L1::no_allocate.v8", "cg.v8", "v8 (ca)", "relaxed.gpu.v8", "nc.v4 x2", "cg.v4 x2",
-                         "cg.v4 (16B only)", "cv.v8"};
-  for (int mode = 0; mode < 8; ++mode) {
+                         "cg.v4 (16B only)", "cv.v8", "nc.L2::64B.v8"};
+  for (int mode = 0; mode < 9; ++mode) {
     float best = 1e9;
     for (int rep = 0; rep < 5; ++rep) {
       cudaMemsetAsync(flush, rep, fb);
@@ -66,6 +74,7 @@ int main(int argc, char** argv) {
         case 5: k_probe<5><<<g, 256>>>(tab, n_buckets, n, 77 + rep, out); break;
         case 6: k_probe<6><<<g, 256>>>(tab, n_buckets, n, 77 + rep, out); break;
         case 7: k_probe<7><<<g, 256>>>(tab, n_buckets, n, 77 + rep, out); break;
+        case 8: k_probe<8><<<g, 256>>>(tab, n_buckets, n, 77 + rep, out); break;
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
