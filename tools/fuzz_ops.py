@@ -1,3 +1,6 @@
+"""Randomized op streams (random capacity, arity, value specs, backend) on
+the CUDA map against the oracle, exact (GPU box):
+    python tools/fuzz_ops.py FIRST_SEED END_SEED"""
 import sys, os
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import numpy as np

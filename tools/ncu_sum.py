@@ -1,3 +1,5 @@
+"""Per-kernel totals of an ncu gpu__time_duration launch list (CSV):
+    python tools/ncu_sum.py gpurun_out/launches.csv"""
 import csv, sys
 from collections import defaultdict
 rows = list(csv.reader(open(sys.argv[1])))
