@@ -521,12 +521,12 @@ __global__ void k_fill_empty(uint4* slots, int64_t n_slots) {
 // ---------------------------------------------------------------------------
 // kernels: find
 
-template <int A>
-__global__ void __launch_bounds__(kBlock) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
-                                                 int32_t* __restrict__ out_idx,
-                                                 uint8_t* __restrict__ out_mask) {
-  __shared__ uint32_t stage[kBlock * 3];
-  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+template <int A, int B = kBlock>
+__global__ void __launch_bounds__(B) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
+                                            int32_t* __restrict__ out_idx,
+                                            uint8_t* __restrict__ out_mask) {
+  __shared__ uint32_t stage[B * 3];
+  const int64_t p = blockIdx.x * static_cast<int64_t>(B) + threadIdx.x;
   const uint64_t pol = stream_policy(t.hints);
   Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, pol);
   if (p >= n) return;
@@ -622,15 +622,16 @@ __device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint3
 // rounds are issued together: R home-bucket loads, then R 128-bit CASes, so
 // a warp keeps 2R memory round trips in flight instead of 2 serial ones.
 constexpr int kClaimRounds = 1;
+constexpr int kClaimBlock = 128;
 
-template <int A>
-__global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
+template <int A, int B = kBlock>
+__global__ void __launch_bounds__(B) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
                                                   int32_t* counters, int32_t* tile_cnt) {
   constexpr int R = kClaimRounds;
-  __shared__ uint32_t stage[R][kBlock * 3];
+  __shared__ uint32_t stage[R][B * 3];
   const int lane = threadIdx.x & 31;
-  const int64_t blk = blockIdx.x * static_cast<int64_t>(kBlock * R);
+  const int64_t blk = blockIdx.x * static_cast<int64_t>(B * R);
   const uint64_t pol = stream_policy(t.hints);
   Key<A> k[R];
   uint32_t h[R], res[R];
@@ -639,13 +640,13 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
   bool lead[R], cand[R], tomb[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t p = blk + r * kBlock + threadIdx.x;
+    const int64_t p = blk + r * B + threadIdx.x;
     live[r] = __ballot_sync(0xFFFFFFFFu, p < n);
     k[r] = load_key_warp<A>(keys, p, n, t.arity, stage[r], pol);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t p = blk + r * kBlock + threadIdx.x;
+    const int64_t p = blk + r * B + threadIdx.x;
     lead[r] = false;
     cand[r] = tomb[r] = false;
     res[r] = 0;
@@ -682,14 +683,14 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
   for (int r = 0; r < R; ++r) {
     state[r] = kFastDone;
     if (lead[r])
-      state[r] = claim_fast<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * kBlock + threadIdx.x), w[r], keys,
+      state[r] = claim_fast<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * B + threadIdx.x), w[r], keys,
                                mask, tile_cnt, &res[r], &cand[r], &cas_slot[r], &cas_expect[r]);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     cas_ok[r] = false;
     if (state[r] == kFastCas) {
-      const uint32_t j = static_cast<uint32_t>(blk + r * kBlock + threadIdx.x);
+      const uint32_t j = static_cast<uint32_t>(blk + r * B + threadIdx.x);
       cas_ok[r] = cas128(t.slots + cas_slot[r], cas_expect[r], slot_value<A>(k[r], PEND | j));
     }
   }
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
       cand[r] = true;
       tomb[r] = cas_expect[r].w == TOMB;
     } else if (state[r] != kFastDone) {
-      res[r] = probe_claim<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * kBlock + threadIdx.x), keys, mask,
+      res[r] = probe_claim<A>(t, k[r], h[r], static_cast<uint32_t>(blk + r * B + threadIdx.x), keys, mask,
                               counters, tile_cnt, &tomb[r], &cand[r]);
     }
   }
@@ -709,7 +710,7 @@ __global__ void __launch_bounds__(kBlock) k_claim(Table t, const int32_t* __rest
   int32_t cand_total = 0, tomb_total = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t p = blk + r * kBlock + threadIdx.x;
+    const int64_t p = blk + r * B + threadIdx.x;
     if (p >= n) continue;
     __syncwarp(live[r]);
     const uint32_t lres = __shfl_sync(live[r], res[r], leader[r]);
@@ -2041,6 +2042,7 @@ int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uin
   if (!keys || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
   Table t = make_table(m);
   cudaStream_t s = as_stream(stream);
+  // 256-thread blocks (128 within 1%, 512 1-4% slower; r01m A/B)
   ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask)));
   return check_launch("ash_find");
 }
@@ -2070,7 +2072,9 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   cudaStream_t s = as_stream(stream);
   if (int rc = check_tiles(m, n)) return rc;
   cudaMemsetAsync(out_mask, 0, n, s);
-  ASH_DISPATCH_ARITY(m->arity, (k_claim<A><<<grid_for(n, kBlock * kClaimRounds), kBlock, 0, s>>>(
+  // 128-thread blocks: 0.302 ms against 0.310 at 256 and 0.330 at 512 (C2,
+  // r01m A/B; 64 ties with 128): finer block turnover over the ~66 waves
+  ASH_DISPATCH_ARITY(m->arity, (k_claim<A, kClaimBlock><<<grid_for(n, kClaimBlock * kClaimRounds), kClaimBlock, 0, s>>>(
                                    t, keys, n, out_idx, out_mask, m->counters, m->tile_counts)));
   return check_launch("ash_insert_claim");
 }
