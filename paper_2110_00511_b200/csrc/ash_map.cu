@@ -1686,15 +1686,15 @@ struct FrameSrc {
   }
 };
 
-template <typename Src>
-__global__ void __launch_bounds__(kBlock) k_voxel_claim(Table t, Src src, int64_t n, int32_t* __restrict__ tmp,
-                                                        uint8_t* __restrict__ mask, int32_t* counters,
-                                                        int32_t* tile_cnt) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+template <typename Src, int B = kBlock>
+__global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, int32_t* __restrict__ tmp,
+                                                   uint8_t* __restrict__ mask, int32_t* counters,
+                                                   int32_t* tile_cnt) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(B) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool inside = p < n;
   const unsigned live = __ballot_sync(0xFFFFFFFFu, inside);
-  __shared__ uint4 stage[Src::kStaged ? kBlock * Src::kRowBytes / 16 : 1];
+  __shared__ uint4 stage[Src::kStaged ? B * Src::kRowBytes / 16 : 1];
   bool bad = false;
   Key<3> k;
   k.row = nullptr;
@@ -1904,6 +1904,7 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
   const unsigned cap = static_cast<unsigned>(sms) * 8;
   // one bucket per thread per round: U = 2 / 4 measured 1% / 6% slower
   // (bench A/B in r01l: the DRAM read/write mix, not load latency, bounds it)
+  // 8 CTAs per SM (4 and 16 measured 5% slower, r01m)
   k_commit_sweep<1><<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min);
   note_launch();
 }
@@ -1945,8 +1946,10 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
 template <typename Src>
 void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
                       int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s) {
-  k_voxel_claim<Src><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, src, n, scratch_idx, scratch_mask, ws->counters,
-                                                            ws->tile_counts); note_launch();
+  // 128-thread blocks: configs[2] 0.501 ms against 0.513 at 256 (r01m A/B)
+  k_voxel_claim<Src, 128><<<grid_for(n, 128), 128, 0, s>>>(t, src, n, scratch_idx, scratch_mask, ws->counters,
+                                                           ws->tile_counts);
+  note_launch();
   launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
   k_voxel_select<Src><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask, out_coords,
                                                              out_sel, ws->tile_counts); note_launch();
