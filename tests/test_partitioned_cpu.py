@@ -114,7 +114,7 @@ def _worker(rank, world, port, keys_all, vals_all, find_all, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_partitioned_matches_single_map(world):
     rng = np.random.default_rng(5)
     pool = rng.integers(-50, 50, size=(3000, 3)).astype(np.int32)
@@ -159,7 +159,7 @@ def test_partitioned_matches_single_map(world):
     assert np.array_equal(got[fnd], want[fnd])
     # shard sizes sum to the single-map size (size is collective)
     assert sum(out[r][8] for r in range(world)) == ref.size
-    assert out[0][9] == out[1][9] == ref.size
+    assert all(out[r][9] == ref.size for r in range(world))
 
 
 def test_owner_hash_balanced():
