@@ -1740,25 +1740,51 @@ __global__ void __launch_bounds__(kBlock)
     k_voxel_select(uint4* slots, Src src, int64_t n, const int32_t* __restrict__ tmp,
                    const uint8_t* __restrict__ mask, int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel,
                    int32_t* tile_pre) {
-  __shared__ ScanSmem sm;
+  __shared__ int32_t s_warp[kWarps];
+  __shared__ int32_t s_prefix;
   const int64_t tile = blockIdx.x, base = tile * kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // On the all-EMPTY workspace every position leaves the claim PENDING
   // (tmp < 0) and every non-winner DEMOTED, so the winners are exactly the
-  // un-demoted positions: only the 1-byte masks are streamed here, and the
-  // claim's slot words are read for the winners alone (3.5% at configs[2]).
-  bool win[kItems];
+  // un-demoted positions: only the 1-byte masks are streamed here (8
+  // consecutive ones per thread, one 8-byte load), and the claim's slot
+  // words are read for the winners alone (3.5% at configs[2]).
+  const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * kItems;
+  uint32_t bits = 0;
+  static_assert(kItems == 8, "one 8-byte mask load per thread");
+  if (p0 + kItems <= n && (reinterpret_cast<uintptr_t>(mask) & 7) == 0) {
+    const uint2 m8 = __ldg(reinterpret_cast<const uint2*>(mask + p0));
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int64_t p = base + it * kBlock + threadIdx.x;
-    win[it] = p < n && !(__ldg(mask + p) & DEMOTED);
+    for (int j = 0; j < 4; ++j) {
+      if (!((m8.x >> (8 * j)) & DEMOTED)) bits |= 1u << j;
+      if (!((m8.y >> (8 * j)) & DEMOTED)) bits |= 1u << (j + 4);
+    }
+  } else {
+    for (int j = 0; j < kItems; ++j)
+      if (p0 + j < n && !(__ldg(mask + p0 + j) & DEMOTED)) bits |= 1u << j;
   }
-  uint32_t bal[kItems];
-  tile_scan_known(win, bal, sm, tile_pre, tile, nullptr);
+  // block exclusive scan of the per-thread winner counts (thread order =
+  // position order), plus the tile's prefix from the tile scan
+  const int32_t cnt = __popc(bits);
+  int32_t incl = cnt;
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    if (!win[it]) continue;
-    const int64_t p = base + it * kBlock + threadIdx.x;
-    const uint32_t r = item_rank(sm, bal, it);
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  if (threadIdx.x == 0) {
+    s_prefix = tile_pre[tile];
+    tile_pre[tile] = 0;  // the counts are zero between calls
+  }
+  __syncthreads();
+  int32_t before = s_prefix + incl - cnt;
+  for (int w = 0; w < warp; ++w) before += s_warp[w];
+  while (bits) {
+    const int j = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const int64_t p = p0 + j;
+    const uint32_t r = static_cast<uint32_t>(before++);
     // the winner's key words are in its claimed slot (L2-hot: the workspace
     // is sized to stay resident), no need to regenerate them from the source
     const uint32_t slot = static_cast<uint32_t>(__ldg(tmp + p)) & SLOT_MASK;
