@@ -1727,10 +1727,12 @@ __global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, 
   __syncwarp(live);
   const unsigned cand = __ballot_sync(live, candidate);
   if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
+  // the select reads tmp (the claimed slot) for winners only, and only a
+  // candidate can win: everything else is DEMOTED (by probe_claim for
+  // leaders that lost, here for in-warp duplicates and skipped positions)
   if (lane == leader && !skip) {
-    tmp[p] = static_cast<int32_t>(res);
+    if (candidate) tmp[p] = static_cast<int32_t>(res);
   } else {
-    tmp[p] = static_cast<int32_t>(PEND);
     mask[p] = DEMOTED;
   }
 }
