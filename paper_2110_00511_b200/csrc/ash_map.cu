@@ -1737,6 +1737,8 @@ __global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, 
   }
 }
 
+constexpr int kSelTiles = 32 * kBlock / kTile;  // scan tiles per select block (32 positions per thread)
+
 template <typename Src>
 __global__ void __launch_bounds__(kBlock)
     k_voxel_select(uint4* slots, Src src, int64_t n, const int32_t* __restrict__ tmp,
@@ -1744,29 +1746,34 @@ __global__ void __launch_bounds__(kBlock)
                    int32_t* tile_pre) {
   __shared__ int32_t s_warp[kWarps];
   __shared__ int32_t s_prefix;
-  const int64_t tile = blockIdx.x, base = tile * kTile;
+  // one block per kSelTiles scan tiles; 32 consecutive positions per thread
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kSelTiles, base = tile0 * kTile;
+  const int64_t n_tiles = (n + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // On the all-EMPTY workspace every position leaves the claim PENDING
   // (tmp < 0) and every non-winner DEMOTED, so the winners are exactly the
-  // un-demoted positions: only the 1-byte masks are streamed here (8
-  // consecutive ones per thread, one 8-byte load), and the claim's slot
-  // words are read for the winners alone (3.5% at configs[2]).
-  const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * kItems;
+  // un-demoted positions: only the 1-byte masks are streamed here (four
+  // independent 8-byte loads per thread), and the claim's slot words are
+  // read for the winners alone (3.5% at configs[2]).
+  const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * 32;
   uint32_t bits = 0;
-  static_assert(kItems == 8, "one 8-byte mask load per thread");
-  if (p0 + kItems <= n && (reinterpret_cast<uintptr_t>(mask) & 7) == 0) {
-    const uint2 m8 = __ldg(reinterpret_cast<const uint2*>(mask + p0));
+  if (p0 + 32 <= n && (reinterpret_cast<uintptr_t>(mask) & 7) == 0) {
+    uint2 m8[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!((m8.x >> (8 * j)) & DEMOTED)) bits |= 1u << j;
-      if (!((m8.y >> (8 * j)) & DEMOTED)) bits |= 1u << (j + 4);
-    }
+    for (int q = 0; q < 4; ++q) m8[q] = __ldg(reinterpret_cast<const uint2*>(mask + p0) + q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((m8[q].x >> (8 * j)) & DEMOTED)) bits |= 1u << (8 * q + j);
+        if (!((m8[q].y >> (8 * j)) & DEMOTED)) bits |= 1u << (8 * q + j + 4);
+      }
   } else {
-    for (int j = 0; j < kItems; ++j)
+    for (int j = 0; j < 32; ++j)
       if (p0 + j < n && !(__ldg(mask + p0 + j) & DEMOTED)) bits |= 1u << j;
   }
   // block exclusive scan of the per-thread winner counts (thread order =
-  // position order), plus the tile's prefix from the tile scan
+  // position order), plus the first tile's prefix from the tile scan
   const int32_t cnt = __popc(bits);
   int32_t incl = cnt;
 #pragma unroll
@@ -1775,11 +1782,10 @@ __global__ void __launch_bounds__(kBlock)
     if (lane >= o) incl += y;
   }
   if (lane == 31) s_warp[warp] = incl;
-  if (threadIdx.x == 0) {
-    s_prefix = tile_pre[tile];
-    tile_pre[tile] = 0;  // the counts are zero between calls
-  }
+  if (threadIdx.x == 0) s_prefix = tile_pre[tile0];
   __syncthreads();
+  // the counts are zero between calls (every prefix of this block is read)
+  if (threadIdx.x < kSelTiles && tile0 + threadIdx.x < n_tiles) tile_pre[tile0 + threadIdx.x] = 0;
   int32_t before = s_prefix + incl - cnt;
   for (int w = 0; w < warp; ++w) before += s_warp[w];
   while (bits) {
@@ -1978,8 +1984,9 @@ void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, 
                                                            ws->tile_counts);
   note_launch();
   launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
-  k_voxel_select<Src><<<grid_for(n, kTile), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask, out_coords,
-                                                             out_sel, ws->tile_counts); note_launch();
+  k_voxel_select<Src><<<grid_for(n, kTile * kSelTiles), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask,
+                                                                         out_coords, out_sel, ws->tile_counts);
+  note_launch();
 }
 
 int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t width, const double* cam,
