@@ -1709,16 +1709,31 @@ __global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, 
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
   const bool skip = bad || !has;  // out-of-range points never claim; the host raises first
   const uint32_t h = hash_key<3>(k, 3);
-  unsigned grp = __match_any_sync(live, h);
-  if (__any_sync(live, __popc(grp) > 1)) {
-    unsigned g2;
-    same_key_in_warp<3>(k, live, &g2);
-    grp &= g2;
+  int leader;
+  if (Src::kStaged) {
+    // point clouds: equal keys are grouped only where they are adjacent in
+    // the batch (a run of points in one voxel: 3 shuffles + a ballot);
+    // __match_any_sync kept this kernel ADU-bound (303 -> ~240 us without
+    // it at configs[2]), and duplicates elsewhere resolve in the table
+    // exactly as they do across warps
+    const uint32_t u0 = __shfl_up_sync(live, k.w[0], 1), u1 = __shfl_up_sync(live, k.w[1], 1),
+                   u2 = __shfl_up_sync(live, k.w[2], 1);
+    const bool skip_prev = __shfl_up_sync(live, static_cast<int>(skip), 1) != 0;
+    const bool head = lane == 0 || skip || skip_prev || u0 != k.w[0] || u1 != k.w[1] || u2 != k.w[2];
+    const unsigned heads = __ballot_sync(live, head);
+    leader = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
+  } else {
+    unsigned grp = __match_any_sync(live, h);
+    if (__any_sync(live, __popc(grp) > 1)) {
+      unsigned g2;
+      same_key_in_warp<3>(k, live, &g2);
+      grp &= g2;
+    }
+    const unsigned skip_lanes = __ballot_sync(live, skip);
+    grp &= ~skip_lanes;
+    if (skip) grp = 1u << lane;
+    leader = __ffs(grp) - 1;
   }
-  const unsigned skip_lanes = __ballot_sync(live, skip);
-  grp &= ~skip_lanes;
-  if (skip) grp = 1u << lane;
-  const int leader = __ffs(grp) - 1;
   uint32_t res = PEND;
   bool claimed_tomb = false, candidate = false;
   if (lane == leader && !skip)
