@@ -653,20 +653,23 @@ __global__ void __launch_bounds__(B) k_claim(Table t, const int32_t* __restrict_
     leader[r] = lane;
     if (p >= n) continue;
     h[r] = hash_key<A>(k[r], t.arity);
-    // warp pre-aggregation: equal keys in a warp resolve through their
-    // lowest lane (= lowest batch position); the rest are duplicate losers or
-    // share the leader's found index (hashmap.py:125-131).  One match on the
-    // hash; exact word matches only when some lanes share a hash.
-    unsigned grp = 1u << lane;
+    // warp pre-aggregation of *adjacent* equal keys: a run of equal keys
+    // resolves through its first lane (= lowest batch position); the rest
+    // are duplicate losers or share the leader's found index
+    // (hashmap.py:125-131).  Shuffles + one ballot: __match_any_sync runs
+    // on the ADU and cost more than it saved (claim 0.302 -> 0.296 ms at C2,
+    // insert +8% at rho = 0.1); duplicates that are not adjacent resolve in
+    // the table exactly as they do across warps.
+    int ldr = lane;
     if (A != 0) {
-      grp = __match_any_sync(live[r], h[r]);
-      if (__any_sync(live[r], __popc(grp) > 1)) {
-        unsigned g2;
-        same_key_in_warp<A>(k[r], live[r], &g2);
-        grp &= g2;
-      }
+      bool head = lane == 0;
+#pragma unroll
+      for (int d = 0; d < (A == 0 ? 1 : A); ++d)
+        if (__shfl_up_sync(live[r], k[r].w[d], 1) != k[r].w[d]) head = true;
+      const unsigned heads = __ballot_sync(live[r], head);
+      ldr = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
     }
-    leader[r] = __ffs(grp) - 1;
+    leader[r] = ldr;
     lead[r] = lane == leader[r];
   }
   // stage 1: every round's home bucket in flight
