@@ -1582,6 +1582,21 @@ __device__ __forceinline__ int32_t quantize_one(T x, double cell, bool* bad) {
   return static_cast<int32_t>(q);
 }
 
+// floor(x / cell) without the division where that is provably exact: q =
+// RN(x * RN(1 / cell)) is within 2 ulp(q) of x / cell (one rounding of the
+// reciprocal, one of the product), so when q's fractional part is farther
+// than 4 ulp(q) from an integer, floor(q) == floor(x / cell).  Anything
+// else (near an integer, |q| >= 2^31, NaN, inf) takes the exact path.
+template <typename T>
+__device__ __forceinline__ int32_t quantize_fast(T x, double cell, double rcell, bool* bad) {
+  const double q = static_cast<double>(x) * rcell;
+  const double fq = floor(q);
+  const double f = q - fq;                     // exact for |q| < 2^52
+  const double tol = fabs(q) * 0x1p-50 + 0x1p-1000;
+  if (fabs(q) < 2147483648.0 && f > tol && f < 1.0 - tol) return static_cast<int32_t>(fq);
+  return quantize_one<T>(x, cell, bad);
+}
+
 template <typename T>
 __global__ void k_quantize(const T* __restrict__ pts, int64_t n, double cell, int32_t* __restrict__ out,
                            int32_t* flags) {
@@ -1603,6 +1618,7 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
   static constexpr int kRowBytes = 3 * sizeof(T);
   const T* pts;
   double cell;
+  double rcell;  // RN(1 / cell), for quantize_fast
   // warp-cooperative: the warp's 32 consecutive points (32 x 3 x sizeof(T)
   // bytes, 16-byte aligned) come in as 16-byte vector loads through shared
   // memory instead of three strided scalar loads per lane
@@ -1616,7 +1632,7 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
     __syncwarp();
     const T* row = reinterpret_cast<const T*>(stage) + 3 * lane;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(row[d], cell, bad));
+    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_fast<T>(row[d], cell, rcell, bad));
     return true;
   }
   __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
@@ -1624,7 +1640,8 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
     // of hot voxel slots resident
     const uint64_t pol = stream_policy(1);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) k.w[d] = static_cast<uint32_t>(quantize_one<T>(ld_stream_t<T>(pts + 3 * p + d, pol), cell, bad));
+    for (int d = 0; d < 3; ++d)
+      k.w[d] = static_cast<uint32_t>(quantize_fast<T>(ld_stream_t<T>(pts + 3 * p + d, pol), cell, rcell, bad));
     return true;
   }
 };
@@ -2359,16 +2376,16 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   Table t = make_table(ws);
   const bool al = aligned16(points);
   if (points_are_f64 && al) {
-    run_dedup_select(t, ws, CloudSrc<double>{static_cast<const double*>(points), voxel}, n, out_coords, out_sel,
+    run_dedup_select(t, ws, CloudSrc<double>{static_cast<const double*>(points), voxel, 1.0 / voxel}, n, out_coords, out_sel,
                      scratch_idx, scratch_mask, s);
   } else if (points_are_f64) {
-    run_dedup_select(t, ws, CloudSrc<double, false>{static_cast<const double*>(points), voxel}, n, out_coords,
+    run_dedup_select(t, ws, CloudSrc<double, false>{static_cast<const double*>(points), voxel, 1.0 / voxel}, n, out_coords,
                      out_sel, scratch_idx, scratch_mask, s);
   } else if (al) {
-    run_dedup_select(t, ws, CloudSrc<float>{static_cast<const float*>(points), voxel}, n, out_coords, out_sel,
+    run_dedup_select(t, ws, CloudSrc<float>{static_cast<const float*>(points), voxel, 1.0 / voxel}, n, out_coords, out_sel,
                      scratch_idx, scratch_mask, s);
   } else {
-    run_dedup_select(t, ws, CloudSrc<float, false>{static_cast<const float*>(points), voxel}, n, out_coords,
+    run_dedup_select(t, ws, CloudSrc<float, false>{static_cast<const float*>(points), voxel, 1.0 / voxel}, n, out_coords,
                      out_sel, scratch_idx, scratch_mask, s);
   }
   return check_launch("ash_voxelize");
