@@ -58,7 +58,8 @@ def algorithmic_bytes(op: str, rho_new: float, value_bytes: int, key_bytes: int 
 def _profiled_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the newest committed ncu summary
     (profiles/<tag>_kernels.json, tools/summarize_profiles.py); None if absent."""
-    files = sorted((ROOT / "profiles").glob("*_kernels.json"), key=lambda p: p.stat().st_mtime)
+    # newest by capture tag (r01f < r01l < r01r ...): file times do not survive a checkout
+    files = sorted((ROOT / "profiles").glob("*_kernels.json"), key=lambda p: p.name)
     for f in reversed(files):
         try:
             d = json.loads(f.read_text())
