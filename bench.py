@@ -39,12 +39,21 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-N_KEYS = 10_000_000
+# ASH_BENCH_KEYS only shrinks the workload for the CPU contract test
+N_KEYS = int(os.environ.get("ASH_BENCH_KEYS", 10_000_000))
 RHO = 0.5
-CAPACITY = 10_000_000
-CPU_SAMPLE_KEYS = int(os.environ.get("ASH_CPU_SAMPLE_KEYS", 1_000_000))  # per host core (sharded by key hash)
+CAPACITY = N_KEYS
 METRIC = "insert & find Mops/s (int3 keys)"
 UNIT = "Mops/s"
+# one config dict for both arms (the driver compares them)
+CONFIG = {"workload": f"configs[1]: gen_keys({N_KEYS:_}, 0.5, 'int3', seed=0) (reference bench.py:25-48), "
+                      f"values default_rng(1).random((n, 1), float32); insert into a fresh capacity-{N_KEYS:_} "
+                      "map, then find the same keys",
+          "keys": N_KEYS, "uniqueness": RHO, "capacity": CAPACITY, "value": "f32[1]",
+          "construction": "excluded (fresh map per step, reference bench.py:110,123)",
+          "l2": "GPU arm: flushed between steps (256 MB write); working set > L2"}
+C1_WORKLOAD = ("configs[0]: gen_keys(100_000, 0.5, 'int3', seed=0), f32[1] values default_rng(1), "
+               "capacity 200K; insert + find")
 
 
 def algorithmic_bytes(op: str, rho_new: float, value_bytes: int, key_bytes: int = 12) -> float:
@@ -140,99 +149,154 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the reference algorithm (numpy oracle port) on host cores
+# reference arm: the reference's own CPU implementation on the host cores
 
-def cpu_reference_step(keys: np.ndarray, vals: np.ndarray):
-    from oracle.ash_oracle import OracleMap
-    m = OracleMap(len(keys), 3, [np.float32])
+def _workloads():
+    """workloads.py (gen_keys, sphere_points): host-only numpy; importing it
+    does not load libash.so (the package resolves device names lazily)."""
+    from paper_2110_00511_b200 import workloads
+    return workloads
+
+
+def headline_inputs():
+    """configs[1] at rho = 0.5, exactly as the reference bench builds it
+    (bench.py:25-48, 112-116): gen_keys(10M, 0.5, "int3", seed=0) and values
+    default_rng(1).random((n, 1), float32)."""
+    keys = _workloads().gen_keys(N_KEYS, RHO, "int3", seed=0)
+    vals = np.random.default_rng(1).random((N_KEYS, 1), dtype=np.float32)
+    return keys, vals
+
+
+def load_reference():
+    """(HashMap class, kind, where): the reference ``spatialhash`` installed
+    into baseline/_ref (pip --target) when importable there,
+    else the numpy oracle port of its algorithm (oracle/ash_oracle.py)."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "spatialhash" / "__init__.py").exists():
+        sys.path.insert(0, str(ref))
+        try:
+            import spatialhash
+            if Path(spatialhash.__file__).resolve().is_relative_to(ref.resolve()):
+                return spatialhash, "reference", f"spatialhash {spatialhash.__version__} from baseline/_ref"
+        except Exception as exc:  # noqa: BLE001 - reported, then the port
+            print(f"reference not importable from baseline/_ref ({exc!r}); using the oracle port",
+                  file=sys.stderr)
+        finally:
+            sys.path.remove(str(ref))
+    from oracle import ash_oracle
+
+    class _Port:  # the oracle port under the reference's names
+        HashMap = staticmethod(lambda c, a, specs=(), threads=1: ash_oracle.OracleMap(c, a, specs))
+        voxel_downsample = staticmethod(lambda p, v, threads=1: ash_oracle.voxel_downsample(p, v))
+    return _Port, "port", "oracle/ash_oracle.py (numpy port of the reference algorithm)"
+
+
+def cpu_map_step(ref, keys, vals, threads: int, capacity: int = None) -> float:
+    """One step on the CPU: a fresh map (construction excluded, reference
+    bench.py:110,123), insert, then find the same keys."""
+    m = ref.HashMap(capacity or len(keys), 3, [((vals.shape[1],), np.float32)], threads=threads)
     t0 = time.perf_counter()
-    m.insert(keys, vals)
-    r = m.find(keys)
+    r = m.insert(keys, vals)
+    f = m.find(keys)
     dt = time.perf_counter() - t0
-    assert bool(r.masks.all())
+    assert bool(np.asarray(f.masks).all()) and int(np.asarray(r.masks).sum()) == m.size
     return dt
 
 
-# The reference is single-threaded numpy (its thread pool only splits the
-# chain walk, under the GIL).  To give it every host core, the
-# CPU arm runs the reference algorithm on P key-hash shards in P processes:
-# all copies of a key land in one shard in batch order, so every shard is an
-# exact reference map of its keys and the masks equal one big map's.
-
-_SHARD = {}
-
-
-def _shard_init(keys, vals):
-    import os as _os
-    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        _os.environ[var] = "1"
-    _SHARD["keys"], _SHARD["vals"] = keys, vals
+def _host_cpu():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def _shard_step(_):
-    return cpu_reference_step(_SHARD["keys"], _SHARD["vals"])
-
-
-def _owner_shards(keys, vals, parts):
-    h = (keys[:, 0].astype(np.uint64) * np.uint64(73856093)) ^ \
-        (keys[:, 1].astype(np.uint64) * np.uint64(19349669)) ^ \
-        (keys[:, 2].astype(np.uint64) * np.uint64(83492791))
-    own = ((h * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)) % np.uint64(parts)
-    return [(keys[own == w], vals[own == w]) for w in range(parts)]
-
-
-class ShardedCpuReference:
-    """P worker processes, one reference map per key-hash shard; a step is
-    the wall time of all shards' insert + find (started together)."""
-
-    def __init__(self, keys, vals, parts=None):
-        import multiprocessing as mp
-        import os as _os
-        self.parts = parts or len(_os.sched_getaffinity(0))
-        self.n = len(keys)
-        ctx = mp.get_context("spawn")
-        shards = _owner_shards(keys, vals, self.parts)
-        self.pools = [ctx.Pool(1, initializer=_shard_init, initargs=sh) for sh in shards]
-
-    def step(self) -> float:
-        t0 = time.perf_counter()
-        res = [p.apply_async(_shard_step, (0,)) for p in self.pools]
-        for r in res:
-            r.get()
-        return time.perf_counter() - t0
-
-    def close(self):
-        for p in self.pools:
-            p.terminate()
+def _libash_mapped() -> bool:
+    try:
+        return "libash.so" in Path("/proc/self/maps").read_text()
+    except OSError:
+        return False
 
 
 def run_reference(args, rank: int, world: int):
+    """The reference arm: the same configs[1] workload, config dict, metric
+    and unit as the GPU arm, timed with the reference's protocol (fresh map
+    per step, construction excluded) at threads=1 and threads=os.cpu_count()
+    (BASELINE.md §2): the warm-up steps alternate the two settings, the
+    timed steps use the faster."""
     if rank != 0:
         return
-    cpu = ShardedCpuReference(*_cpu_sample())
-    try:
-        for _ in range(args.warmup):
-            cpu.step()
-        times = [cpu.step() for _ in range(args.steps)]
-    finally:
-        cpu.close()
+    ref, kind, where = load_reference()
+    keys, vals = headline_inputs()
+    ncpu = os.cpu_count() or 1
+    settings = [1] if ncpu == 1 else [1, ncpu]
+    warm = {t: [] for t in settings}
+    for i in range(args.warmup):
+        t = settings[i % len(settings)]
+        warm[t].append(cpu_map_step(ref, keys, vals, t, CAPACITY))
+    best = min(settings, key=lambda t: min(warm[t]) if warm[t] else float("inf"))
+    times = [cpu_map_step(ref, keys, vals, best, CAPACITY) for _ in range(args.steps)]
     t = sum(times) / len(times)
-    value = 2 * cpu.n / t / 1e6
-    sample = (f"per step: insert+find of {cpu.n:,} int3 keys (rho={RHO}, f32[1]) split by key hash "
-              f"over {cpu.parts} processes, each a fresh reference map of its shard (the reference "
-              f"generic-backend algorithm, numpy oracle port, one core per process)")
+    value = 2 * N_KEYS / t / 1e6
+    step_stats = {"mean_ms": round(t * 1e3, 1), "median_ms": round(statistics.median(times) * 1e3, 1),
+                  "min_ms": round(min(times) * 1e3, 1), "trials": len(times),
+                  "value_at_median": round(2 * N_KEYS / statistics.median(times) / 1e6, 4),
+                  "value_at_min": round(2 * N_KEYS / min(times) / 1e6, 4)}
+    threads = {str(k): {"warmup_best_ms": round(min(v) * 1e3, 1)} for k, v in warm.items() if v}
+    other = {"c1": cpu_c1(ref, settings)}
+    if not args.no_sweep:
+        other["sweep"] = cpu_sweep(ref, best, times)
+    sample = (f"per step: the identical configs[1] workload (gen_keys(10M, 0.5, seed 0), f32[1] values, fresh "
+              f"capacity-10M map, insert + find), {where}, threads={best} (the faster of threads=1 and "
+              f"threads={ncpu} over the warm-up steps)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"C2 sample: {cpu.n:,} int3 keys rho={RHO} f32[1] insert+find, "
-                               f"{cpu.parts} key-hash shards", "capacity": cpu.n},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cpu.parts, "kind": "port",
-                         "sample": sample},
+        "config": CONFIG,
+        "step_time": step_stats,
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": best, "kind": kind,
+                         "sample": sample, "host_cpu": _host_cpu(), "host_cores": ncpu,
+                         "threads_tried": threads},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "other_configs": other,
+        "libash_mapped": _libash_mapped(),
     }), flush=True)
+
+
+def cpu_c1(ref, settings, trials: int = 10):
+    """configs[0] on the CPU: gen_keys(100K, 0.5, seed 0), f32[1], capacity
+    200K, insert + find; median and min of `trials` per thread setting."""
+    keys = _workloads().gen_keys(100_000, 0.5, "int3", seed=0)
+    vals = np.random.default_rng(1).random((len(keys), 1), dtype=np.float32)
+    out = {"workload": C1_WORKLOAD}
+    for t in settings:
+        ts = [cpu_map_step(ref, keys, vals, t, 200_000) for _ in range(trials)]
+        out[f"threads={t}"] = {"median_ms": round(statistics.median(ts) * 1e3, 2),
+                               "min_ms": round(min(ts) * 1e3, 2),
+                               "mops_at_median": round(2 * len(keys) / statistics.median(ts) / 1e6, 3)}
+    return out
+
+
+def cpu_sweep(ref, threads, headline_times):
+    """configs[1]'s six points on the CPU (one step each, insert + find of
+    10M keys; rho = 0.5 f32[1] is the headline's median)."""
+    out = []
+    for rho in (0.1, 0.5, 1.0):
+        keys = _workloads().gen_keys(N_KEYS, rho, "int3", seed=0)
+        for width in (1, 8):
+            if rho == RHO and width == 1:
+                t, how = statistics.median(headline_times), "headline median"
+            else:
+                vals = np.random.default_rng(1).random((N_KEYS, width), dtype=np.float32)
+                t, how = cpu_map_step(ref, keys, vals, threads, CAPACITY), "one step"
+            out.append({"rho": rho, "value": f"f32[{width}]", "insert_find_mops": round(2 * N_KEYS / t / 1e6, 4),
+                        "ms": round(t * 1e3, 1), "trials": how})
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -258,6 +322,10 @@ class Events:
         self.torch.cuda.synchronize()
         return sum(s.elapsed_time(e) for s, e in self.pairs)
 
+    def each_ms(self):
+        self.torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in self.pairs]
+
 
 def l2_flush(torch, buf):
     buf.add_(1)  # 256 MB read+write > 126 MB L2
@@ -267,11 +335,9 @@ def gpu_single(args, torch, dev):
     """N=1: the plain map (no routing)."""
     import paper_2110_00511_b200 as ash
     from paper_2110_00511_b200 import _lib
-    from paper_2110_00511_b200.workloads import int3_batch
 
     stream = torch.cuda.current_stream(dev)
-    keys_np = int3_batch(N_KEYS, RHO, seed=0)
-    vals_np = np.random.default_rng(1).random((N_KEYS, 1), dtype=np.float32)
+    keys_np, vals_np = headline_inputs()
     keys_h = torch.from_numpy(keys_np).pin_memory()
     vals_h = torch.from_numpy(vals_np).pin_memory()
     keys = keys_h.to(dev)
@@ -287,12 +353,16 @@ def gpu_single(args, torch, dev):
         m.find(keys)
         ev.stop(s)
 
-    # correctness backstop (reference bench.py:134-150)
+    # correctness backstop (reference bench.py:134-150), here bit-exact:
+    # indices, masks, key and value rows against the reference's own digests
     m.clear()
     r = m.insert(keys, vals)
     f = m.find(keys)
     n_unique = int(np.ceil(RHO * N_KEYS))
     assert m.size == n_unique and int(r.masks.sum()) == n_unique and bool(f.masks.all())
+    parity = digest_check(m, r, f, "c2_rho0.5_f32x1")
+    assert parity is None or parity.startswith("bit-exact"), parity
+    del r, f
 
     warm = Events(torch, stream)
     for _ in range(args.warmup):
@@ -314,6 +384,11 @@ def gpu_single(args, torch, dev):
         torch.cuda.synchronize()
     ms = timed.total_ms() / args.steps
     value = 2 * N_KEYS / (ms / 1e3) / 1e6
+    each = timed.each_ms()
+    step_stats = {"mean_ms": round(ms, 4), "median_ms": round(statistics.median(each), 4),
+                  "min_ms": round(min(each), 4), "trials": len(each),
+                  "value_at_median": round(2 * N_KEYS / statistics.median(each) / 1e3, 2),
+                  "value_at_min": round(2 * N_KEYS / min(each) / 1e3, 2)}
     if args.profile:
         print(json.dumps({"profile_ms_per_step": ms, "value": value}), flush=True)
         sys.exit(0)
@@ -370,11 +445,45 @@ def gpu_single(args, torch, dev):
     h2d = 2 * keys_np.nbytes + vals_np.nbytes
     d2h = 2 * (r.indices.numel() * 4 + r.masks.numel())
 
-    sweep = run_sweep(torch, dev, ash, flush)
-    other = run_other_configs(torch, dev, ash, flush, with_cpu=not args.no_cpu_baseline)
+    e2e_stats = {"median_ms": round(statistics.median(e2e), 3), "min_ms": round(min(e2e), 3),
+                 "trials": len(e2e)}
+    del m
+    torch.cuda.empty_cache()
+    other = {"c1": run_c1(torch, dev, ash, flush, args.steps)}
+    sweep = [] if args.no_sweep else run_sweep(torch, dev, ash, flush)
+    other.update(run_other_configs(torch, dev, ash, flush, with_cpu=not args.no_cpu_baseline))
     other["c5_stream_1gpu"] = run_c5(torch, dev, ash)
-    return dict(ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
-                sweep=sweep, other=other, launches=launches)
+    return dict(parity=parity, ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
+                sweep=sweep, other=other, launches=launches, step_stats=step_stats, e2e_stats=e2e_stats,
+                keys_np=keys_np, vals_np=vals_np)
+
+
+def run_c1(torch, dev, ash, flush, trials: int):
+    """configs[0] on the GPU: the reference's CPU-runnable case (100K keys,
+    capacity 200K, insert + find); median and min over `trials` steps.
+    The 2.4 MB table is L2-resident: this point is launch/L2-bound, not HBM."""
+    keys_np = _workloads().gen_keys(100_000, 0.5, "int3", seed=0)
+    vals_np = np.random.default_rng(1).random((len(keys_np), 1), dtype=np.float32)
+    keys, vals = torch.from_numpy(keys_np).to(dev), torch.from_numpy(vals_np).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    m = ash.HashMap(200_000, 3, [np.float32], device=dev)
+    ts = []
+    for i in range(3 + max(trials, 10)):
+        m.clear()
+        l2_flush(torch, flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r = m.insert(keys, vals)
+        f = m.find(keys)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b))
+    assert int(r.masks.sum()) == 50_000 and bool(f.masks.all())
+    med = statistics.median(ts)
+    return {"workload": C1_WORKLOAD, "median_ms": round(med, 4), "min_ms": round(min(ts), 4),
+            "trials": len(ts), "mops_at_median": round(2 * len(keys_np) / med / 1e3, 1),
+            "bound": "launch latency / L2 (2.4 MB table)"}
 
 
 def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
@@ -486,13 +595,15 @@ def run_c5(torch, dev, ash):
     (each step inserts 2^25 new keys and finds 2^25 keys, half present),
     keys generated in HBM by the counter-based generator.  The N-GPU
     hash-partitioned run of the same stream is `bench.py --c5` under torchrun."""
-    from paper_2110_00511_b200.workloads import c5_step_batches
+    from paper_2110_00511_b200.workloads import c5_step_counters, keys_from_counters_torch
     stream = torch.cuda.current_stream(dev)
     steps = -(-C5_TOTAL // C5_BATCH)
     m = ash.HashMap(C5_TOTAL, 3, [np.float32], device=dev)
     ms_ins, ms_find, ops = [], [], 0
     for s in range(steps):
-        ins, q = c5_step_batches(s * C5_BATCH, min(C5_BATCH, C5_TOTAL - s * C5_BATCH), C5_TOTAL, device=dev)
+        ins_c, q_c = c5_step_counters(s * C5_BATCH, min(C5_BATCH, C5_TOTAL - s * C5_BATCH), C5_TOTAL,
+                                      device=dev)
+        ins, q = keys_from_counters_torch(ins_c), keys_from_counters_torch(q_c)
         vals = torch.rand((len(ins), 1), dtype=torch.float32, device=dev)
         torch.cuda.synchronize()
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -505,10 +616,12 @@ def run_c5(torch, dev, ash):
         ms_ins.append(a.elapsed_time(b))
         ms_find.append(b.elapsed_time(c))
         ops += 2 * len(ins)
-        assert bool(r.masks.all())
+        # index-exact: all-new keys on a fresh heap, so counter c gets index c
+        assert bool(r.masks.all()) and torch.equal(r.indices.long(), ins_c)
+        assert torch.equal(f.indices.long(), torch.where(q_c < C5_TOTAL, q_c, torch.full_like(q_c, -1)))
         hits = int(f.masks.sum())
         assert hits == len(q) // 2, hits
-        del ins, q, vals, r, f
+        del ins, q, vals, r, f, ins_c, q_c
     assert m.size == C5_TOTAL
     tot = sum(ms_ins) + sum(ms_find)
     out = {"workload": "configs[4] at N=1: 400M-key map built by a mixed stream, 12 steps of "
@@ -518,35 +631,73 @@ def run_c5(torch, dev, ash):
            "find_ms_first_last": [round(ms_find[0], 3), round(ms_find[-2], 3)],
            "note": "table 9.6 GB (600M 16-byte slots); the map grows from 0 to 400M keys; "
                    "key generation and value fill excluded; no CPU baseline (400M is infeasible "
-                   "for the reference)"}
+                   "for the reference)",
+           "parity": "index-exact every step: insert indices == pool counters, find indices == "
+                     "queried counter or -1"}
     del m
     torch.cuda.empty_cache()
     return out
 
 
-def run_sweep(torch, dev, ash, flush):
-    """configs[1] sweep: rho in {0.1, 0.5, 1.0} x value f32[1] / f32[8];
-    insert-only and find-only Mops/s (fresh map per trial)."""
-    from paper_2110_00511_b200.workloads import int3_batch
+def _sha(t) -> str:
+    import hashlib
+    a = t.detach().cpu().contiguous()
+    if a.dtype == __import__("torch").bool:
+        a = a.view(__import__("torch").uint8)
+    return hashlib.sha256(a.numpy().tobytes()).hexdigest()
+
+
+def _golden_digests():
+    p = ROOT / "tests" / "golden" / "fullsize_sha.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
+def digest_check(m, r, f, name):
+    """Bit-exact check of one insert + find against the digests the
+    reference itself wrote on the same inputs (oracle/make_fullsize_golden.py):
+    indices, masks, key rows and value rows."""
+    g = _golden_digests()
+    if g is None or name not in g["maps"]:
+        return None
+    want = g["maps"][name]
+    s = m.size
+    got = {"insert_indices": _sha(r.indices), "insert_masks": _sha(r.masks),
+           "find_indices": _sha(f.indices), "find_masks": _sha(f.masks),
+           "key_rows": _sha(m.key_buffer[:s]), "value_rows": _sha(m.value_buffer(0)[:s])}
+    bad = [k for k, v in got.items() if v != want[k]] + (["size"] if s != want["size"] else [])
+    return "bit-exact vs reference digests" if not bad else f"MISMATCH: {bad}"
+
+
+def run_sweep(torch, dev, ash, flush, trials: int = 10):
+    """configs[1] sweep: rho in {0.1, 0.5, 1.0} x value f32[1] / f32[8] on
+    the reference's own inputs (gen_keys seed 0, default_rng(1) values);
+    insert-only and find-only times, fresh map per trial, median and min of
+    `trials`, and a digest check of each point against the reference.  A
+    point whose distinct keys' buckets fit in the L2 (rho = 0.1: 1M x 32 B)
+    is labelled L2-bound: its HBM fraction is not a roofline claim."""
     out = []
     stream = torch.cuda.current_stream(dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     for rho in (0.1, 0.5, 1.0):
-        keys = torch.from_numpy(int3_batch(N_KEYS, rho, seed=0)).to(dev)
+        keys_np = _workloads().gen_keys(N_KEYS, rho, "int3", seed=0)
+        keys = torch.from_numpy(keys_np).to(dev)
+        distinct = int(np.ceil(rho * N_KEYS))
+        bound = "l2" if distinct * 32 < l2 else "hbm"
         for width in (1, 8):
-            vals = torch.rand((N_KEYS, width), dtype=torch.float32, device=dev)
+            vals = torch.from_numpy(np.random.default_rng(1).random((N_KEYS, width), dtype=np.float32)).to(dev)
             m = ash.HashMap(CAPACITY, 3, [((width,), np.float32)], device=dev)
             ti, tf = [], []
-            for trial in range(6):
+            for trial in range(trials + 1):
                 m.clear()
                 l2_flush(torch, flush)
                 a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 a.record(stream)
-                m.insert(keys, vals)
+                r = m.insert(keys, vals)
                 b.record(stream)
                 l2_flush(torch, flush)
                 b2 = torch.cuda.Event(enable_timing=True)
                 b2.record(stream)
-                m.find(keys)
+                f = m.find(keys)
                 c.record(stream)
                 torch.cuda.synchronize()
                 if trial:
@@ -556,43 +707,29 @@ def run_sweep(torch, dev, ash, flush):
             bw, _ = _peaks()
             ib = algorithmic_bytes("insert", rho, 4 * width) * N_KEYS
             fb = algorithmic_bytes("find", rho, 4 * width) * N_KEYS
-            out.append({"rho": rho, "value": f"f32[{width}]",
+            out.append({"rho": rho, "value": f"f32[{width}]", "bound": bound,
                         "insert_mops": round(N_KEYS / ims / 1e3, 1),
                         "find_mops": round(N_KEYS / fms / 1e3, 1),
+                        "insert_min_ms": round(min(ti), 4), "find_min_ms": round(min(tf), 4),
+                        "insert_median_ms": round(ims, 4), "find_median_ms": round(fms, 4),
+                        "trials": trials,
                         "insert_frac": round(ib / (ims / 1e3) / 1e9 / bw, 4),
-                        "find_frac": round(fb / (fms / 1e3) / 1e9 / bw, 4)})
-            del m
+                        "find_frac": round(fb / (fms / 1e3) / 1e9 / bw, 4),
+                        "parity": digest_check(m, r, f, f"c2_rho{rho}_f32x{width}")})
+            del m, r, f
     return out
 
 
-def _cpu_sample():
-    """C2-shaped sample for the CPU arm: CPU_SAMPLE_KEYS keys per host core
-    (uniqueness RHO, f32[1] values)."""
-    import os as _os
-    from paper_2110_00511_b200.workloads import int3_batch
-    n = CPU_SAMPLE_KEYS * len(_os.sched_getaffinity(0))
-    keys = int3_batch(n, RHO, seed=0)
-    vals = np.random.default_rng(1).random((len(keys), 1), dtype=np.float32)
-    return keys, vals
-
-
-def cpu_baseline_sample():
-    keys, vals = _cpu_sample()
-    cpu = ShardedCpuReference(keys, vals)
-    try:
-        cpu.step()
-        t = min(cpu.step() for _ in range(3))
-    finally:
-        cpu.close()
-    # the reference's own reach: one process (its thread pool does not scale, SURVEY §2.3)
-    one = keys[:CPU_SAMPLE_KEYS], vals[:CPU_SAMPLE_KEYS]
-    t1 = min(cpu_reference_step(*one) for _ in range(2))
-    return {"value": round(2 * cpu.n / t / 1e6, 4), "unit": UNIT, "cores": cpu.parts, "kind": "port",
-            "sample": f"insert+find of {cpu.n:,} int3 keys (rho={RHO}, f32[1]) split by key hash over "
-                      f"{cpu.parts} processes, each a fresh reference map of its shard (reference "
-                      f"generic-backend algorithm via the numpy oracle port), best of 3",
-            "single_process": {"value": round(2 * CPU_SAMPLE_KEYS / t1 / 1e6, 4), "cores": 1,
-                               "sample": f"first {CPU_SAMPLE_KEYS:,} keys of the same sample, one map"}}
+def cpu_baseline_sample(keys, vals):
+    """The GPU arm's CPU leg: one step of the identical configs[1] workload
+    by the reference (baseline/_ref; else the oracle port) at threads=1,
+    about 8-10 s of host work (the reference arm times all K steps and both
+    thread settings)."""
+    ref, kind, where = load_reference()
+    t = cpu_map_step(ref, keys, vals, 1, CAPACITY)
+    return {"value": round(2 * N_KEYS / t / 1e6, 4), "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"one step of the identical configs[1] workload (10M keys insert + find, fresh "
+                      f"capacity-10M map), {where}, threads=1", "host_cpu": _host_cpu()}
 
 
 def main():
@@ -610,11 +747,16 @@ def main():
                     help="configs[4]: the 400M-key partitioned map built by the mixed stream (strong scaling)")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] six-point sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -642,34 +784,39 @@ def main():
         "tile_scan": 4 * 2 * (N_KEYS / 2048),
     }
     dom = max(kms, key=kms.get)
+    ins_ms = kms["claim"] + kms["tile_scan"] + kms["commit"]
+    op_level = {
+        "insert_bytes_per_op": algorithmic_bytes("insert", RHO, 4),
+        "find_bytes_per_op": algorithmic_bytes("find", RHO, 4),
+        "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS / (ins_ms / 1e3) / 1e9 / bw, 4),
+        "find_frac": round(per_kernel_bytes["find"] / (kms["find"] / 1e3) / 1e9 / bw, 4),
+        "step_frac": round((algorithmic_bytes("insert", RHO, 4) + algorithmic_bytes("find", RHO, 4)) * N_KEYS /
+                           (res["ms"] / 1e3) / 1e9 / bw, 4)}
     achieved = per_kernel_bytes[dom] / (kms[dom] / 1e3) / 1e9
     traffic, traffic_src = _profiled_traffic(f"k_{dom}")
-    cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
+    cpu = None if args.no_cpu_baseline else cpu_baseline_sample(res["keys_np"], res["vals_np"])
     line = {
         "metric": METRIC, "value": round(res["value"], 2), "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms"], 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": "configs[1]: 10M int3 keys, uniqueness 0.5, value f32[1]; "
-                               "insert into a fresh capacity-10M map, then find the same keys",
-                   "keys": N_KEYS, "uniqueness": RHO, "capacity": CAPACITY, "value": "f32[1]",
-                   "l2": "flushed between steps (256 MB write); working set > L2",
-                   "construction": "excluded (HashMap.clear before each step)"},
+        "config": CONFIG,
+        "step_time": res["step_stats"],
+        "parity": res["parity"],
         "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": round(achieved, 1),
                      "peak": bw, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / bw, 4), "traffic": traffic,
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": int(per_kernel_bytes[dom]),
-                     "kernel_ms": {k: round(v, 4) for k, v in kms.items()}},
-        "op_roofline": {
-            "insert_frac": round(algorithmic_bytes("insert", RHO, 4) * N_KEYS /
-                                 ((kms["claim"] + kms["tile_scan"] + kms["commit"]) / 1e3) / 1e9 / bw, 4),
-            "find_frac": round(per_kernel_bytes["find"] / (kms["find"] / 1e3) / 1e9 / bw, 4)},
+                     "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+                     # SURVEY §8(d)'s op-level figures: insert 75 B, find 49 B per position
+                     "op_level": op_level},
         # the bound that actually binds a random probe: DRAM bandwidth at the
         # ~85 B the memory system moves per 32-byte probe (profiles/*_random_access.json)
         "random_access": _random_access(kms),
         "e2e": {"value": round(2 * N_KEYS / (res["e2e_ms"] / 1e3) / 1e6, 2), "unit": UNIT,
-                "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
+                "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"]),
+                **res["e2e_stats"]},
         "gpu_launches": res["launches"],  # libash kernels in the timed region (ash_launch_count)
         "clocks": res["clocks"],
         "sweep": res["sweep"],
@@ -677,6 +824,19 @@ def main():
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
+
+
+def self_launch(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: launch the N ranks the
+    way the driver does (torch.distributed.run, 127.0.0.1) and return their
+    exit status."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -1,19 +1,41 @@
 """B200-native batch spatial hash map (ASH, arxiv 2110.00511).
 
-Drop-in for the reference ``spatialhash`` map API on CUDA tensors; every
-batch operation runs hand-written sm_100a kernels from libash.so.
+Drop-in for the reference ``spatialhash`` package API
+(/root/reference/pkg/src/spatialhash/__init__.py:3-16); every batch
+operation runs hand-written sm_100a kernels from libash.so.
+
+Names resolve lazily (PEP 562): importing the package, or a host-only
+module such as ``workloads``, does not load libash.so; the first use of a
+device name does, and raises if the library is missing (no CPU fallback).
 """
-from .hashmap import (BatchResult, CapacityError, ConcurrentAccessError, HashMap,
-                      HashSet, ValueSpec)
-from .geometry import (PointCloud, lattice_offsets, quantize, radius_neighbors,
-                       set_intersection, voxel_downsample)
-from .blocks import BlockGrid, allocate_blocks, allocate_frame, frame_blocks, frame_candidates
+from __future__ import annotations
+
+import importlib
 
 __version__ = "0.1.0"
 
-__all__ = [
-    "BatchResult", "CapacityError", "ConcurrentAccessError", "HashMap", "HashSet",
-    "ValueSpec", "PointCloud", "quantize", "voxel_downsample", "lattice_offsets",
-    "radius_neighbors", "set_intersection", "BlockGrid", "allocate_blocks",
-    "allocate_frame", "frame_blocks", "frame_candidates",
-]
+_EXPORTS = {
+    "BatchResult": "hashmap", "CapacityError": "hashmap", "ConcurrentAccessError": "hashmap",
+    "HashMap": "hashmap", "HashSet": "hashmap", "ValueSpec": "hashmap",
+    "IndexHeap": "index_heap", "IndexHeapExhausted": "index_heap",
+    "PointCloud": "geometry", "quantize": "geometry", "voxel_downsample": "geometry",
+    "lattice_offsets": "geometry", "radius_neighbors": "geometry",
+    "set_intersection": "geometry", "cube_embed": "geometry",
+    "BlockGrid": "blocks", "allocate_blocks": "blocks", "allocate_frame": "blocks",
+    "frame_blocks": "blocks", "frame_candidates": "blocks",
+}
+
+__all__ = sorted(_EXPORTS)
+
+
+def __getattr__(name: str):
+    mod = _EXPORTS.get(name)
+    if mod is None:
+        raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+    value = getattr(importlib.import_module(f".{mod}", __name__), name)
+    globals()[name] = value
+    return value
+
+
+def __dir__():
+    return sorted(set(globals()) | set(_EXPORTS))

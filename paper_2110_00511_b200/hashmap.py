@@ -257,20 +257,34 @@ class HashMap:
 
     @on_device
     def _init_state(self, capacity: int, zero_rows: bool = True) -> None:
-        """hashmap.py:200-210: fresh table, heap = arange, zeroed buffers."""
+        """hashmap.py:200-210: fresh table, heap = arange, zeroed buffers.
+
+        Everything is sized and allocated into locals first; the map's fields
+        and the ctypes struct change only once all of it succeeded, so a
+        rehash that fails (table limit ValueError, CUDA OOM) leaves the old
+        map fully intact."""
         dev = self._device
+        n_slots = _table_slots(capacity)  # raises past the table limit
+        slots = torch.empty(n_slots * 4, dtype=torch.int32, device=dev)
+        key_buf = torch.empty((capacity, self.key_arity), dtype=torch.int32, device=dev)
+        value_bufs = tuple(torch.empty((capacity, *s.shape), dtype=td, device=dev)
+                           for s, td in zip(self.value_specs, self._torch_dtypes))
+        heap_buf = torch.empty(capacity, dtype=torch.int32, device=dev)
+        active = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        erase_claim = torch.empty(capacity, dtype=torch.int32, device=dev)
+        freed = torch.empty(capacity, dtype=torch.uint8, device=dev)
+        counters = torch.zeros(_lib.N_COUNTERS, dtype=torch.int32, device=dev)
+        need = _lib.scan_tiles(capacity)
+        scan = torch.zeros(need, dtype=torch.int64, device=dev)
+        tiles = torch.zeros(2 * need + 1, dtype=torch.int32, device=dev)
+        rank_words = torch.empty(2 * (_lib.TILE // 32) * need, dtype=torch.int32, device=dev)
+        # commit
         self._capacity = capacity
-        self._n_slots = _table_slots(capacity)
-        self._slots = torch.empty(self._n_slots * 4, dtype=torch.int32, device=dev)
-        self._key_buf = torch.empty((capacity, self.key_arity), dtype=torch.int32, device=dev)
-        self._value_bufs = tuple(torch.empty((capacity, *s.shape), dtype=td, device=dev)
-                                 for s, td in zip(self.value_specs, self._torch_dtypes))
-        self._heap_buf = torch.empty(capacity, dtype=torch.int32, device=dev)
-        self._active = torch.empty(capacity, dtype=torch.uint8, device=dev)
-        self._erase_claim = torch.empty(capacity, dtype=torch.int32, device=dev)
-        self._freed = torch.empty(capacity, dtype=torch.uint8, device=dev)
-        self._counters = torch.zeros(_lib.N_COUNTERS, dtype=torch.int32, device=dev)
-        self._scan = torch.zeros(0, dtype=torch.int64, device=dev)
+        self._n_slots = n_slots
+        self._slots, self._key_buf, self._value_bufs = slots, key_buf, value_bufs
+        self._heap_buf, self._active, self._erase_claim, self._freed = heap_buf, active, erase_claim, freed
+        self._counters = counters
+        self._scan, self._tiles, self._rank_words = scan, tiles, rank_words
         self._struct = AshMap()
         self._fill_struct()
         self._ensure_scan(capacity)
@@ -296,6 +310,12 @@ class HashMap:
         s.freed = self._freed.data_ptr()
         s.counters = self._counters.data_ptr()
         s.capacity = self._capacity
+        s.scan_status = self._scan.data_ptr()
+        s.scan_status_len = self._scan.numel()
+        s.tile_counts = self._tiles.data_ptr()
+        s.tile_counts_len = self._tiles.numel()
+        s.rank_words = self._rank_words.data_ptr()
+        s.rank_words_len = self._rank_words.numel()
 
     def _ensure_scan(self, n: int) -> None:
         need = _lib.scan_tiles(max(n, self._capacity))
@@ -488,11 +508,33 @@ class HashMap:
         self._tombs_ub = tombs
         if size + tombs + min(m, self._capacity - size) <= limit:
             return
-        new_slots = torch.empty_like(self._slots)
-        call("ash_rebuild_table", self._ptr(), new_slots.data_ptr(), self._n_slots, self._stream())
+        self._rebuild_slots(self._n_slots)
+
+    def _rebuild_slots(self, n_slots: int) -> None:
+        """Re-place every live slot into a fresh array of n_slots slots (same
+        buffer indices; tombstones dropped)."""
+        new_slots = torch.empty(n_slots * 4, dtype=torch.int32, device=self._device)
+        call("ash_rebuild_table", self._ptr(), new_slots.data_ptr(), n_slots, self._stream())
         self._slots = new_slots
+        self._n_slots = n_slots
         self._struct.slots = new_slots.data_ptr()
+        self._struct.n_slots = n_slots
         self._tombs_ub = 0
+
+    def _widen_for_claims(self, m: int) -> None:
+        """A batch longer than the free space claims up to m new slots
+        before its exact winner count is known.  Make the slot array hold
+        size + m under the load limit first (capacity and indices unchanged),
+        so an oversize batch of distinct keys cannot run the table full and
+        probe it end to end; the rehash that follows, if the winners do not
+        fit, sizes the table from the new capacity again."""
+        size = self._sync_size()
+        tombs = int(self._counters[_lib.CTR_TOMBS].item())
+        if size + tombs + m <= int(_SLOT_LIMIT * self._n_slots):
+            return
+        want = int(math.ceil((size + m) / _SLOT_LIMIT)) + 2
+        want = min(1 << 30, max(self._n_slots, want + (want & 1)))
+        self._rebuild_slots(want)
 
     # -- operations (hashmap.py:336-456) ---------------------------------
 
@@ -639,6 +681,7 @@ class HashMap:
                          idx[a:b].data_ptr(), msk[a:b].data_ptr(), self._stream())
                 self._top_ub = min(self._capacity, self._top_ub + m)
                 break
+            self._widen_for_claims(m)
             call("ash_insert_claim", self._ptr(), keys.data_ptr(), m, idx.data_ptr(),
                  msk.data_ptr(), self._stream())
             call("ash_insert_count", self._ptr(), m, idx.data_ptr(), msk.data_ptr(),
