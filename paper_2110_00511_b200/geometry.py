@@ -18,7 +18,7 @@ from ._lib import AshMap, call
 from .hashmap import BatchResult, HashMap, HashSet, _stream_handle, _table_slots
 
 __all__ = ["PointCloud", "quantize", "voxel_downsample", "lattice_offsets", "radius_neighbors",
-           "set_intersection"]
+           "set_intersection", "cube_embed"]
 
 
 class PointCloud:
@@ -276,3 +276,31 @@ def set_intersection(keys_a, keys_b, backend: str = "generic", threads: int = 1,
     probe.insert(a)
     out = b[probe.find(b).masks]
     return out.cpu() if host else out
+
+
+_CUBE_CORNERS = torch.tensor([[i >> 2 & 1, i >> 1 & 1, i & 1] for i in range(8)], dtype=torch.int32)
+
+
+def cube_embed(points, grid_spacing: float, device=None):
+    """Enclosing-cell corners and trilinear weights per point
+    (geometry.py:105-126): ``(corners int32 (n, 8, 3), weights float64
+    (n, 8))``, corner j = floor(p / spacing) + the j-th ``(0,1)^3`` offset in
+    lexicographic order.  Not on the map path: exported for the
+    drop-in surface and computed with fp64 tensor ops in the reference's
+    order (true division, floor, ``w = w_x * w_y * w_z`` left to right), so
+    the weights are bit-identical to numpy's."""
+    if grid_spacing <= 0:
+        raise ValueError("grid spacing must be > 0")
+    dev = _device(device)
+    host = _on_host(points.positions if isinstance(points, PointCloud) else points)
+    pts = _points_tensor(points, dev).to(torch.float64)  # np.asarray(..., float64)
+    scaled = pts / grid_spacing
+    base = torch.floor(scaled)
+    frac = scaled - base
+    if base.numel() and (float(base.min()) < -(2 ** 31) or float(base.max()) >= 2 ** 31):
+        raise ValueError("grid coordinates exceed int32 range")
+    off = _CUBE_CORNERS.to(dev)
+    corners = base.to(torch.int32)[:, None, :] + off[None, :, :]
+    axis_w = torch.where(off[None, :, :] == 1, frac[:, None, :], 1.0 - frac[:, None, :])
+    weights = axis_w[..., 0] * axis_w[..., 1] * axis_w[..., 2]
+    return (corners.cpu(), weights.cpu()) if host else (corners, weights)
