@@ -824,14 +824,14 @@ class HashMap:
 
     @on_device
     def items_arrays(self) -> tuple:
-        act = self.active_indices().long()
+        act = HashMap.active_indices(self).long()
         return (self._key_buf[act].clone(), *(b[act].clone() for b in self._value_bufs))
 
     @on_device
     def validate(self) -> None:
         """Structural invariants (hashmap.py:483-496); raises AssertionError."""
         size = self._sync_size()
-        act = self.active_indices().long()
+        act = HashMap.active_indices(self).long()
         free = self._heap_buf[size:].long()
         assert act.numel() == size, "size counter vs active flags"
         assert int(self._active.sum().item()) == size, "size counter vs active flags"
@@ -840,7 +840,7 @@ class HashMap:
         assert torch.equal(both, torch.arange(self._capacity, device=self._device)), \
             "active/free sets must partition the index range"
         if size:
-            res = self.find(self._key_buf[act])
+            res = HashMap.find(self, self._key_buf[act])
             assert bool(res.masks.all()), "stored key failed lookup"
             assert torch.equal(torch.sort(res.indices.long()).values, act), \
                 "lookup resolved to foreign indices"

@@ -1,6 +1,6 @@
 """The reference's OWN test files, run unmodified against the drop-in.
 
-tests/reference_suite/reference_alias.py registers ``spatialhash`` as the
+tests/reference_suite/spatialhash/ binds the name ``spatialhash`` to the
 numpy-facing drop-in (``paper_2110_00511_b200.numpy_api``); the reference's
 TSDF / bench / io / cli code and its ``spatialhash_arrays`` wrapper run from
 the reference's own sources on top of the device map.  The reference files
@@ -23,8 +23,11 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 STAGED = ROOT / "baseline" / "_ref_suite"
 
-# reference test id -> why the drop-in deliberately differs
-DEVIATIONS: dict = {}
+# reference test id -> why it cannot pass here (not a drop-in difference)
+DEVIATIONS: dict = {
+    "test_report_renders_figures": "needs matplotlib, which this image does not have (report "
+                                   "plotting is out of scope, SURVEY §2)",
+}
 
 
 def _layout():
@@ -42,8 +45,8 @@ def test_reference_suite_on_the_drop_in(cuda_ok, tmp_path):
         pytest.skip("reference test files not available (run tools/stage_reference_suite.sh)")
     tests, pkg, btests, bsrc = lay
     report = tmp_path / "report.json"
-    env = dict(os.environ, ASH_REF_PKG=str(pkg), ASH_REF_BINDINGS=str(bsrc),
-               PYTHONPATH=os.pathsep.join([str(ROOT / "tests" / "reference_suite"), str(tests)]))
+    env = dict(os.environ, ASH_REF_PKG=str(pkg),
+               PYTHONPATH=os.pathsep.join([str(ROOT / "tests" / "reference_suite"), str(bsrc), str(tests)]))
     code = (
         "import json, sys, pytest\n"
         "class R:\n"
@@ -53,7 +56,7 @@ def test_reference_suite_on_the_drop_in(cuda_ok, tmp_path):
         "            self.out.setdefault(report.nodeid, report.outcome)\n"
         "            if report.outcome == 'failed': self.out[report.nodeid] = 'failed'\n"
         "r = R()\n"
-        f"rc = pytest.main(['-q', '-p', 'reference_alias', '-p', 'no:cacheprovider', '--rootdir', {str(tests.parent)!r}, "
+        f"rc = pytest.main(['-q', '-p', 'no:cacheprovider', '--rootdir', {str(tests.parent)!r}, "
         f"{str(tests)!r}, {str(btests)!r}], plugins=[r])\n"
         f"open({str(report)!r}, 'w').write(json.dumps(r.out))\n")
     proc = subprocess.run([sys.executable, "-c", code], env=env, cwd=str(tmp_path),
