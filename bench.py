@@ -395,7 +395,13 @@ def gpu_single(args, torch, dev):
 
     # per-kernel split (same workload): claim / commit / find, CUDA events on
     # the launching stream
+    # with the deferred commit (the product default) the step's commit is the
+    # staged commit alone; the table sweep runs at the next mutation of the
+    # map (ash_settle) or never when the map is cleared, and is timed apart
+    from paper_2110_00511_b200 import hashmap as _hm
+    commit_fn = "ash_insert_commit_lazy" if _hm.LAZY_COMMIT else "ash_insert_commit"
     kern = {"claim": [], "tile_scan": [], "commit": [], "find": []}
+    settle_ms = []
     for _ in range(5):
         m.clear()
         l2_flush(torch, flush)
@@ -409,20 +415,30 @@ def gpu_single(args, torch, dev):
         e[1].record(stream)
         _lib.call("ash_insert_count", m._ptr(), N_KEYS, idx.data_ptr(), msk.data_ptr(), m._stream())
         e[2].record(stream)
-        _lib.call("ash_insert_commit", m._ptr(), keys.data_ptr(), N_KEYS, vptr, 0, idx.data_ptr(), msk.data_ptr(), m._stream())
+        _lib.call(commit_fn, m._ptr(), keys.data_ptr(), N_KEYS, vptr, 0, idx.data_ptr(), msk.data_ptr(), m._stream())
         e[3].record(stream)
         m._size_known = False
+        m._unsettled = _hm.LAZY_COMMIT
         l2_flush(torch, flush)
         e4 = torch.cuda.Event(enable_timing=True)
         e4.record(stream)
         m.find(keys)
         e[4].record(stream)
+        e5, e6 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e5.record(stream)
+        m._settle()
+        e6.record(stream)
         torch.cuda.synchronize()
+        settle_ms.append(e5.elapsed_time(e6))
         kern["claim"].append(e[0].elapsed_time(e[1]))
         kern["tile_scan"].append(e[1].elapsed_time(e[2]))
         kern["commit"].append(e[2].elapsed_time(e[3]))
         kern["find"].append(e4.elapsed_time(e[4]))
     kms = {k: statistics.median(v) for k, v in kern.items()}
+    deferred = {"lazy_commit": _hm.LAZY_COMMIT, "settle_ms": round(statistics.median(settle_ms), 4),
+                "note": "ash_settle (the table sweep) runs at the next mutating call, not in the step; "
+                        "the bench clears the map between steps (reference protocol: fresh map per trial), "
+                        "which discards the pending table"}
 
     # e2e: public API with pinned host buffers; H2D of inputs and D2H of the
     # results inside the timed region
@@ -453,7 +469,7 @@ def gpu_single(args, torch, dev):
     sweep = [] if args.no_sweep else run_sweep(torch, dev, ash, flush)
     other.update(run_other_configs(torch, dev, ash, flush, with_cpu=not args.no_cpu_baseline))
     other["c5_stream_1gpu"] = run_c5(torch, dev, ash)
-    return dict(parity=parity, ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
+    return dict(deferred=deferred, parity=parity, ms=ms, value=value, kms=kms, e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, clocks=clk.summary(),
                 sweep=sweep, other=other, launches=launches, step_stats=step_stats, e2e_stats=e2e_stats,
                 keys_np=keys_np, vals_np=vals_np)
 
@@ -809,6 +825,7 @@ def main():
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": int(per_kernel_bytes[dom]),
                      "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+                     "deferred_sweep": res["deferred"],
                      # SURVEY §8(d)'s op-level figures: insert 75 B, find 49 B per position
                      "op_level": op_level},
         # the bound that actually binds a random probe: DRAM bandwidth at the

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ASH_ABI_VERSION 5
+#define ASH_ABI_VERSION 6
 
 #define ASH_OK 0
 #define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
@@ -156,6 +156,24 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n,
                       int32_t* out_idx, uint8_t* out_mask, void* stream);
 int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx,
                         void* stream);
+
+/* Deferred slot-state commit (same contract and results as ash_insert /
+ * ash_insert_commit; needs m->rank_words).  When the batch is large enough
+ * for the table-sweep commit, the sweep is not run: the table keeps the
+ * batch's winners as PENDING|pos, which ash_find / ash_find_lattice resolve
+ * on the fly from the rank words (index = top + rank(pos), or
+ * heap[top + rank]).  The caller MUST call ash_settle before the next
+ * mutating call on m (insert / activate / erase / rebuild / rehash / reset
+ * excepted: a reset discards the table).  The sweep then runs once, or never
+ * if the map is reset first.  Reference semantics are unchanged
+ * (hashmap.py:397-413): only the moment the slot states are written moves. */
+int ash_insert_lazy(ash_map_t* m, const int32_t* keys, int64_t n,
+                    const void* const* values, int32_t association,
+                    int32_t* out_idx, uint8_t* out_mask, void* stream);
+int ash_insert_commit_lazy(ash_map_t* m, const int32_t* keys, int64_t n,
+                           const void* const* values, int32_t association,
+                           int32_t* out_idx, uint8_t* out_mask, void* stream);
+int ash_settle(ash_map_t* m, void* stream);
 
 /* HashMap.erase (hashmap.py:431-456): first found occurrence per key is
  * removed; freed indices return to the heap sorted (index_heap.py:38-47).

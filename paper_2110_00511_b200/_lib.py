@@ -53,6 +53,10 @@ _SIGNATURES = {
     "ash_insert_count": (c_int32, [_M, c_int64, c_void_p, c_void_p, c_void_p]),
     "ash_insert_commit": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ash_insert_rollback": (c_int32, [_M, c_int64, c_void_p, c_void_p]),
+    "ash_insert_lazy": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_commit_lazy": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                         c_void_p]),
+    "ash_settle": (c_int32, [_M, c_void_p]),
     "ash_insert_commit_delegate": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                              c_void_p, c_void_p]),
     "ash_heap_put_losers": (c_int32, [_M, c_void_p, c_int64, c_void_p]),
@@ -104,7 +108,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ash_abi_version() != 5:
+    if lib.ash_abi_version() != 6:
         raise ImportError("libash.so ABI version mismatch; rebuild")
     return lib
 

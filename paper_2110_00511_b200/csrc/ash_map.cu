@@ -405,10 +405,34 @@ __device__ __forceinline__ uint4 slot_value(const Key<A>& k, uint32_t state) {
   return make_uint4(k.w[0], k.w[1], k.w[2], state);
 }
 
+// A deferred slot-state commit (ash_insert_commit_lazy): the last insert's
+// winners still hold PENDING|pos in the table until ash_settle runs the table
+// sweep.  Read-only probes resolve such a slot the way the sweep would:
+// index = top + rank(pos) (heap[top + rank] once frees touched the heap above
+// top), rank from the batch's rank words (2.5 MB per 10M positions: L2
+// resident).  rank_words == nullptr: nothing can be pending.
+struct Settle {
+  const uint2* rank_words;
+  const int32_t* heap;
+  const int32_t* counters;
+};
+
+Settle make_settle(const ash_map_t* m) {
+  return Settle{m->rank_words ? reinterpret_cast<const uint2*>(m->rank_words) : nullptr, m->heap, m->counters};
+}
+
+__device__ __forceinline__ uint32_t settle_index(const Settle& z, uint32_t j) {
+  const uint2 rw = __ldg(z.rank_words + (j >> 5));
+  const uint32_t rank = rw.y + __popc(rw.x & ((1u << (j & 31)) - 1u));
+  const uint32_t top = static_cast<uint32_t>(__ldg(z.counters + ASH_CTR_TOP_BASE));
+  const bool ident = __ldg(z.counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(top);
+  return ident ? top + rank : static_cast<uint32_t>(__ldg(z.heap + top + rank));
+}
+
 // Read-only probe (find / erase): returns the buffer index or -1; slot out.
 template <int A>
 __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, uint32_t h,
-                                              uint32_t* slot_out) {
+                                              uint32_t* slot_out, const Settle* z = nullptr) {
   uint32_t b = home_bucket(h, t.n_buckets);
   for (uint32_t step = 0; step < t.n_buckets; ++step) {
     uint32_t w[8];
@@ -417,9 +441,18 @@ __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, u
     for (int s = 0; s < 2; ++s) {
       uint32_t st = w[4 * s + 3];
       if (st == EMPTY) return -1;
-      if (st < PEND && slot_matches<A>(w + 4 * s, st, k, t, nullptr)) {
-        if (slot_out) *slot_out = 2 * b + s;
-        return static_cast<int32_t>(st);
+      if (st < PEND) {
+        if (slot_matches<A>(w + 4 * s, st, k, t, nullptr)) {
+          if (slot_out) *slot_out = 2 * b + s;
+          return static_cast<int32_t>(st);
+        }
+      } else if (z && (st & 0xC0000000u) == PEND && w[4 * s] == k.w[0] &&
+                 ((A != 0 && A < 2) || w[4 * s + 1] == k.w[1]) && ((A != 0 && A < 3) || w[4 * s + 2] == k.w[2])) {
+        const uint32_t idx = settle_index(*z, st & ~PEND);
+        if (A != 0 || slot_matches<A>(w + 4 * s, idx, k, t, nullptr)) {
+          if (slot_out) *slot_out = 2 * b + s;
+          return static_cast<int32_t>(idx);
+        }
       }
     }
     b = next_bucket(b, t.n_buckets);
@@ -524,13 +557,13 @@ __global__ void k_fill_empty(uint4* slots, int64_t n_slots) {
 template <int A, int B = kBlock>
 __global__ void __launch_bounds__(B) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
                                             int32_t* __restrict__ out_idx,
-                                            uint8_t* __restrict__ out_mask) {
+                                            uint8_t* __restrict__ out_mask, Settle z) {
   __shared__ uint32_t stage[B * 3];
   const int64_t p = blockIdx.x * static_cast<int64_t>(B) + threadIdx.x;
   const uint64_t pol = stream_policy(t.hints);
   Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, pol);
   if (p >= n) return;
-  int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), nullptr);
+  int32_t idx = probe_find<A>(t, k, hash_key<A>(k, t.arity), nullptr, z.rank_words ? &z : nullptr);
   st_stream(out_idx + p, static_cast<uint32_t>(idx), pol);
   st_stream_u8(out_mask + p, idx >= 0, pol);
 }
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(B) k_find(Table t, const int32_t* __restrict__
 // materialised.  int32 addition wraps, as numpy's does.
 __global__ void __launch_bounds__(kBlock) k_find_lattice(Table t, const int32_t* __restrict__ coords, int64_t n,
                                                          int r, int32_t* __restrict__ out_idx,
-                                                         uint8_t* __restrict__ out_mask) {
+                                                         uint8_t* __restrict__ out_mask, Settle z) {
   const int s = 2 * r + 1, K = s * s * s;
   const int64_t q = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
   if (q >= n * K) return;
@@ -554,7 +587,7 @@ __global__ void __launch_bounds__(kBlock) k_find_lattice(Table t, const int32_t*
   k.w[0] = static_cast<uint32_t>(__ldg(coords + 3 * p)) + static_cast<uint32_t>(j / (s * s) - r);
   k.w[1] = static_cast<uint32_t>(__ldg(coords + 3 * p + 1)) + static_cast<uint32_t>((j / s) % s - r);
   k.w[2] = static_cast<uint32_t>(__ldg(coords + 3 * p + 2)) + static_cast<uint32_t>(j % s - r);
-  const int32_t idx = probe_find<3>(t, k, hash_key<3>(k, 3), nullptr);
+  const int32_t idx = probe_find<3>(t, k, hash_key<3>(k, 3), nullptr, z.rank_words ? &z : nullptr);
   st_stream(out_idx + q, static_cast<uint32_t>(idx), pol);
   st_stream_u8(out_mask + q, idx >= 0, pol);
 }
@@ -2115,7 +2148,8 @@ int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uin
   Table t = make_table(m);
   cudaStream_t s = as_stream(stream);
   // 256-thread blocks (128 within 1%, 512 1-4% slower; r01m A/B)
-  ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask)));
+  ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
+                                                                                make_settle(m))));
   return check_launch("ash_find");
 }
 
@@ -2130,7 +2164,8 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
   if (n > (int64_t(1) << 38) / K) return fail(ASH_ERR_INVALID, "too many lattice queries");
   if (!coords || !out_idx || !out_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
   Table t = make_table(m);
-  k_find_lattice<<<grid_for(n * K, kBlock), kBlock, 0, as_stream(stream)>>>(t, coords, n, r, out_idx, out_mask); note_launch();
+  k_find_lattice<<<grid_for(n * K, kBlock), kBlock, 0, as_stream(stream)>>>(t, coords, n, r, out_idx, out_mask,
+                                                                            make_settle(m)); note_launch();
   return check_launch("ash_find_lattice");
 }
 
@@ -2166,8 +2201,31 @@ int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint
   return check_launch("ash_insert_count");
 }
 
+static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
+                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy);
+
 int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
                       int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  return insert_commit(m, keys, n, values, association, out_idx, out_mask, stream, false);
+}
+
+int ash_insert_commit_lazy(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
+                           int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (!m || !m->rank_words) return fail(ASH_ERR_INVALID, "a deferred commit needs rank_words");
+  return insert_commit(m, keys, n, values, association, out_idx, out_mask, stream, true);
+}
+
+int ash_settle(ash_map_t* m, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (!m->rank_words) return ASH_OK;
+  Table t = make_table(m);
+  const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
+  launch_sweep(t, nullptr, m->rank_words, m, sweep_min, as_stream(stream));
+  return check_launch("ash_settle");
+}
+
+static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
+                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
@@ -2186,6 +2244,9 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
   // winners at which the slot states are committed by the table sweep
   const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
   int32_t* rank_words = (m->rank_words && m->rank_words_len >= 2 * ((n + 31) / 32)) ? m->rank_words : nullptr;
+  // deferred: the table keeps PENDING|pos for this batch's winners until
+  // ash_settle (finds resolve them through the rank words meanwhile)
+  const bool defer = lazy && rank_words;
   if (pre && vw >= 0 && m->arity <= 3 && g_commit_bulk && aligned16(keys) && aligned16(out_idx) &&
       aligned16(out_mask) && aligned16(m->heap) && (vw == 0 || aligned16(va.src[0]))) {
     int rc = ASH_OK;
@@ -2205,7 +2266,7 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
     }
 #undef ASH_BULK
     if (rc) return rc;
-    launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
+    if (!defer) launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
     return check_launch("ash_insert_commit");
   }
   int32_t* tile_pre = pre ? pre : m->tile_counts;
@@ -2223,7 +2284,7 @@ int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* 
     default: ASH_COMMIT(-1); break;
   }
 #undef ASH_COMMIT
-  launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
+  if (!defer) launch_sweep(t, out_idx, rank_words, m, sweep_min, s);
   return check_launch("ash_insert_commit");
 }
 
@@ -2259,6 +2320,13 @@ int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* 
   if (int rc = ash_insert_claim(m, keys, n, out_idx, out_mask, stream)) return rc;
   if (int rc = ash_insert_count(m, n, out_idx, out_mask, stream)) return rc;
   return ash_insert_commit(m, keys, n, values, association, out_idx, out_mask, stream);
+}
+
+int ash_insert_lazy(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values, int32_t association,
+                    int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (int rc = ash_insert_claim(m, keys, n, out_idx, out_mask, stream)) return rc;
+  if (int rc = ash_insert_count(m, n, out_idx, out_mask, stream)) return rc;
+  return ash_insert_commit_lazy(m, keys, n, values, association, out_idx, out_mask, stream);
 }
 
 int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* stream) {

@@ -219,6 +219,9 @@ _SLOT_LIMIT = 0.75  # rebuild the table when non-EMPTY slots would pass this
 # (0 = one batch); exact for insert, see HashMap._pipelined
 INSERT_CHUNK = int(os.environ.get("ASH_INSERT_CHUNK", "0"))
 
+# deferred slot-state commit (ash_insert_lazy / ash_settle); 0 = eager sweep
+LAZY_COMMIT = os.environ.get("ASH_LAZY_COMMIT", "1") == "1"
+
 
 class HashMap:
     """Batch-parallel map from fixed-arity int32 keys to value buffers, on a
@@ -293,6 +296,16 @@ class HashMap:
         self._size_known = True
         self._top_ub = 0
         self._tombs_ub = 0
+        self._unsettled = False
+
+    def _settle(self) -> None:
+        """Write the slot states a deferred commit left PENDING (libash
+        ``ash_settle``: the table sweep of the last insert).  Every mutating
+        operation calls it first; finds resolve pending slots on the fly, so
+        an insert followed by finds and a clear() never pays the sweep."""
+        if self._unsettled:
+            call("ash_settle", self._ptr(), self._stream())
+            self._unsettled = False
 
     def _fill_struct(self) -> None:
         s = self._struct
@@ -479,6 +492,7 @@ class HashMap:
     def _rehash_into(self, new_capacity: int) -> None:
         """Rebuild: active rows in ascending index order become rows
         0..size-1 of fresh zeroed buffers (hashmap.py:326-332)."""
+        self._settle()
         size = self._sync_size()
         act = torch.empty(size, dtype=torch.int32, device=self._device)
         if size:
@@ -503,6 +517,7 @@ class HashMap:
         limit = int(_SLOT_LIMIT * self._n_slots)
         if self._top_ub + self._tombs_ub + m <= limit:
             return
+        self._settle()
         tombs = int(self._counters[_lib.CTR_TOMBS].item())
         size = self._sync_size()
         self._tombs_ub = tombs
@@ -513,6 +528,7 @@ class HashMap:
     def _rebuild_slots(self, n_slots: int) -> None:
         """Re-place every live slot into a fresh array of n_slots slots (same
         buffer indices; tombstones dropped)."""
+        self._settle()
         new_slots = torch.empty(n_slots * 4, dtype=torch.int32, device=self._device)
         call("ash_rebuild_table", self._ptr(), new_slots.data_ptr(), n_slots, self._stream())
         self._slots = new_slots
@@ -564,6 +580,8 @@ class HashMap:
         return BatchResult(res.indices.cpu(), res.masks.cpu())
 
     def _pipelined(self, keys_h: torch.Tensor, vals_h, op: str) -> BatchResult:
+        if op == "insert":
+            self._settle()
         """Chunked H2D / kernels / D2H overlap for a host batch (op = insert
         or find).  Caller holds the guard and has checked capacity."""
         m = keys_h.shape[0]
@@ -647,6 +665,7 @@ class HashMap:
     def _insert_like(self, keys: torch.Tensor, vals, association: bool, idx=None) -> BatchResult:
         m = keys.shape[0]
         dev = self._device
+        self._settle()
         if idx is None:
             idx = torch.empty(m, dtype=torch.int32, device=dev)
         msk = torch.empty(m, dtype=torch.uint8, device=dev)
@@ -677,8 +696,12 @@ class HashMap:
                     cp = vptr
                     if vals:
                         cp = (_lib.c_void_p * len(vals))(*[v[a:b].data_ptr() for v in vals])
-                    call("ash_insert", self._ptr(), keys[a:b].data_ptr(), b - a, cp, assoc,
-                         idx[a:b].data_ptr(), msk[a:b].data_ptr(), self._stream())
+                    if c < m:
+                        self._settle()  # a chunk's claim must see the previous chunk committed
+                    call("ash_insert_lazy" if LAZY_COMMIT else "ash_insert", self._ptr(),
+                         keys[a:b].data_ptr(), b - a, cp, assoc, idx[a:b].data_ptr(), msk[a:b].data_ptr(),
+                         self._stream())
+                    self._unsettled = LAZY_COMMIT
                 self._top_ub = min(self._capacity, self._top_ub + m)
                 break
             self._widen_for_claims(m)
@@ -688,8 +711,10 @@ class HashMap:
                  self._stream())
             winners = int(self._counters[_lib.CTR_WINNERS].item())
             if winners <= free:
-                call("ash_insert_commit", self._ptr(), keys.data_ptr(), m, vptr, assoc,
+                call("ash_insert_commit_lazy" if LAZY_COMMIT else "ash_insert_commit", self._ptr(),
+                     keys.data_ptr(), m, vptr, assoc,
                      idx.data_ptr(), msk.data_ptr(), self._stream())
+                self._unsettled = LAZY_COMMIT
                 self._top_ub = min(self._capacity, self._top_ub + winners)
                 break
             call("ash_insert_rollback", self._ptr(), m, idx.data_ptr(), self._stream())
@@ -778,6 +803,7 @@ class HashMap:
             m = keys.shape[0]
             out = torch.empty(m, dtype=torch.uint8, device=self._device)
             if m:
+                self._settle()
                 scratch = torch.empty(2 * m, dtype=torch.int32, device=self._device)
                 call("ash_erase", self._ptr(), keys.data_ptr(), m, out.data_ptr(),
                      scratch.data_ptr(), self._stream())
@@ -819,6 +845,7 @@ class HashMap:
             self._size_known = True
             self._top_ub = 0
             self._tombs_ub = 0
+            self._unsettled = False  # the reset discards the pending table
 
     # -- content helpers (hashmap.py:476-496) ----------------------------
 
