@@ -219,8 +219,11 @@ _SLOT_LIMIT = 0.75  # rebuild the table when non-EMPTY slots would pass this
 # (0 = one batch); exact for insert, see HashMap._pipelined
 INSERT_CHUNK = int(os.environ.get("ASH_INSERT_CHUNK", "0"))
 
-# deferred slot-state commit (ash_insert_lazy / ash_settle); 0 = eager sweep
-LAZY_COMMIT = os.environ.get("ASH_LAZY_COMMIT", "1") == "1"
+# deferred slot-state commit (ash_insert_lazy / ash_settle): opt-in.  The
+# sweep moves to the next mutating call, so it only saves work when a map is
+# cleared or dropped before it is mutated again; finds meanwhile resolve
+# PENDING slots through the rank words (~6% slower probes).  0 = eager sweep
+LAZY_COMMIT = os.environ.get("ASH_LAZY_COMMIT", "0") == "1"
 
 
 class HashMap:

@@ -19,6 +19,16 @@ def ash(cuda_ok):
     return ash
 
 
+@pytest.fixture(autouse=True)
+def lazy_default():
+    """The deferred commit is opt-in (ASH_LAZY_COMMIT=1); these tests turn it on."""
+    from paper_2110_00511_b200 import hashmap as hm
+    old = hm.LAZY_COMMIT
+    hm.LAZY_COMMIT = True
+    yield
+    hm.LAZY_COMMIT = old
+
+
 @contextlib.contextmanager
 def eager():
     from paper_2110_00511_b200 import hashmap as hm
@@ -35,7 +45,7 @@ def pair(ash, *args, **kw):
 
 
 def same(a, b):
-    if isinstance(a, tuple) or hasattr(a, "indices"):
+    if not isinstance(a, torch.Tensor):  # BatchResult (a tensor's .indices is a method)
         return torch.equal(a.indices, b.indices) and torch.equal(a.masks, b.masks)
     return torch.equal(a, b)
 
