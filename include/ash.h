@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ASH_ABI_VERSION 6
+#define ASH_ABI_VERSION 7
 
 #define ASH_OK 0
 #define ASH_ERR_INVALID 1   /* bad argument (caller bug) -> ValueError        */
@@ -49,6 +49,7 @@ extern "C" {
 
 #define ASH_FLAG_TABLE_FULL 1  /* a claim probe wrapped the table (or hit max_probe) */
 #define ASH_FLAG_RANGE 2       /* quantized coordinate outside int32 */
+#define ASH_FLAG_CAPACITY 4    /* a device-sized insert did not fit: nothing committed */
 
 /*
  * Map state.  Table slots are 16 bytes {w0, w1, w2, state}: the first three
@@ -212,7 +213,8 @@ int ash_quantize(const void* points, int32_t points_are_f64, int64_t n,
  * from an estimate, ws->max_probe bounding the probes) may overflow, which
  * sets ASH_FLAG_TABLE_FULL: the results are then invalid, the table must be
  * refilled with EMPTY and the call repeated with a larger one.
- * scratch_idx: n int32, scratch_mask: n bytes. */
+ * scratch_idx: n int32 (>= ceil(n / 32) used: word prefixes); scratch_mask:
+ * 8 * ceil(n / 32) bytes, 4-byte aligned (candidate / displaced bitmaps). */
 int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64,
                  int64_t n, double voxel, int32_t* out_coords, int64_t* out_sel,
                  int32_t* scratch_idx, uint8_t* scratch_mask, void* stream);
@@ -275,11 +277,53 @@ int ash_frame_candidates(const double* depth, int64_t height, int64_t width, con
 /* Fused candidates + dedup (the local activate of grid.py:140-142): the
  * frame's distinct block coordinates in first-occurrence order, written to
  * out_coords[0 .. ws->counters[ASH_CTR_COUNT]).  ws is an all-EMPTY workspace
- * table as for ash_voxelize (left EMPTY again); scratch: positions entries. */
+ * table as for ash_voxelize (left EMPTY again); scratch_idx: positions int32,
+ * scratch_mask: 8 * ceil(positions / 32) bytes. */
 int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t width,
                      const double* cam, const double* pose, double block_size, double trunc,
                      int32_t neighbor, int32_t* out_coords, int32_t* scratch_idx,
                      uint8_t* scratch_mask, void* stream);
+
+/* Device-sized batches: ash_find / ash_insert (claim + count + commit) on
+ * keys[0 .. *d_n), the length read on the device when each kernel starts;
+ * n_max >= *d_n bounds it (grids, scratch, tile workspace for n_max).  Lets
+ * one stream chain an op whose result count stays on the device (a dedup,
+ * a routed shard batch) into a map op with no host round trip.  The insert
+ * clears counters[FLAGS] first and checks capacity on the device: when the
+ * winners do not fit below capacity it commits nothing and sets
+ * ASH_FLAG_CAPACITY; a claim that cannot place a key within 4096 buckets
+ * sets ASH_FLAG_TABLE_FULL.  On either flag the caller runs
+ * ash_insert_rollback(m, *d_n, out_idx) (which also clears the flags) and
+ * redoes the batch on the host-checked path (growth / CapacityError,
+ * hashmap.py:389-396). */
+int ash_find_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_t* d_n,
+                int32_t* out_idx, uint8_t* out_mask, void* stream);
+int ash_insert_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_t* d_n,
+                  const void* const* values, int32_t association, int32_t* out_idx,
+                  uint8_t* out_mask, void* stream);
+
+/* VoxelBlockGrid.allocate_blocks map calls (tsdf/grid.py:136-150) as one
+ * stream-ordered sequence with no host round trip: the distinct rows of
+ * coords[0..n) in first-occurrence order -> out_blocks (ash_unique_rows on
+ * the workspace ws), then the global activate of those rows
+ * (ash_insert_dn, association = 1) -> out_gi / out_gmask.  status (device,
+ * int32[5]): [0] rows activated (0 when the workspace prefix overflowed:
+ * refill it and repeat on a larger one), [1] distinct rows, [2] workspace
+ * flags, [3] global flags (ASH_FLAG_CAPACITY / TABLE_FULL: roll back
+ * [0] claims and redo the activate on the host path), [4] new blocks.
+ * out_blocks: n x 3, out_gi / out_gmask: n entries; scratch as for
+ * ash_unique_rows; global tile workspace for n positions. */
+int ash_allocate_blocks(ash_map_t* global, ash_map_t* ws, const int32_t* coords, int64_t n,
+                        int32_t* out_blocks, int32_t* out_gi, uint8_t* out_gmask,
+                        int32_t* scratch_idx, uint8_t* scratch_mask, int32_t* status, void* stream);
+
+/* The same from a depth frame (candidates generated in-kernel, as
+ * ash_frame_blocks): VoxelBlockGrid.allocate_blocks(frame), grid.py:127-150. */
+int ash_allocate_frame(ash_map_t* global, ash_map_t* ws, const double* depth, int64_t height,
+                       int64_t width, const double* cam, const double* pose, double block_size,
+                       double trunc, int32_t neighbor, int32_t* out_blocks, int32_t* out_gi,
+                       uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
+                       int32_t* status, void* stream);
 
 /* Delegate-backend insert commit (hashmap.py:369-387), after
  * ash_insert_claim + ash_insert_count: position p owns heap[top + p]; every

@@ -16,7 +16,7 @@ MAX_VALUE_BUFFERS = 8
 CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT, CTR_TOP_BASE = 0, 1, 2, 3, 4, 5, 6
 CTR_HEAP_DIRTY = 7
 N_COUNTERS = 8
-FLAG_TABLE_FULL, FLAG_RANGE = 1, 2
+FLAG_TABLE_FULL, FLAG_RANGE, FLAG_CAPACITY = 1, 2, 4
 TILE = 2048  # positions per scan tile (csrc kTile)
 
 
@@ -57,6 +57,13 @@ _SIGNATURES = {
     "ash_insert_commit_lazy": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                          c_void_p]),
     "ash_settle": (c_int32, [_M, c_void_p]),
+    "ash_find_dn": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ash_insert_dn": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "ash_allocate_blocks": (c_int32, [_M, _M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
+    "ash_allocate_frame": (c_int32, [_M, _M, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,
+                                     c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p]),
     "ash_insert_commit_delegate": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                              c_void_p, c_void_p]),
     "ash_heap_put_losers": (c_int32, [_M, c_void_p, c_int64, c_void_p]),
@@ -108,7 +115,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ash_abi_version() != 6:
+    if lib.ash_abi_version() != 7:
         raise ImportError("libash.so ABI version mismatch; rebuild")
     return lib
 

@@ -33,7 +33,7 @@ def unique_rows(keys: torch.Tensor) -> torch.Tensor:
         ws.reserve(n)
         out = torch.empty((n, 3), dtype=torch.int32, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
-        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        scratch_mask = torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev)  # cand / dem bitmaps
         count, _ = ws.run(lambda: call(
             "ash_unique_rows", ctypes.byref(ws.struct), keys.data_ptr(), n, out.data_ptr(), None,
             scratch_idx.data_ptr(), scratch_mask.data_ptr(), _stream_handle(dev)))
@@ -45,17 +45,78 @@ def allocate_blocks(global_map: HashMap, coords, threads: int = 1):
 
     Returns ``(gi, local_map)``: global indices of the frame's distinct blocks
     (first-occurrence order) and the local map (block -> global index).  The
-    distinct blocks come from one fused dedup pass; the local map — needed
-    only by frame-scoped queries (tsdf/raycast.py:32-35) — is built on first
-    use with the reference's indices (``LocalBlockMap``)."""
+    distinct blocks and the global activate run as one device sequence with
+    a single host read (libash ``ash_allocate_blocks``); the local map —
+    needed only by frame-scoped queries (tsdf/raycast.py:32-35) — is built on
+    first use with the reference's indices (``LocalBlockMap``)."""
     coords = global_map._check_keys(coords)
     if coords.shape[0] == 0:
         return torch.zeros(0, dtype=torch.int32, device=global_map.device), None
     if global_map.key_arity != 3:
         raise ValueError("block coordinates must have key arity 3")
-    survivors = unique_rows(coords.contiguous())
-    gi, gmask = global_map.activate(survivors)
-    return gi, LocalBlockMap(survivors, gi, coords.shape[0], global_map.device)
+    coords = coords.contiguous()
+    n = coords.shape[0]
+    if not _fused_ok(global_map):  # delegate semantics: the host-planned activate
+        survivors = unique_rows(coords)
+        gi, _ = global_map.activate(survivors)
+        return gi, LocalBlockMap(survivors, gi, n, global_map.device)
+    blocks, gi = _allocate_fused(
+        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, stream: call(
+            "ash_allocate_blocks", global_map._ptr(), ctypes.byref(ws.struct), coords.data_ptr(), n,
+            out.data_ptr(), gi_.data_ptr(), gm_.data_ptr(), si.data_ptr(), sm.data_ptr(), st.data_ptr(),
+            stream))
+    return gi, LocalBlockMap(blocks, gi, n, global_map.device)
+
+
+def _fused_ok(gm: HashMap) -> bool:
+    """The fused sequence activates with generic-backend semantics."""
+    return gm.backend_name != "delegate"
+
+
+def _allocate_fused(gm: HashMap, n: int, launch):
+    """Dedup + global activate as one device sequence (ash_allocate_blocks /
+    ash_allocate_frame): one host read of the 5-word status.  Falls back to
+    the host-checked activate (growth, CapacityError) when the device guard
+    reports that the new blocks did not fit.  Returns (blocks, gi)."""
+    from .geometry import _VoxelWorkspace
+    dev = gm.device
+    ws = _VoxelWorkspace.get(dev)
+    with _VoxelWorkspace._lock, torch.cuda.device(dev), gm._guard.writing():
+        gm._settle()
+        ws.reserve(n)
+        gm._ensure_scan(n)
+        # the new blocks are at most capacity - size (else the device guard
+        # rejects the batch): keep even that many claims under the slot limit
+        gm._reserve_slots(max(gm._capacity - gm._top_ub, 0))
+        out = torch.empty((n, 3), dtype=torch.int32, device=dev)
+        gi = torch.empty(n, dtype=torch.int32, device=dev)
+        gmask = torch.empty(n, dtype=torch.uint8, device=dev)
+        scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
+        scratch_mask = torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev)  # cand / dem bitmaps
+        status = torch.empty(5, dtype=torch.int32, device=dev)
+        stream = _stream_handle(dev)
+        for slots, probe in ws.attempts():
+            ws.use(slots, probe)
+            launch(ws, out, gi, gmask, scratch_idx, scratch_mask, status, stream)
+            rows, count, wflags, gflags, winners = status.tolist()  # the one host read
+            if probe and wflags & _lib.FLAG_TABLE_FULL:
+                continue  # the workspace prefix overflowed (the global map was not touched)
+            ws.estimate = count
+            break
+        else:  # unreachable: the full workspace table holds every distinct row
+            raise RuntimeError("voxel workspace overflow")
+        if wflags & _lib.FLAG_RANGE:
+            raise ValueError("block coordinates exceed int32 range")
+        gm._size_known = False
+        if gflags & (_lib.FLAG_CAPACITY | _lib.FLAG_TABLE_FULL):
+            # nothing committed: undo the claims, then the host-checked
+            # activate (doubling growth, hashmap.py:389-396)
+            call("ash_insert_rollback", gm._ptr(), rows, gi.data_ptr(), stream)
+            gm._tombs_ub += rows
+            gi = gm._insert_like(out[:count], None, association=True).indices
+        else:
+            gm._top_ub = min(gm._capacity, gm._top_ub + winners)
+    return out[:count], gi[:count]
 
 
 class BlockGrid:
@@ -170,7 +231,7 @@ def frame_blocks(depth, intrinsics, pose, block_size: float, trunc: float,
         ws.reserve(n)
         coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
-        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        scratch_mask = torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev)  # cand / dem bitmaps
         count, flags = ws.run(lambda: call(
             "ash_frame_blocks", ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c, float(block_size),
             float(trunc), nb, coords.data_ptr(), scratch_idx.data_ptr(), scratch_mask.data_ptr(),
@@ -207,18 +268,31 @@ class LocalBlockMap:
 def allocate_frame(global_map: HashMap, depth, intrinsics, pose, block_size: float, trunc: float,
                    depth_min: float = 0.2, depth_max: float = 3.0, allocation: str = "ray"):
     """VoxelBlockGrid.allocate_blocks (tsdf/grid.py:127-150) from the depth
-    image: fused candidate dedup, then the global activate whose indices are
-    the frame's global buffer indices (the reference's follow-up find returns
-    the same indices).  Returns ``(gi, local_map)``."""
+    image: candidate generation, dedup and the global activate (whose
+    indices are the frame's global buffer indices; the reference's follow-up
+    find returns the same) as one device sequence with a single host read
+    (libash ``ash_allocate_frame``).  Returns ``(gi, local_map)``."""
     dev = global_map.device
-    blocks = frame_blocks(depth, intrinsics, pose, block_size, trunc, depth_min, depth_max,
-                          allocation, device=dev)
+    if global_map.key_arity != 3:
+        raise ValueError("block coordinates must have key arity 3")
+    d, h, w, cam, pose_c, nb = _frame_args(depth, intrinsics, pose, block_size, trunc, depth_min,
+                                           depth_max, allocation, dev)
+    n = int(_lib.lib.ash_frame_positions(h, w, float(block_size), float(trunc), nb))
+    if n == 0:
+        return torch.zeros(0, dtype=torch.int32, device=dev), None
+    if not _fused_ok(global_map):
+        blocks = frame_blocks(depth, intrinsics, pose, block_size, trunc, depth_min, depth_max,
+                              allocation, device=dev)
+        gi = global_map.activate(blocks).indices if blocks.shape[0] else blocks[:0, 0]
+    else:
+        blocks, gi = _allocate_fused(
+        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, stream: call(
+            "ash_allocate_frame", global_map._ptr(), ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c,
+                float(block_size), float(trunc), nb, out.data_ptr(), gi_.data_ptr(), gm_.data_ptr(),
+                si.data_ptr(), sm.data_ptr(), st.data_ptr(), stream))
     if blocks.shape[0] == 0:
         return torch.zeros(0, dtype=torch.int32, device=dev), None
-    gi, gmask = global_map.activate(blocks)
-    d = depth if isinstance(depth, torch.Tensor) else torch.from_numpy(np.asarray(depth, np.float64))
-    per_pixel = int(_lib.lib.ash_frame_positions(1, 1, float(block_size), float(trunc),
-                                                 int(allocation == "neighbor")))
+    per_pixel = n // (h * w)
 
     def n_candidates():  # valid pixels x samples (Frame.valid_mask, tsdf/types.py:67-69)
         valid = (d > 0) & (d >= depth_min) & (d <= depth_max)

@@ -429,6 +429,27 @@ __device__ __forceinline__ uint32_t settle_index(const Settle& z, uint32_t j) {
   return ident ? top + rank : static_cast<uint32_t>(__ldg(z.heap + top + rank));
 }
 
+// Device-sized batches (ash_insert_dn / ash_find_dn): the batch length is
+// min(n, *d_n), read when the kernel starts; n (the host's bound) sizes the
+// grid and the scratch.
+__device__ __forceinline__ int64_t dev_len(int64_t n, const int32_t* d_n) {
+  if (!d_n) return n;
+  const int64_t v = ld_volatile_i32(d_n);
+  return v < 0 ? 0 : (v < n ? v : n);
+}
+
+// Capacity guard of the commits (hashmap.py:389-396 raises before any
+// change): the batch's winners must fit below capacity.  A batch that does
+// not fit commits nothing and sets ASH_FLAG_CAPACITY; the caller rolls the
+// claims back.  Host-checked batches always fit.
+__device__ __forceinline__ bool commit_fits(int32_t* counters, int64_t capacity) {
+  const int64_t need = static_cast<int64_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE)) +
+                       ld_volatile_i32(counters + ASH_CTR_WINNERS);
+  if (need <= capacity) return true;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_CAPACITY);
+  return false;
+}
+
 // Read-only probe (find / erase): returns the buffer index or -1; slot out.
 template <int A>
 __device__ __forceinline__ int32_t probe_find(const Table& t, const Key<A>& k, uint32_t h,
@@ -557,8 +578,9 @@ __global__ void k_fill_empty(uint4* slots, int64_t n_slots) {
 template <int A, int B = kBlock>
 __global__ void __launch_bounds__(B) k_find(Table t, const int32_t* __restrict__ keys, int64_t n,
                                             int32_t* __restrict__ out_idx,
-                                            uint8_t* __restrict__ out_mask, Settle z) {
+                                            uint8_t* __restrict__ out_mask, Settle z, const int32_t* d_n) {
   __shared__ uint32_t stage[B * 3];
+  n = dev_len(n, d_n);
   const int64_t p = blockIdx.x * static_cast<int64_t>(B) + threadIdx.x;
   const uint64_t pol = stream_policy(t.hints);
   Key<A> k = load_key_warp<A>(keys, p, n, t.arity, stage, pol);
@@ -660,8 +682,10 @@ constexpr int kClaimBlock = 128;
 template <int A, int B = kBlock>
 __global__ void __launch_bounds__(B) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                                  int32_t* counters, int32_t* tile_cnt) {
+                                                  int32_t* counters, int32_t* tile_cnt, const int32_t* d_n) {
   constexpr int R = kClaimRounds;
+  n = dev_len(n, d_n);
+  if (blockIdx.x * static_cast<int64_t>(B * R) >= n) return;  // past a device-sized batch
   __shared__ uint32_t stage[R][B * 3];
   const int lane = threadIdx.x & 31;
   const int64_t blk = blockIdx.x * static_cast<int64_t>(B * R);
@@ -913,7 +937,9 @@ constexpr int kScanBlock = 1024;
 // With pre_out, the exclusive prefixes (plus the total at [n_tiles]) go to
 // pre_out and the counts are zeroed in place for the next batch.
 __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int64_t n_tiles, int32_t* counters,
-                                                          int top_slot, int total_slot, int32_t* pre_out) {
+                                                          int top_slot, int total_slot, int32_t* pre_out,
+                                                          const int32_t* d_n) {
+  if (d_n) n_tiles = (dev_len(n_tiles * kTile, d_n) + kTile - 1) / kTile;
   __shared__ int32_t warp_tot[kScanBlock / 32];
   __shared__ int32_t carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1012,9 +1038,13 @@ __global__ void __launch_bounds__(kBlock)
     k_commit(Table t, const int32_t* __restrict__ keys, int64_t n, ValueArgs va, int assoc,
              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
              uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
-             int32_t* tile_pre, int64_t sweep_min, int32_t* __restrict__ rank_words) {
+             int32_t* tile_pre, int64_t sweep_min, int32_t* __restrict__ rank_words, int64_t capacity,
+             const int32_t* d_n) {
   __shared__ ScanSmem sm;
+  n = dev_len(n, d_n);
+  if (!commit_fits(counters, capacity)) return;
   const int64_t tile = blockIdx.x;
+  if (tile * kTile >= n) return;
   const int64_t base = tile * kTile;
   const uint64_t pol = stream_policy(t.hints);
   // large batches leave the slot states to k_commit_sweep (see there); the
@@ -1205,9 +1235,14 @@ __global__ void __launch_bounds__(kCommitThreads)
                   int32_t* __restrict__ tmp, uint8_t* __restrict__ mask, const int32_t* __restrict__ heap,
                   int64_t capacity, uint8_t* __restrict__ active, int32_t* __restrict__ key_buf,
                   int32_t* counters, const int32_t* __restrict__ tile_pre, int64_t n_tiles,
-                  int64_t sweep_min, int32_t* __restrict__ rank_words) {
+                  int64_t sweep_min, int32_t* __restrict__ rank_words, const int32_t* d_n) {
   constexpr int SV = (VW > 0 && VW <= 4) ? VW : 0;
   using L = CommitStage<A, SV>;
+  if (d_n) {
+    n = dev_len(n, d_n);
+    n_tiles = (n + kTile - 1) / kTile;
+  }
+  if (!commit_fits(counters, capacity) || blockIdx.x >= n_tiles) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kCommitStages], empty[kCommitStages];
   __shared__ CommitStageInfo info[kCommitStages];
@@ -1252,7 +1287,6 @@ __global__ void __launch_bounds__(kCommitThreads)
         tx += stage_range(st + L::kKeys, keys + base * A, rows * A * 4, &full[s], pol);
         if (SV) tx += stage_range(st + L::kVals, va.src[0] + base * SV * 4, rows * SV * 4, &full[s], pol);
         if (he > hs) tx += stage_range(st + L::kHeap, heap + hs_al, (he - hs_al) * 4, &full[s], pol);
-        (void)capacity;
         mbar_arrive_expect_tx(&full[s], tx);
       }
     }
@@ -1387,6 +1421,7 @@ __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t*
                                                          const int32_t* __restrict__ heap,
                                                          const int32_t* counters, int64_t sweep_min) {
   if (ld_volatile_i32(counters + ASH_CTR_WINNERS) < sweep_min) return;
+  if (ld_volatile_i32(counters + ASH_CTR_FLAGS) & ASH_FLAG_CAPACITY) return;  // nothing was committed
   const uint32_t stride = gridDim.x * kBlock;
   const uint32_t top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
   // fresh heap region (no frees at or above top): index = top + rank
@@ -1649,6 +1684,8 @@ template <typename T, bool STAGED = true>
 struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
   static constexpr bool kStaged = STAGED;  // full warps stage their 32 rows with 16-byte loads (aligned clouds)
   static constexpr int kRowBytes = 3 * sizeof(T);
+  static constexpr int kGroup = 1;  // runs of points in one voxel (previous lane only)
+  __device__ __forceinline__ int period() const { return 0; }
   const T* pts;
   double cell;
   double rcell;  // RN(1 / cell), for quantize_fast
@@ -1682,6 +1719,8 @@ struct CloudSrc {  // geometry.py:49-76: floor(float64(p) / cell)
 struct RowSrc {  // int3 key rows as given (the local activate of grid.py:140-142)
   static constexpr bool kStaged = false;
   static constexpr int kRowBytes = 16;
+  static constexpr int kGroup = 2;  // block candidates repeat within a warp: any lower lane
+  __device__ __forceinline__ int period() const { return 0; }
   __device__ __forceinline__ bool key_staged(int64_t, Key<3>&, bool*, uint4*) const { return false; }
   const int32_t* keys;
   __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool*) const {
@@ -1703,6 +1742,10 @@ struct RowSrc {  // int3 key rows as given (the local activate of grid.py:140-14
 struct FrameSrc {
   static constexpr bool kStaged = false;
   static constexpr int kRowBytes = 16;
+  // a pixel's block repeats at the same sample of the next pixel (one
+  // period back) and often along the ray (previous lane)
+  static constexpr int kGroup = 1;
+  __device__ __forceinline__ int period() const { return per_pixel; }
   __device__ __forceinline__ bool key_staged(int64_t, Key<3>&, bool*, uint4*) const { return false; }
   const double* depth;
   int64_t width;
@@ -1739,10 +1782,84 @@ struct FrameSrc {
   }
 };
 
-template <typename Src, int B = kBlock>
-__global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, int32_t* __restrict__ tmp,
-                                                   uint8_t* __restrict__ mask, int32_t* counters,
-                                                   int32_t* tile_cnt) {
+// ---------------------------------------------------------------------------
+// dedup-select path (voxelize / unique rows / frame blocks): the first
+// occurrence of every distinct key, in ascending position order
+// (geometry.py:59-76 flatnonzero(HashSet.insert(coords).masks); the local
+// activate + survivor gather of tsdf/grid.py:140-142).
+//
+//   claim  each position whose key does not repeat a (valid) lower lane of
+//          its warp probes the all-EMPTY workspace table; the key's slot
+//          ends up holding PENDING | min(position) (CAS on EMPTY, atomicMin
+//          on a PENDING state).  A position that takes a slot (CAS) or
+//          displaces a higher one (atomicMin) is a candidate: its bit is set
+//          in `cand`, and the displaced position's bit in `dem` (both
+//          monotonic ORs: no ordering race between a claimer and its
+//          displacer); exact per-tile winner counts (+1 / -1).  A duplicate
+//          that finds a lower position costs one L2 probe and no store.
+//   scan   exclusive prefix of the tile counts (k_tile_scan).
+//   words  per 32 positions: winners = cand & ~dem, exclusive word prefix.
+//   emit   one sequential pass over the table prefix in use: every
+//          PENDING|p slot is winner p; its rank is word_pre + the winners
+//          below p in its word; key (from the slot) and p go to the outputs
+//          and the slot is EMPTY again.  Only small arrays (bitmaps, word
+//          prefixes, outputs) are touched at random.
+
+// The workspace is private to this path, so it uses a cheaper hash than the
+// map's murmur chain (a multiply-rotate combine + the murmur finaliser).
+__device__ __forceinline__ uint32_t dd_hash(const Key<3>& k) {
+  return fmix32((k.w[0] * 0x9E3779B1u) ^ rotl32(k.w[1] * 0x85EBCA77u, 11) ^ rotl32(k.w[2] * 0xC2B2AE3Du, 22));
+}
+
+// True when p becomes a candidate (took a slot, or displaced a higher
+// position, whose `dem` bit it sets).
+__device__ __forceinline__ bool dd_claim_probe(const Table& t, const Key<3>& k, uint32_t h, uint32_t p,
+                                               int32_t* counters, uint32_t* dem) {
+  const uint32_t me = PEND | p;
+  uint32_t b = home_bucket(h, t.n_buckets);
+  int first = 0;
+  uint32_t scanned = 0;
+  while (true) {
+    uint32_t w[8];
+    ld256_relaxed(t.slots + 2 * static_cast<size_t>(b), w);
+    int retry = -1;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s < first || retry >= 0) continue;
+      const uint32_t slot = 2 * b + s;
+      const uint32_t st = w[4 * s + 3];
+      if (st == EMPTY) {
+        if (cas128(t.slots + slot, make_uint4(w[4 * s], w[4 * s + 1], w[4 * s + 2], st),
+                   make_uint4(k.w[0], k.w[1], k.w[2], me)))
+          return true;
+        retry = s;  // taken meanwhile (maybe by our key): look at it again
+      } else if (w[4 * s] == k.w[0] && w[4 * s + 1] == k.w[1] && w[4 * s + 2] == k.w[2]) {
+        if (st < me) return false;
+        const uint32_t old = atomicMin(&t.slots[slot].w, me);
+        if (old < me) return false;
+        const uint32_t q = old & ~PEND;
+        atomicOr(&dem[q >> 5], 1u << (q & 31));
+        return true;
+      }
+    }
+    if (retry >= 0) {
+      first = retry;
+      continue;
+    }
+    first = 0;
+    b = next_bucket(b, t.n_buckets);
+    if (++scanned >= t.max_scan) {
+      atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_TABLE_FULL);
+      return false;
+    }
+  }
+}
+
+// 16 blocks of 128 per SM (32 registers): the claim is latency-bound, and
+// 36 registers (12 blocks) cost 20% at configs[2]
+template <typename Src, int B = 128>
+__global__ void __launch_bounds__(B, 2048 / B) k_dd_claim(Table t, Src src, int64_t n, int32_t* counters,
+                                                uint32_t* __restrict__ cand, uint32_t* __restrict__ dem) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(B) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool inside = p < n;
@@ -1760,89 +1877,74 @@ __global__ void __launch_bounds__(B) k_voxel_claim(Table t, Src src, int64_t n, 
     has = src.key(p, k, &bad);
   }
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
-  const bool skip = bad || !has;  // out-of-range points never claim; the host raises first
-  const uint32_t h = hash_key<3>(k, 3);
-  int leader;
-  if (Src::kStaged) {
-    // point clouds: equal keys are grouped only where they are adjacent in
-    // the batch (a run of points in one voxel: 3 shuffles + a ballot);
-    // __match_any_sync kept this kernel ADU-bound (303 -> ~240 us without
-    // it at configs[2]), and duplicates elsewhere resolve in the table
-    // exactly as they do across warps
+  const bool valid = has && !bad;  // out-of-range points never claim; the host raises
+  const uint32_t h = dd_hash(k);
+  // a position whose key equals that of a valid lower lane can never be a
+  // first occurrence: it skips the table (the lower position, or one lower
+  // still, claims)
+  bool dup = false;
+  if (Src::kGroup == 1) {  // the previous lane, and the lane one period back
+    const unsigned vmask = __ballot_sync(live, valid);
     const uint32_t u0 = __shfl_up_sync(live, k.w[0], 1), u1 = __shfl_up_sync(live, k.w[1], 1),
                    u2 = __shfl_up_sync(live, k.w[2], 1);
-    const bool skip_prev = __shfl_up_sync(live, static_cast<int>(skip), 1) != 0;
-    const bool head = lane == 0 || skip || skip_prev || u0 != k.w[0] || u1 != k.w[1] || u2 != k.w[2];
-    const unsigned heads = __ballot_sync(live, head);
-    leader = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-  } else {
-    unsigned grp = __match_any_sync(live, h);
-    if (__any_sync(live, __popc(grp) > 1)) {
-      unsigned g2;
-      same_key_in_warp<3>(k, live, &g2);
-      grp &= g2;
+    dup = lane > 0 && ((vmask >> (lane - 1)) & 1) && u0 == k.w[0] && u1 == k.w[1] && u2 == k.w[2];
+    const int per = src.period();
+    if (per > 1 && per < 32) {
+      const int q = lane >= per ? lane - per : lane;
+      const uint32_t v0 = __shfl_sync(live, k.w[0], q), v1 = __shfl_sync(live, k.w[1], q),
+                     v2 = __shfl_sync(live, k.w[2], q);
+      dup = dup || (lane >= per && ((vmask >> q) & 1) && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2]);
     }
-    const unsigned skip_lanes = __ballot_sync(live, skip);
-    grp &= ~skip_lanes;
-    if (skip) grp = 1u << lane;
-    leader = __ffs(grp) - 1;
+  } else if (Src::kGroup == 2) {  // any lower lane: match on the hash, verify the lowest
+    const unsigned vmask = __ballot_sync(live, valid);
+    const unsigned grp = __match_any_sync(live, h) & vmask;
+    const int low = __ffs(grp) - 1;
+    const int src_lane = low < 0 ? lane : low;
+    const uint32_t v0 = __shfl_sync(live, k.w[0], src_lane), v1 = __shfl_sync(live, k.w[1], src_lane),
+                   v2 = __shfl_sync(live, k.w[2], src_lane);
+    dup = low >= 0 && low < lane && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2];
   }
-  uint32_t res = PEND;
-  bool claimed_tomb = false, candidate = false;
-  if (lane == leader && !skip)
-    res = probe_claim<3>(t, k, h, static_cast<uint32_t>(p), nullptr, mask, counters, tile_cnt, &claimed_tomb,
-                         &candidate);
+  const bool ev = valid && !dup && dd_claim_probe(t, k, h, static_cast<uint32_t>(p), counters, dem);
   __syncwarp(live);
-  const unsigned cand = __ballot_sync(live, candidate);
-  if (cand && lane == __ffs(live) - 1) atomicAdd(&tile_cnt[p / kTile], __popc(cand));
-  // the select reads tmp (the claimed slot) for winners only, and only a
-  // candidate can win: everything else is DEMOTED (by probe_claim for
-  // leaders that lost, here for in-warp duplicates and skipped positions)
-  if (lane == leader && !skip) {
-    if (candidate) tmp[p] = static_cast<int32_t>(res);
-  } else {
-    mask[p] = DEMOTED;
+  // the warp's 32 positions share one bitmap word (blocks of B positions
+  // are B-aligned).  Per-tile counts come from the bitmaps afterwards
+  // (k_dd_count): counting here put ~64 warps' atomics on each tile word.
+  const unsigned cb = __ballot_sync(live, ev);
+  if (cb && lane == __ffs(live) - 1) atomicOr(&cand[p >> 5], cb);
+}
+
+// winners per 256 bitmap words (8192 positions: one k_dd_words block) ->
+// blk_cnt (plain stores; scanned by k_tile_scan)
+__global__ void __launch_bounds__(kBlock)
+    k_dd_count(int64_t n, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
+               int32_t* __restrict__ blk_cnt) {
+  __shared__ int32_t s_warp[kWarps];
+  const int64_t n_words = (n + 31) / 32;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  int32_t c = w < n_words ? __popc(__ldg(cand + w) & ~__ldg(dem + w)) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) sum += s_warp[i];
+    blk_cnt[blockIdx.x] = sum;
   }
 }
 
-constexpr int kSelTiles = 32 * kBlock / kTile;  // scan tiles per select block (32 positions per thread)
-
-template <typename Src>
+// winners per 32-position word -> exclusive word prefixes (ranks of the word's
+// first winner), from the exclusive per-block prefixes of k_dd_count
 __global__ void __launch_bounds__(kBlock)
-    k_voxel_select(uint4* slots, Src src, int64_t n, const int32_t* __restrict__ tmp,
-                   const uint8_t* __restrict__ mask, int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel,
-                   int32_t* tile_pre) {
+    k_dd_words(int64_t n, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
+               int32_t* __restrict__ word_pre, const int32_t* blk_pre) {
   __shared__ int32_t s_warp[kWarps];
   __shared__ int32_t s_prefix;
-  // one block per kSelTiles scan tiles; 32 consecutive positions per thread
-  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kSelTiles, base = tile0 * kTile;
-  const int64_t n_tiles = (n + kTile - 1) / kTile;
+  const int64_t n_words = (n + 31) / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // On the all-EMPTY workspace every position leaves the claim PENDING
-  // (tmp < 0) and every non-winner DEMOTED, so the winners are exactly the
-  // un-demoted positions: only the 1-byte masks are streamed here (four
-  // independent 8-byte loads per thread), and the claim's slot words are
-  // read for the winners alone (3.5% at configs[2]).
-  const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * 32;
-  uint32_t bits = 0;
-  if (p0 + 32 <= n && (reinterpret_cast<uintptr_t>(mask) & 7) == 0) {
-    uint2 m8[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) m8[q] = __ldg(reinterpret_cast<const uint2*>(mask + p0) + q);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (!((m8[q].x >> (8 * j)) & DEMOTED)) bits |= 1u << (8 * q + j);
-        if (!((m8[q].y >> (8 * j)) & DEMOTED)) bits |= 1u << (8 * q + j + 4);
-      }
-  } else {
-    for (int j = 0; j < 32; ++j)
-      if (p0 + j < n && !(__ldg(mask + p0 + j) & DEMOTED)) bits |= 1u << j;
-  }
-  // block exclusive scan of the per-thread winner counts (thread order =
-  // position order), plus the first tile's prefix from the tile scan
-  const int32_t cnt = __popc(bits);
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  const int32_t cnt = w < n_words ? __popc(__ldg(cand + w) & ~__ldg(dem + w)) : 0;
   int32_t incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1850,27 +1952,29 @@ __global__ void __launch_bounds__(kBlock)
     if (lane >= o) incl += y;
   }
   if (lane == 31) s_warp[warp] = incl;
-  if (threadIdx.x == 0) s_prefix = tile_pre[tile0];
+  if (threadIdx.x == 0) s_prefix = blk_pre[blockIdx.x];
   __syncthreads();
-  // the counts are zero between calls (every prefix of this block is read)
-  if (threadIdx.x < kSelTiles && tile0 + threadIdx.x < n_tiles) tile_pre[tile0 + threadIdx.x] = 0;
   int32_t before = s_prefix + incl - cnt;
-  for (int w = 0; w < warp; ++w) before += s_warp[w];
-  while (bits) {
-    const int j = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const int64_t p = p0 + j;
-    const uint32_t r = static_cast<uint32_t>(before++);
-    // the winner's key words are in its claimed slot (L2-hot: the workspace
-    // is sized to stay resident), no need to regenerate them from the source
-    const uint32_t slot = static_cast<uint32_t>(__ldg(tmp + p)) & SLOT_MASK;
-    const uint4 sv = slots[slot];
-    out_coords[3 * static_cast<int64_t>(r)] = static_cast<int32_t>(sv.x);
-    out_coords[3 * static_cast<int64_t>(r) + 1] = static_cast<int32_t>(sv.y);
-    out_coords[3 * static_cast<int64_t>(r) + 2] = static_cast<int32_t>(sv.z);
+  for (int i = 0; i < warp; ++i) before += s_warp[i];
+  if (w < n_words) word_pre[w] = before;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_dd_emit(uint4* slots, uint32_t n_slots, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
+              const int32_t* __restrict__ word_pre, int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel) {
+  const uint32_t stride = gridDim.x * kBlock;
+  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n_slots; i += stride) {
+    const uint4 sv = slots[i];
+    if ((sv.w & 0xC0000000u) != PEND) continue;  // EMPTY (the workspace has no tombstones)
+    const uint32_t p = sv.w & SLOT_MASK;
+    const uint32_t wi = p >> 5;
+    const uint32_t below = (__ldg(cand + wi) & ~__ldg(dem + wi)) & ((1u << (p & 31)) - 1u);
+    const int64_t r = __ldg(word_pre + wi) + __popc(below);
+    out_coords[3 * r] = static_cast<int32_t>(sv.x);
+    out_coords[3 * r + 1] = static_cast<int32_t>(sv.y);
+    out_coords[3 * r + 2] = static_cast<int32_t>(sv.z);
     if (out_sel) out_sel[r] = p;
-    // leave the workspace table EMPTY for the next call
-    slots[slot] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+    slots[i] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);  // the workspace is EMPTY again
   }
 }
 
@@ -1938,8 +2042,9 @@ int32_t* split_prefix(const ash_map_t* m, int64_t n) {
 }
 
 void launch_tile_scan(const ash_map_t* m, int64_t n, int top_slot, int total_slot, cudaStream_t s,
-                      int32_t* pre_out = nullptr) {
-  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot, pre_out); note_launch();
+                      int32_t* pre_out = nullptr, const int32_t* d_n = nullptr) {
+  k_tile_scan<<<1, kScanBlock, 0, s>>>(m->tile_counts, tiles_for(n), m->counters, top_slot, total_slot, pre_out, d_n);
+  note_launch();
 }
 
 int check_scan(const ash_map_t* m, int64_t n) {
@@ -2013,7 +2118,7 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
 template <int A, int VW>
 int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const ValueArgs& va, int assoc,
                        int32_t* out_idx, uint8_t* out_mask, const ash_map_t* m, const int32_t* pre,
-                       int64_t sweep_min, int32_t* rank_words, cudaStream_t s) {
+                       int64_t sweep_min, int32_t* rank_words, const int32_t* d_n, cudaStream_t s) {
   constexpr int SV = (VW > 0 && VW <= 4) ? VW : 0;
   constexpr size_t smem = kCommitStages * CommitStage<A, SV>::kBytes;
   // the >48 KB dynamic shared memory opt-in and the occupancy, per device
@@ -2032,7 +2137,7 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
   const unsigned grid = static_cast<unsigned>(T < cap ? T : cap);
   k_commit_bulk<A, VW><<<grid, kCommitThreads, smem, s>>>(t, keys, n, va, assoc, out_idx, out_mask, m->heap,
                                                           m->capacity, m->active, m->key_buf, m->counters, pre, T,
-                                                          sweep_min, rank_words); note_launch();
+                                                          sweep_min, rank_words, d_n); note_launch();
   return ASH_OK;
 }
 
@@ -2044,16 +2149,27 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
     default: { constexpr int A = 0; KERNEL_CALL; note_launch(); break; } \
   }
 
+// scratch_mask: the cand / dem bitmaps (2 x ceil(n / 32) words);
+// scratch_idx: the word prefixes (ceil(n / 32) words)
 template <typename Src>
 void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
                       int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s) {
-  // 128-thread blocks: configs[2] 0.501 ms against 0.513 at 256 (r01m A/B)
-  k_voxel_claim<Src, 128><<<grid_for(n, 128), 128, 0, s>>>(t, src, n, scratch_idx, scratch_mask, ws->counters,
-                                                           ws->tile_counts);
+  const int64_t words = (n + 31) / 32;
+  uint32_t* cand = reinterpret_cast<uint32_t*>(scratch_mask);
+  uint32_t* dem = cand + words;
+  cudaMemsetAsync(cand, 0, sizeof(uint32_t) * 2 * words, s);
+  k_dd_claim<Src, 128><<<grid_for(n, 128), 128, 0, s>>>(t, src, n, ws->counters, cand, dem);
   note_launch();
-  launch_tile_scan(ws, n, -1, ASH_CTR_COUNT, s);
-  k_voxel_select<Src><<<grid_for(n, kTile * kSelTiles), kBlock, 0, s>>>(t.slots, src, n, scratch_idx, scratch_mask,
-                                                                         out_coords, out_sel, ws->tile_counts);
+  const unsigned wg = grid_for(words, kBlock);
+  k_dd_count<<<wg, kBlock, 0, s>>>(n, cand, dem, ws->tile_counts);
+  note_launch();
+  k_tile_scan<<<1, kScanBlock, 0, s>>>(ws->tile_counts, wg, ws->counters, -1, ASH_CTR_COUNT, nullptr, nullptr);
+  note_launch();
+  k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts);
+  note_launch();
+  const unsigned cap = static_cast<unsigned>(device_sms()) * 8;
+  const unsigned eg = grid_for(t.n_slots, kBlock);
+  k_dd_emit<<<eg < cap ? eg : cap, kBlock, 0, s>>>(t.slots, t.n_slots, cand, dem, scratch_idx, out_coords, out_sel);
   note_launch();
 }
 
@@ -2082,6 +2198,40 @@ int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t wid
   }
   *n = height * width * f->per_pixel;
   return check_batch(*n);
+}
+
+// status[0] = rows the global activate takes (0 when the dedup overflowed
+// its workspace prefix or met an out-of-range block), [1] = distinct rows, [2] = workspace flags; after
+// the activate [3] = global flags, [4] = new blocks.
+__global__ void k_alloc_status(const int32_t* ws_counters, const int32_t* g_counters, int32_t* status, int phase) {
+  if (phase == 0) {
+    const int32_t count = ws_counters[ASH_CTR_COUNT], flags = ws_counters[ASH_CTR_FLAGS];
+    // an overflowed workspace or an out-of-range block leaves the map untouched
+    status[0] = (flags & (ASH_FLAG_TABLE_FULL | ASH_FLAG_RANGE)) ? 0 : count;
+    status[1] = count;
+    status[2] = flags;
+  } else {
+    status[3] = g_counters[ASH_CTR_FLAGS];
+    status[4] = g_counters[ASH_CTR_WINNERS];
+  }
+}
+
+template <typename Src>
+static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_blocks,
+                          int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
+                          int32_t* status, cudaStream_t s) {
+  if (int rc = check_map(global)) return rc;
+  if (global->arity != 3) return fail(ASH_ERR_INVALID, "block coordinates need key arity 3");
+  if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
+  if (int rc = check_tiles(ws, n)) return rc;
+  if (!out_blocks || !out_gi || !out_gmask || !scratch_idx || !scratch_mask || !status)
+    return fail(ASH_ERR_INVALID, "null output pointer");
+  cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
+  run_dedup_select(make_table(ws), ws, src, n, out_blocks, nullptr, scratch_idx, scratch_mask, s);
+  k_alloc_status<<<1, 1, 0, s>>>(ws->counters, global->counters, status, 0); note_launch();
+  if (int rc = ash_insert_dn(global, out_blocks, n, status, nullptr, 1, out_gi, out_gmask, s)) return rc;
+  k_alloc_status<<<1, 1, 0, s>>>(ws->counters, global->counters, status, 1); note_launch();
+  return check_launch("ash_allocate_blocks");
 }
 
 }  // namespace
@@ -2140,7 +2290,8 @@ int ash_map_reset(ash_map_t* m, int32_t zero_rows, void* stream) {
   return check_launch("ash_map_reset");
 }
 
-int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+static int find_impl(ash_map_t* m, const int32_t* keys, int64_t n, const int32_t* d_n, int32_t* out_idx,
+                     uint8_t* out_mask, void* stream) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
@@ -2149,8 +2300,18 @@ int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uin
   cudaStream_t s = as_stream(stream);
   // 256-thread blocks (128 within 1%, 512 1-4% slower; r01m A/B)
   ASH_DISPATCH_ARITY(m->arity, (k_find<A><<<grid_for(n, kBlock), kBlock, 0, s>>>(t, keys, n, out_idx, out_mask,
-                                                                                make_settle(m))));
+                                                                                make_settle(m), d_n)));
   return check_launch("ash_find");
+}
+
+int ash_find(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  return find_impl(m, keys, n, nullptr, out_idx, out_mask, stream);
+}
+
+int ash_find_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_t* d_n, int32_t* out_idx,
+                uint8_t* out_mask, void* stream) {
+  if (!d_n) return fail(ASH_ERR_INVALID, "null device length");
+  return find_impl(m, keys, n_max, d_n, out_idx, out_mask, stream);
 }
 
 int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, int32_t* out_idx,
@@ -2169,8 +2330,8 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
   return check_launch("ash_find_lattice");
 }
 
-int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
-                     void* stream) {
+static int claim_impl(ash_map_t* m, const int32_t* keys, int64_t n, const int32_t* d_n, int32_t* out_idx,
+                      uint8_t* out_mask, void* stream) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
@@ -2182,11 +2343,16 @@ int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_
   // 128-thread blocks: 0.302 ms against 0.310 at 256 and 0.330 at 512 (C2,
   // r01m A/B; 64 ties with 128): finer block turnover over the ~66 waves
   ASH_DISPATCH_ARITY(m->arity, (k_claim<A, kClaimBlock><<<grid_for(n, kClaimBlock * kClaimRounds), kClaimBlock, 0, s>>>(
-                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts)));
+                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts, d_n)));
   return check_launch("ash_insert_claim");
 }
 
-int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint8_t* out_mask, void* stream) {
+int ash_insert_claim(ash_map_t* m, const int32_t* keys, int64_t n, int32_t* out_idx, uint8_t* out_mask,
+                     void* stream) {
+  return claim_impl(m, keys, n, nullptr, out_idx, out_mask, stream);
+}
+
+static int count_impl(ash_map_t* m, int64_t n, const int32_t* d_n, void* stream) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   cudaStream_t s = as_stream(stream);
@@ -2195,14 +2361,19 @@ int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint
     return check_launch("ash_insert_count");
   }
   if (int rc = check_tiles(m, n)) return rc;
-  (void)out_idx;
-  (void)out_mask;
-  launch_tile_scan(m, n, ASH_CTR_TOP_BASE, ASH_CTR_WINNERS, s, split_prefix(m, n));
+  launch_tile_scan(m, n, ASH_CTR_TOP_BASE, ASH_CTR_WINNERS, s, split_prefix(m, n), d_n);
   return check_launch("ash_insert_count");
 }
 
+int ash_insert_count(ash_map_t* m, int64_t n, const int32_t* out_idx, const uint8_t* out_mask, void* stream) {
+  (void)out_idx;
+  (void)out_mask;
+  return count_impl(m, n, nullptr, stream);
+}
+
 static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
-                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy);
+                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy,
+                         const int32_t* d_n = nullptr);
 
 int ash_insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
                       int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
@@ -2225,7 +2396,8 @@ int ash_settle(ash_map_t* m, void* stream) {
 }
 
 static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
-                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy) {
+                         int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy,
+                         const int32_t* d_n) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
@@ -2252,9 +2424,9 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
     int rc = ASH_OK;
 #define ASH_BULK(VW_)                                                                                    \
   switch (m->arity) {                                                                                    \
-    case 1: rc = launch_commit_bulk<1, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
-    case 2: rc = launch_commit_bulk<2, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
-    default: rc = launch_commit_bulk<3, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, s); break; \
+    case 1: rc = launch_commit_bulk<1, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, d_n, s); break; \
+    case 2: rc = launch_commit_bulk<2, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, d_n, s); break; \
+    default: rc = launch_commit_bulk<3, VW_>(t, keys, n, va, association, out_idx, out_mask, m, pre, sweep_min, rank_words, d_n, s); break; \
   }
     switch (vw) {
       case 0: ASH_BULK(0); break;
@@ -2273,7 +2445,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
 #define ASH_COMMIT(VW_)                                                                                   \
   ASH_DISPATCH_ARITY(m->arity, (k_commit<A, VW_><<<grid_for(n, kTile), kBlock, 0, s>>>(                  \
                                    t, keys, n, va, association, out_idx, out_mask, m->heap, m->active, \
-                                   m->key_buf, m->counters, tile_pre, sweep_min, rank_words)))
+                                   m->key_buf, m->counters, tile_pre, sweep_min, rank_words, m->capacity, d_n)))
   switch (vw) {
     case 0: ASH_COMMIT(0); break;
     case 1: ASH_COMMIT(1); break;
@@ -2329,11 +2501,31 @@ int ash_insert_lazy(ash_map_t* m, const int32_t* keys, int64_t n, const void* co
   return ash_insert_commit_lazy(m, keys, n, values, association, out_idx, out_mask, stream);
 }
 
+// probe bound of device-sized inserts: a table the batch overfills flags
+// ASH_FLAG_TABLE_FULL after this many buckets instead of scanning it whole
+constexpr uint32_t kDnProbe = 4096;
+
+int ash_insert_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_t* d_n, const void* const* values,
+                  int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
+  if (int rc = check_map(m)) return rc;
+  if (!d_n) return fail(ASH_ERR_INVALID, "null device length");
+  if (int rc = check_batch(n_max)) return rc;
+  if (n_max == 0) return ASH_OK;
+  ash_map_t b = *m;
+  if (b.max_probe == 0 || b.max_probe > kDnProbe) b.max_probe = kDnProbe;
+  cudaMemsetAsync(m->counters + ASH_CTR_FLAGS, 0, sizeof(int32_t), as_stream(stream));
+  if (int rc = claim_impl(&b, keys, n_max, d_n, out_idx, out_mask, stream)) return rc;
+  if (int rc = count_impl(&b, n_max, d_n, stream)) return rc;
+  return insert_commit(&b, keys, n_max, values, association, out_idx, out_mask, stream, false, d_n);
+}
+
 int ash_insert_rollback(ash_map_t* m, int64_t n, const int32_t* out_idx, void* stream) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
   if (int rc = check_tiles(m, n)) return rc;
+  // the batch is undone: its ASH_FLAG_CAPACITY / TABLE_FULL with it
+  cudaMemsetAsync(m->counters + ASH_CTR_FLAGS, 0, sizeof(int32_t), as_stream(stream));
   k_rollback<<<grid_for(n, kBlock), kBlock, 0, as_stream(stream)>>>(static_cast<uint4*>(m->slots), out_idx, n,
                                                                     m->counters, m->tile_counts); note_launch();
   return check_launch("ash_insert_rollback");
@@ -2440,7 +2632,6 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
   if (n == 0) return check_launch("ash_voxelize");
-  cudaMemsetAsync(scratch_mask, 0, n, s);
   Table t = make_table(ws);
   const bool al = aligned16(points);
   if (points_are_f64 && al) {
@@ -2471,7 +2662,6 @@ int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t
   if (!out_coords || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null output pointer");
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
-  cudaMemsetAsync(scratch_mask, 0, n, s);
   run_dedup_select(make_table(ws), ws, f, n, out_coords, nullptr, scratch_idx, scratch_mask, s);
   return check_launch("ash_frame_blocks");
 }
@@ -2486,9 +2676,32 @@ int ash_unique_rows(ash_map_t* ws, const int32_t* keys, int64_t n, int32_t* out_
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
   if (n == 0) return check_launch("ash_unique_rows");
   if (!keys || !out_keys || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null batch pointer");
-  cudaMemsetAsync(scratch_mask, 0, n, s);
   run_dedup_select(make_table(ws), ws, RowSrc{keys}, n, out_keys, out_first, scratch_idx, scratch_mask, s);
   return check_launch("ash_unique_rows");
+}
+
+int ash_allocate_blocks(ash_map_t* global, ash_map_t* ws, const int32_t* coords, int64_t n, int32_t* out_blocks,
+                        int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
+                        int32_t* status, void* stream) {
+  if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
+  if (int rc = check_batch(n)) return rc;
+  if (n == 0) return fail(ASH_ERR_INVALID, "empty candidate batch");
+  if (!coords) return fail(ASH_ERR_INVALID, "null batch pointer");
+  return allocate_fused(global, ws, RowSrc{coords}, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask,
+                        status, as_stream(stream));
+}
+
+int ash_allocate_frame(ash_map_t* global, ash_map_t* ws, const double* depth, int64_t height, int64_t width,
+                       const double* cam, const double* pose, double block_size, double trunc, int32_t neighbor,
+                       int32_t* out_blocks, int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx,
+                       uint8_t* scratch_mask, int32_t* status, void* stream) {
+  if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
+  FrameSrc f;
+  int64_t n = 0;
+  if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
+  if (n == 0) return fail(ASH_ERR_INVALID, "empty frame");
+  return allocate_fused(global, ws, f, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask, status,
+                        as_stream(stream));
 }
 
 int ash_frame_candidates(const double* depth, int64_t height, int64_t width, const double* cam, const double* pose,

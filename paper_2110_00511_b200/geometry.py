@@ -211,7 +211,7 @@ def voxel_downsample(points, voxel_size: float, backend: str = "generic", thread
         coords = torch.empty((n, 3), dtype=torch.int32, device=dev)
         sel = torch.empty(n, dtype=torch.int64, device=dev)
         scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
-        scratch_mask = torch.empty(n, dtype=torch.uint8, device=dev)
+        scratch_mask = torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev)  # cand / dem bitmaps
         count, flags = ws.run(lambda: call(
             "ash_voxelize", _lib.ctypes.byref(ws.struct), pts.data_ptr(), int(pts.dtype == torch.float64), n,
             float(voxel_size), coords.data_ptr(), sel.data_ptr(), scratch_idx.data_ptr(),

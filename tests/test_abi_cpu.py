@@ -23,7 +23,7 @@ def test_library_loads_and_exports_all_declared_symbols():
     for n in names:
         assert hasattr(_lib.lib, n), f"libash.so does not export {n}"
     assert set(names) == set(_lib.EXPORTED), "ctypes signatures out of sync with ash.h"
-    assert _lib.lib.ash_abi_version() == 6
+    assert _lib.lib.ash_abi_version() == 7
 
 
 def test_struct_layout_matches_header(tmp_path):

@@ -1,0 +1,8 @@
+set -u
+O=gpurun_out
+timeout 900 python -m pytest tests/test_device_len_gpu.py tests/test_geometry_gpu.py tests/test_frame_gpu.py tests/test_parity_gpu.py tests/test_hashmap_gpu.py tests/test_fullsize_gpu.py -x -q > $O/r02j_tests.log 2>&1; echo "pytest rc=$?"; tail -25 $O/r02j_tests.log
+timeout 300 python tools/exp_dedup.py all 6 2>&1 | tail -5
+for w in c3 c4 c4f; do
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02j_launch_$w.csv python tools/exp_dedup.py $w 3 > /dev/null 2>&1
+  python tools/ncu_sum.py $O/r02j_launch_$w.csv 2>/dev/null | head -12
+done
