@@ -317,6 +317,13 @@ int ash_allocate_blocks(ash_map_t* global, ash_map_t* ws, const int32_t* coords,
                         int32_t* out_blocks, int32_t* out_gi, uint8_t* out_gmask,
                         int32_t* scratch_idx, uint8_t* scratch_mask, int32_t* status, void* stream);
 
+/* Copy rows [0, min(*d_count, cap)) of two arrays (row sizes multiples of 4
+ * bytes) in one launch: the caller's own copies of a fused allocate's
+ * results (status + 1 = the distinct rows), enqueued before the count is
+ * read on the host. */
+int ash_copy_prefix2(const void* src0, void* dst0, int64_t row_bytes0, const void* src1, void* dst1,
+                     int64_t row_bytes1, const int32_t* d_count, int64_t cap, void* stream);
+
 /* The same from a depth frame (candidates generated in-kernel, as
  * ash_frame_blocks): VoxelBlockGrid.allocate_blocks(frame), grid.py:127-150. */
 int ash_allocate_frame(ash_map_t* global, ash_map_t* ws, const double* depth, int64_t height,

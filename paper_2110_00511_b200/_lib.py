@@ -59,6 +59,8 @@ _SIGNATURES = {
     "ash_settle": (c_int32, [_M, c_void_p]),
     "ash_find_dn": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ash_insert_dn": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    "ash_copy_prefix2": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                                   c_void_p]),
     "ash_allocate_blocks": (c_int32, [_M, _M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p]),
     "ash_allocate_frame": (c_int32, [_M, _M, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,

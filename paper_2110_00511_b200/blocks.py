@@ -88,16 +88,20 @@ def _allocate_fused(gm: HashMap, n: int, launch):
         # the new blocks are at most capacity - size (else the device guard
         # rejects the batch): keep even that many claims under the slot limit
         gm._reserve_slots(max(gm._capacity - gm._top_ub, 0))
-        out = torch.empty((n, 3), dtype=torch.int32, device=dev)
-        gi = torch.empty(n, dtype=torch.int32, device=dev)
-        gmask = torch.empty(n, dtype=torch.uint8, device=dev)
-        scratch_idx = torch.empty(n, dtype=torch.int32, device=dev)
-        scratch_mask = torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev)  # cand / dem bitmaps
-        status = torch.empty(5, dtype=torch.int32, device=dev)
+        # per-size buffers kept by the workspace: a repeated sequence keeps
+        # its pointers and replays from libash's graph cache
+        out, gi, gmask, scratch_idx, scratch_mask, status = ws.sequence_buffers(n)
         stream = _stream_handle(dev)
         for slots, probe in ws.attempts():
             ws.use(slots, probe)
             launch(ws, out, gi, gmask, scratch_idx, scratch_mask, status, stream)
+            # the caller's result copies go in before the count is known
+            # (sized from the previous call): no launch after the host read
+            cap = min(n, max(256, 2 * ws.estimate))
+            blocks_c = torch.empty((cap, 3), dtype=torch.int32, device=dev)
+            gi_c = torch.empty(cap, dtype=torch.int32, device=dev)
+            call("ash_copy_prefix2", out.data_ptr(), blocks_c.data_ptr(), 12, gi.data_ptr(), gi_c.data_ptr(), 4,
+                 status.data_ptr() + 4, cap, stream)
             rows, count, wflags, gflags, winners = status.tolist()  # the one host read
             if probe and wflags & _lib.FLAG_TABLE_FULL:
                 continue  # the workspace prefix overflowed (the global map was not touched)
@@ -113,10 +117,12 @@ def _allocate_fused(gm: HashMap, n: int, launch):
             # activate (doubling growth, hashmap.py:389-396)
             call("ash_insert_rollback", gm._ptr(), rows, gi.data_ptr(), stream)
             gm._tombs_ub += rows
-            gi = gm._insert_like(out[:count], None, association=True).indices
-        else:
-            gm._top_ub = min(gm._capacity, gm._top_ub + winners)
-    return out[:count], gi[:count]
+            blocks = out[:count].clone()
+            return blocks, gm._insert_like(blocks, None, association=True).indices
+        gm._top_ub = min(gm._capacity, gm._top_ub + winners)
+        if count <= cap:
+            return blocks_c[:count], gi_c[:count]
+        return out[:count].clone(), gi[:count].clone()
 
 
 class BlockGrid:

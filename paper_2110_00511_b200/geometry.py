@@ -127,6 +127,7 @@ class _VoxelWorkspace:
         self.struct.arity = 3
         self.struct.counters = self.counters.data_ptr()
         self.estimate = 0  # distinct keys of the previous call
+        self._seq_bufs = None
 
     @classmethod
     def get(cls, device: torch.device) -> "_VoxelWorkspace":
@@ -155,6 +156,19 @@ class _VoxelWorkspace:
             self.tiles = torch.zeros(tiles, dtype=torch.int32, device=self.device)
             self.struct.tile_counts = self.tiles.data_ptr()
             self.struct.tile_counts_len = tiles
+
+    def sequence_buffers(self, n: int):
+        """(blocks, gi, gmask, scratch_idx, scratch_mask, status) for a fused
+        allocate of n candidates, reused while n repeats (stable pointers)."""
+        if self._seq_bufs is None or self._seq_bufs[0] != n:
+            dev = self.device
+            self._seq_bufs = (n, torch.empty((n, 3), dtype=torch.int32, device=dev),
+                              torch.empty(n, dtype=torch.int32, device=dev),
+                              torch.empty(n, dtype=torch.uint8, device=dev),
+                              torch.empty(n, dtype=torch.int32, device=dev),
+                              torch.empty(8 * ((n + 31) // 32), dtype=torch.uint8, device=dev),  # cand / dem bitmaps
+                              torch.empty(5, dtype=torch.int32, device=dev))
+        return self._seq_bufs[1:]
 
     def attempts(self):
         """(table slots, probe limit) to try in order: the estimate-sized

@@ -1,6 +1,6 @@
 set -u
 O=gpurun_out
-timeout 900 python -m pytest tests/test_device_len_gpu.py tests/test_geometry_gpu.py tests/test_frame_gpu.py tests/test_parity_gpu.py -x -q > $O/r02k_tests.log 2>&1; echo "pytest rc=$?"; tail -3 $O/r02k_tests.log
+timeout 900 python -m pytest tests/test_device_len_gpu.py tests/test_geometry_gpu.py tests/test_frame_gpu.py tests/test_parity_gpu.py -x -q > $O/r02l_tests.log 2>&1; echo "pytest rc=$?"; tail -3 $O/r02l_tests.log
 timeout 300 python tools/exp_dedup.py all 6 2>&1 | tail -5
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02k_launch_c3.csv python tools/exp_dedup.py c3 3 > /dev/null 2>&1
-python tools/ncu_sum.py $O/r02k_launch_c3.csv 2>/dev/null | head -12
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02l_launch_c3.csv python tools/exp_dedup.py c3 3 > /dev/null 2>&1
+python tools/ncu_sum.py $O/r02l_launch_c3.csv 2>/dev/null | head -12
