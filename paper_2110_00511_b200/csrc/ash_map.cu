@@ -1829,9 +1829,9 @@ struct FrameSrc {
 //          displaces a higher one (atomicMin) is a candidate: its bit is set
 //          in `cand`, and the displaced position's bit in `dem` (both
 //          monotonic ORs: no ordering race between a claimer and its
-//          displacer); exact per-tile winner counts (+1 / -1).  A duplicate
-//          that finds a lower position costs one L2 probe and no store.
-//   scan   exclusive prefix of the tile counts (k_tile_scan).
+//          displacer).  A duplicate that finds a lower position costs one
+//          L2 probe and no store.
+//   count  winners per 8192 positions from the bitmaps; k_tile_scan.
 //   words  per 32 positions: winners = cand & ~dem, exclusive word prefix.
 //   emit   one sequential pass over the table prefix in use: every
 //          PENDING|p slot is winner p; its rank is word_pre + the winners
@@ -1847,15 +1847,18 @@ __device__ __forceinline__ uint32_t dd_hash(const Key<3>& k) {
 
 // True when p becomes a candidate (took a slot, or displaced a higher
 // position, whose `dem` bit it sets).
-__device__ __forceinline__ bool dd_claim_probe(const Table& t, const Key<3>& k, uint32_t h, uint32_t p,
-                                               int32_t* counters, uint32_t* dem) {
+// w: the home bucket, already loaded (so a caller can keep several home
+// bucket loads in flight)
+__device__ __forceinline__ bool dd_claim_resolve(const Table& t, const Key<3>& k, uint32_t h, uint32_t p,
+                                                 uint32_t (&w)[8], int32_t* counters, uint32_t* dem) {
   const uint32_t me = PEND | p;
   uint32_t b = home_bucket(h, t.n_buckets);
   int first = 0;
   uint32_t scanned = 0;
+  bool loaded = true;
   while (true) {
-    uint32_t w[8];
-    ld256_relaxed(t.slots + 2 * static_cast<size_t>(b), w);
+    if (!loaded) ld256_relaxed(t.slots + 2 * static_cast<size_t>(b), w);
+    loaded = false;
     int retry = -1;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -1889,6 +1892,56 @@ __device__ __forceinline__ bool dd_claim_probe(const Table& t, const Key<3>& k, 
   }
 }
 
+__device__ __forceinline__ bool dd_claim_probe(const Table& t, const Key<3>& k, uint32_t h, uint32_t p,
+                                               int32_t* counters, uint32_t* dem) {
+  uint32_t w[8];
+  ld256_relaxed(t.slots + 2 * static_cast<size_t>(home_bucket(h, t.n_buckets)), w);
+  return dd_claim_resolve(t, k, h, p, w, counters, dem);
+}
+
+// 16 blocks of 128 per SM (32 registers): the claim is latency-bound, and
+// 36 registers (12 blocks) cost 20% at configs[2]
+// Claim step of one position p (lane of a warp of consecutive positions,
+// `live` the lanes in the batch): in-warp duplicate skip, probe, candidate
+// bit.  Every live lane must call it.
+template <int GROUP>
+__device__ __forceinline__ void dd_claim_lane(const Table& t, const Key<3>& k, bool valid, int64_t p, int lane,
+                                              unsigned live, int period, int32_t* counters, uint32_t* cand,
+                                              uint32_t* dem) {
+  const uint32_t h = dd_hash(k);
+  // a position whose key equals that of a valid lower lane can never be a
+  // first occurrence: it skips the table (the lower position, or one lower
+  // still, claims)
+  bool dup = false;
+  if (GROUP == 1) {  // the previous lane, and the lane one period back
+    const unsigned vmask = __ballot_sync(live, valid);
+    const uint32_t u0 = __shfl_up_sync(live, k.w[0], 1), u1 = __shfl_up_sync(live, k.w[1], 1),
+                   u2 = __shfl_up_sync(live, k.w[2], 1);
+    dup = lane > 0 && ((vmask >> (lane - 1)) & 1) && u0 == k.w[0] && u1 == k.w[1] && u2 == k.w[2];
+    if (period > 1 && period < 32) {
+      const int q = lane >= period ? lane - period : lane;
+      const uint32_t v0 = __shfl_sync(live, k.w[0], q), v1 = __shfl_sync(live, k.w[1], q),
+                     v2 = __shfl_sync(live, k.w[2], q);
+      dup = dup || (lane >= period && ((vmask >> q) & 1) && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2]);
+    }
+  } else if (GROUP == 2) {  // any lower lane: match on the hash, verify the lowest
+    const unsigned vmask = __ballot_sync(live, valid);
+    const unsigned grp = __match_any_sync(live, h) & vmask;
+    const int low = __ffs(grp) - 1;
+    const int src_lane = low < 0 ? lane : low;
+    const uint32_t v0 = __shfl_sync(live, k.w[0], src_lane), v1 = __shfl_sync(live, k.w[1], src_lane),
+                   v2 = __shfl_sync(live, k.w[2], src_lane);
+    dup = low >= 0 && low < lane && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2];
+  }
+  const bool ev = valid && !dup && dd_claim_probe(t, k, h, static_cast<uint32_t>(p), counters, dem);
+  __syncwarp(live);
+  // the warp's 32 positions share one bitmap word (warps start at multiples
+  // of 32).  Counts come from the bitmaps afterwards (k_dd_count): counting
+  // here put ~64 warps' atomics on each tile word.
+  const unsigned cb = __ballot_sync(live, ev);
+  if (cb && lane == __ffs(live) - 1) atomicOr(&cand[p >> 5], cb);
+}
+
 // 16 blocks of 128 per SM (32 registers): the claim is latency-bound, and
 // 36 registers (12 blocks) cost 20% at configs[2]
 template <typename Src, int B = 128>
@@ -1911,40 +1964,8 @@ __global__ void __launch_bounds__(B, 2048 / B) k_dd_claim(Table t, Src src, int6
     has = src.key(p, k, &bad);
   }
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
-  const bool valid = has && !bad;  // out-of-range points never claim; the host raises
-  const uint32_t h = dd_hash(k);
-  // a position whose key equals that of a valid lower lane can never be a
-  // first occurrence: it skips the table (the lower position, or one lower
-  // still, claims)
-  bool dup = false;
-  if (Src::kGroup == 1) {  // the previous lane, and the lane one period back
-    const unsigned vmask = __ballot_sync(live, valid);
-    const uint32_t u0 = __shfl_up_sync(live, k.w[0], 1), u1 = __shfl_up_sync(live, k.w[1], 1),
-                   u2 = __shfl_up_sync(live, k.w[2], 1);
-    dup = lane > 0 && ((vmask >> (lane - 1)) & 1) && u0 == k.w[0] && u1 == k.w[1] && u2 == k.w[2];
-    const int per = src.period();
-    if (per > 1 && per < 32) {
-      const int q = lane >= per ? lane - per : lane;
-      const uint32_t v0 = __shfl_sync(live, k.w[0], q), v1 = __shfl_sync(live, k.w[1], q),
-                     v2 = __shfl_sync(live, k.w[2], q);
-      dup = dup || (lane >= per && ((vmask >> q) & 1) && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2]);
-    }
-  } else if (Src::kGroup == 2) {  // any lower lane: match on the hash, verify the lowest
-    const unsigned vmask = __ballot_sync(live, valid);
-    const unsigned grp = __match_any_sync(live, h) & vmask;
-    const int low = __ffs(grp) - 1;
-    const int src_lane = low < 0 ? lane : low;
-    const uint32_t v0 = __shfl_sync(live, k.w[0], src_lane), v1 = __shfl_sync(live, k.w[1], src_lane),
-                   v2 = __shfl_sync(live, k.w[2], src_lane);
-    dup = low >= 0 && low < lane && v0 == k.w[0] && v1 == k.w[1] && v2 == k.w[2];
-  }
-  const bool ev = valid && !dup && dd_claim_probe(t, k, h, static_cast<uint32_t>(p), counters, dem);
-  __syncwarp(live);
-  // the warp's 32 positions share one bitmap word (blocks of B positions
-  // are B-aligned).  Per-tile counts come from the bitmaps afterwards
-  // (k_dd_count): counting here put ~64 warps' atomics on each tile word.
-  const unsigned cb = __ballot_sync(live, ev);
-  if (cb && lane == __ffs(live) - 1) atomicOr(&cand[p >> 5], cb);
+  // out-of-range points never claim; the host raises
+  dd_claim_lane<Src::kGroup>(t, k, has && !bad, p, lane, live, src.period(), counters, cand, dem);
 }
 
 // winners per 256 bitmap words (8192 positions: one k_dd_words block) ->
@@ -2003,22 +2024,35 @@ __global__ void __launch_bounds__(kBlock)
   if (w < n_words) word_pre[w] = before;
 }
 
+// one 32-byte bucket (two slots) per thread, a full grid: the table prefix
+// is mostly evicted by the cloud stream of the claim, so this pass is bound
+// by DRAM latency and wants every bucket's load in flight at once
 __global__ void __launch_bounds__(kBlock)
-    k_dd_emit(uint4* slots, uint32_t n_slots, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
+    k_dd_emit(uint4* slots, uint32_t n_buckets, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
               const int32_t* __restrict__ word_pre, int32_t* __restrict__ out_coords, int64_t* __restrict__ out_sel) {
-  const uint32_t stride = gridDim.x * kBlock;
-  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n_slots; i += stride) {
-    const uint4 sv = slots[i];
-    if ((sv.w & 0xC0000000u) != PEND) continue;  // EMPTY (the workspace has no tombstones)
-    const uint32_t p = sv.w & SLOT_MASK;
-    const uint32_t wi = p >> 5;
-    const uint32_t below = (__ldg(cand + wi) & ~__ldg(dem + wi)) & ((1u << (p & 31)) - 1u);
-    const int64_t r = __ldg(word_pre + wi) + __popc(below);
-    out_coords[3 * r] = static_cast<int32_t>(sv.x);
-    out_coords[3 * r + 1] = static_cast<int32_t>(sv.y);
-    out_coords[3 * r + 2] = static_cast<int32_t>(sv.z);
+  const uint32_t b = blockIdx.x * kBlock + threadIdx.x;
+  if (b >= n_buckets) return;
+  uint32_t w[8];
+  ld256_nc(slots + 2 * static_cast<size_t>(b), w);
+  uint32_t wb[2];
+  int32_t wp[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    if ((w[4 * s + 3] & 0xC0000000u) != PEND) continue;  // EMPTY (the workspace has no tombstones)
+    const uint32_t wi = (w[4 * s + 3] & SLOT_MASK) >> 5;
+    wb[s] = __ldg(cand + wi) & ~__ldg(dem + wi);
+    wp[s] = __ldg(word_pre + wi);
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    if ((w[4 * s + 3] & 0xC0000000u) != PEND) continue;
+    const uint32_t p = w[4 * s + 3] & SLOT_MASK;
+    const int64_t r = wp[s] + __popc(wb[s] & ((1u << (p & 31)) - 1u));
+    out_coords[3 * r] = static_cast<int32_t>(w[4 * s]);
+    out_coords[3 * r + 1] = static_cast<int32_t>(w[4 * s + 1]);
+    out_coords[3 * r + 2] = static_cast<int32_t>(w[4 * s + 2]);
     if (out_sel) out_sel[r] = p;
-    slots[i] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);  // the workspace is EMPTY again
+    slots[2 * static_cast<size_t>(b) + s] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);  // the workspace is EMPTY again
   }
 }
 
@@ -2237,9 +2271,8 @@ void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, 
   note_launch();
   k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts, ws->counters, status);
   note_launch();
-  const unsigned cap = static_cast<unsigned>(device_sms()) * 8;
-  const unsigned eg = grid_for(t.n_slots, kBlock);
-  k_dd_emit<<<eg < cap ? eg : cap, kBlock, 0, s>>>(t.slots, t.n_slots, cand, dem, scratch_idx, out_coords, out_sel);
+  k_dd_emit<<<grid_for(t.n_buckets, kBlock), kBlock, 0, s>>>(t.slots, t.n_buckets, cand, dem, scratch_idx, out_coords,
+                                                              out_sel);
   note_launch();
 }
 
@@ -2328,6 +2361,7 @@ static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int6
   if (global->arity != 3) return fail(ASH_ERR_INVALID, "block coordinates need key arity 3");
   if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
+  if (int rc = check_scan(ws, n)) return rc;
   if (!out_blocks || !out_gi || !out_gmask || !scratch_idx || !scratch_mask || !status)
     return fail(ASH_ERR_INVALID, "null output pointer");
   auto body = [&](cudaStream_t st) -> int {
@@ -2831,6 +2865,7 @@ int ash_voxelize(ash_map_t* ws, const void* points, int32_t points_are_f64, int6
   if (!(voxel > 0)) return fail(ASH_ERR_INVALID, "voxel size must be > 0");
   if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
+  if (int rc = check_scan(ws, n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
   if (n == 0) return check_launch("ash_voxelize");
@@ -2861,6 +2896,7 @@ int ash_frame_blocks(ash_map_t* ws, const double* depth, int64_t height, int64_t
   if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
   if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
+  if (int rc = check_scan(ws, n)) return rc;
   if (!out_coords || !scratch_idx || !scratch_mask) return fail(ASH_ERR_INVALID, "null output pointer");
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
@@ -2874,6 +2910,7 @@ int ash_unique_rows(ash_map_t* ws, const int32_t* keys, int64_t n, int32_t* out_
   if (int rc = check_batch(n)) return rc;
   if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
   if (int rc = check_tiles(ws, n)) return rc;
+  if (int rc = check_scan(ws, n)) return rc;
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
   if (n == 0) return check_launch("ash_unique_rows");

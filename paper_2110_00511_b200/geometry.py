@@ -8,6 +8,7 @@ first-occurrence winner + ascending select (libash ``ash_voxelize``).
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -138,6 +139,7 @@ class _VoxelWorkspace:
             return ws
 
     SMALL_MIN = 1 << 16
+    ESTIMATE_FACTOR = float(os.environ.get("ASH_WS_FACTOR", "4"))  # slots per distinct key of the previous call
     PROBE_LIMIT = 64  # buckets, for the estimated-size attempt
 
     def reserve(self, n: int) -> None:
@@ -173,7 +175,7 @@ class _VoxelWorkspace:
     def attempts(self):
         """(table slots, probe limit) to try in order: the estimate-sized
         prefix first when it is smaller than the full table."""
-        small = _table_slots(max(4 * self.estimate, self.SMALL_MIN), 1.0)
+        small = _table_slots(max(self.ESTIMATE_FACTOR * self.estimate, self.SMALL_MIN), 1.0)
         if self.estimate and small < self.full_slots:
             yield small, self.PROBE_LIMIT
         yield self.full_slots, 0
