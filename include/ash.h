@@ -378,6 +378,18 @@ int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t
                    const int64_t* row_off, const void* const* peer_ret, int32_t* out,
                    uint8_t* out_mask /* optional: out >= 0 */, void* stream);
 
+/* Sync-free routing (the peer transport's device-sized shard ops): the rows
+ * this rank receives, sum of its column of the exchanged count matrix, into
+ * status[0] (0 when any owner's rows pass recv_capacity: ash_route_put_counts
+ * then stores nothing on every rank, status[1] = 1, and the caller redoes
+ * the op with grown buffers); ash_route_pull with this rank's row offsets
+ * taken from the count matrix on the device. */
+int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t rank,
+                          int64_t recv_capacity, int32_t* status, void* stream);
+int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world,
+                          int32_t rank, const int64_t* count_matrix, const void* const* peer_ret,
+                          int32_t* out, uint8_t* out_mask, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

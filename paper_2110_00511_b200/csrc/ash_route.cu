@@ -399,9 +399,17 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
 __global__ void __launch_bounds__(kBlock) k_route_pull(const uint8_t* __restrict__ owners,
                                                        const int32_t* __restrict__ jdx, int64_t n, PeerArgs pa,
                                                        uint32_t world, int32_t* __restrict__ out,
-                                                       uint8_t* __restrict__ out_mask) {
+                                                       uint8_t* __restrict__ out_mask,
+                                                       const int64_t* __restrict__ cmat, uint32_t rank) {
   __shared__ const int32_t* s_base[kMaxWorld];
-  for (uint32_t o = threadIdx.x; o < world; o += kBlock) s_base[o] = pa.ret[o] + pa.row_off[o];
+  for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
+    int64_t off = pa.row_off[o];
+    if (cmat) {  // this rank's first row at owner o: rows of the sources before it
+      off = 0;
+      for (uint32_t src = 0; src < rank; ++src) off += cmat[src * world + o];
+    }
+    s_base[o] = pa.ret[o] + off;
+  }
   __syncthreads();
   const int64_t p0 = (blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x) * 4;
   if (p0 >= n) return;
@@ -425,6 +433,29 @@ __global__ void __launch_bounds__(kBlock) k_route_pull(const uint8_t* __restrict
     const int32_t v = s_base[owners[p]][jdx[p]];
     out[p] = v;
     if (out_mask) out_mask[p] = v >= 0;
+  }
+}
+
+// The rows this rank receives (sum of its column of the exchanged count
+// matrix) into status[0] for the device-sized shard op, 0 when some owner's
+// rows pass the receive capacity (k_route_put then stores nothing, on every
+// rank alike); status[1] = that overflow.
+__global__ void k_route_recv_status(const int64_t* __restrict__ cmat, uint32_t world, uint32_t rank, int64_t cap,
+                                    int32_t* status) {
+  __shared__ int s_over;
+  if (threadIdx.x == 0) s_over = 0;
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < world; o += blockDim.x) {
+    int64_t tot = 0;
+    for (uint32_t src = 0; src < world; ++src) tot += cmat[src * world + o];
+    if (tot > cap) s_over = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t m = 0;
+    for (uint32_t src = 0; src < world; ++src) m += cmat[src * world + rank];
+    status[0] = s_over ? 0 : static_cast<int32_t>(m);
+    status[1] = s_over;
   }
 }
 
@@ -581,8 +612,37 @@ int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t
     pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
   }
   k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask); note_launch();
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, 0); note_launch();
   return rcheck("ash_route_pull");
+}
+
+int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t rank, int64_t recv_capacity,
+                          int32_t* status, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || recv_capacity < 0)
+    return rfail("bad routing arguments");
+  if (!count_matrix || !status) return rfail("null routing buffer");
+  k_route_recv_status<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(count_matrix, static_cast<uint32_t>(world),
+                                                                      static_cast<uint32_t>(rank), recv_capacity,
+                                                                      status); note_launch();
+  return rcheck("ash_route_recv_status");
+}
+
+int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world, int32_t rank,
+                          const int64_t* count_matrix, const void* const* peer_ret, int32_t* out,
+                          uint8_t* out_mask, void* stream) {
+  if (n < 0 || world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return rfail("bad routing arguments");
+  if (n == 0) return ASH_OK;
+  if (!owners || !jdx || !count_matrix || !peer_ret || !out) return rfail("null routing buffer");
+  PeerArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  for (int o = 0; o < world; ++o) {
+    if (!peer_ret[o]) return rfail("null peer result buffer");
+    pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
+  }
+  k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank));
+  note_launch();
+  return rcheck("ash_route_pull_counts");
 }
 
 int ash_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {

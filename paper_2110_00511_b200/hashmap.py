@@ -777,6 +777,51 @@ class HashMap:
         with self._guard.writing():
             self._insert_like(keys, vals if op == "insert" else None, op == "activate", idx=out_idx)
 
+    def _dn_ready(self, op: str, n_max: int) -> bool:
+        """Can a device-sized batch of up to n_max keys run with no host
+        check?  find: always.  insert / activate: the generic backend with
+        free indices and slots for all n_max (so the device capacity guard
+        cannot fire)."""
+        if op == "find":
+            return True
+        if self.backend_name == "delegate" or self._capacity - self._top_ub < n_max:
+            return False
+        return self._top_ub + self._tombs_ub + n_max <= int(_SLOT_LIMIT * self._n_slots)
+
+    def _op_into_dn(self, op: str, keys: torch.Tensor, vals, out_idx: torch.Tensor, d_n: torch.Tensor) -> None:
+        """insert / activate / find of keys[0 : d_n[0]) (device length, at most
+        keys.shape[0]) with the indices written into out_idx (ash_insert_dn /
+        ash_find_dn); the caller checked _dn_ready."""
+        n_max = keys.shape[0]
+        if not n_max:
+            return
+        msk = getattr(self, "_dn_mask", None)
+        if msk is None or msk.numel() < n_max:
+            msk = self._dn_mask = torch.empty(n_max, dtype=torch.uint8, device=self._device)
+        if op == "find":
+            with self._guard.reading():
+                call("ash_find_dn", self._ptr(), keys.data_ptr(), n_max, d_n.data_ptr(), out_idx.data_ptr(),
+                     msk.data_ptr(), self._stream())
+            return
+        with self._guard.writing():
+            self._settle()
+            self._ensure_scan(n_max)
+            vptr = None
+            if vals:
+                vptr = (_lib.c_void_p * len(vals))(*[v.data_ptr() for v in vals])
+            call("ash_insert_dn", self._ptr(), keys.data_ptr(), n_max, d_n.data_ptr(), vptr,
+                 1 if op == "activate" else 0, out_idx.data_ptr(), msk.data_ptr(), self._stream())
+            self._top_ub = min(self._capacity, self._top_ub + n_max)
+            self._size_known = False
+
+    def _dn_done(self, op: str) -> None:
+        """After the op's host read: a device-sized insert can only fail on a
+        probe chain past the device bound (load <= 0.75: not in practice);
+        fail loudly rather than return wrong indices."""
+        if op != "find" and int(self._counters[_lib.CTR_FLAGS].item()) & (_lib.FLAG_CAPACITY |
+                                                                           _lib.FLAG_TABLE_FULL):
+            raise RuntimeError("device-sized insert could not place every key (probe bound); rebuild the map")
+
     @on_device
     def find(self, keys) -> BatchResult:
         """Look up keys; the map is not modified (hashmap.py:415-429)."""

@@ -243,6 +243,60 @@ class PeerExchange:
             rpay = self.recv_pay[:m * self.pay_rb].view(dt).view(m, *shape)
         return rkeys, rpay, (n, owners, jdx, offs)
 
+    def dispatch_dn(self, keys: torch.Tensor, payload: torch.Tensor = None):
+        """Sync-free dispatch: the put and this rank's received row count
+        (``status[0]``, device int32) both come from the exchanged count
+        matrix on the device, so the host never waits inside the op.  Returns
+        the receive views at full capacity (the shard op reads its length
+        from ``status``), ``status`` and the combine context.  ``status[1]``
+        = 1 when some owner's rows would pass the receive capacity: nothing
+        was stored and the caller redoes the op on the host-checked path."""
+        lib = self._lib
+        n = keys.shape[0]
+        need = int(lib.lib.ash_route_scratch_len(n, self.world))
+        if self._scratch.numel() < need:
+            self._scratch = torch.empty(max(need, 1), dtype=torch.int32, device=self.device)
+        counts = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        owners = torch.empty(n, dtype=torch.uint8, device=self.device)
+        lib.call("ash_route_count", keys.data_ptr(), n, self.arity, self.world, counts.data_ptr(),
+                 owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), self._stream())
+        if dist.get_backend(self.group) == "gloo":  # CPU control plane (tests: ranks sharing a GPU)
+            parts = [torch.empty(self.world, dtype=torch.int64) for _ in range(self.world)]
+            dist.all_gather(parts, counts.cpu(), group=self.group)
+            mat = torch.stack(parts).to(self.device)
+        else:
+            mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
+            dist.all_gather_into_tensor(mat, counts, group=self.group)
+        status = torch.empty(2, dtype=torch.int32, device=self.device)
+        lib.call("ash_route_recv_status", mat.data_ptr(), self.world, self.rank, self.capacity,
+                 status.data_ptr(), self._stream())
+        jdx = torch.empty(n, dtype=torch.int32, device=self.device)
+        rb = self.pay_rb if (payload is not None and n) else 0
+        if rb:
+            payload = payload.contiguous()
+        lib.call("ash_route_put_counts", keys.data_ptr(), n, self.arity, self.world, self.rank,
+                 owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), mat.data_ptr(),
+                 self.capacity, self._p_keys, payload.data_ptr() if rb else None, rb,
+                 self._p_pay if rb else None, jdx.data_ptr(), self._stream())
+        self._barrier()  # every source's rows have landed
+        cap = self.capacity
+        rkeys = self.recv_keys[:cap * self.arity].view(cap, self.arity)
+        rpay = None
+        if self.pay_rb and payload is not None:
+            shape, dt = self.payload
+            rpay = self.recv_pay[:cap * self.pay_rb].view(dt).view(cap, *shape)
+        return rkeys, rpay, status, (n, owners, jdx, mat)
+
+    def combine_dn(self, ctx):
+        n, owners, jdx, mat = ctx
+        self._barrier()  # every owner's results are in place
+        out = torch.empty(n, dtype=torch.int32, device=self.device)
+        msk = torch.empty(n, dtype=torch.uint8, device=self.device)
+        self._lib.call("ash_route_pull_counts", owners.data_ptr(), jdx.data_ptr(), n, self.world, self.rank,
+                       mat.data_ptr(), self._p_ret, out.data_ptr(), msk.data_ptr(), self._stream())
+        self._barrier()  # all pulls done: buffers reusable
+        return out, msk.view(torch.bool)
+
     def combine(self, local_idx, ctx) -> torch.Tensor:
         """local_idx: this owner's results, or None when the shard op wrote
         them into ``self.ret`` itself."""
@@ -360,6 +414,16 @@ class PartitionedHashMap:
                     raise ValueError(f"value batch has shape {tuple(vals[0].shape)}, expected "
                                      f"({keys.shape[0]}, {', '.join(map(str, specs[0].shape))})")
                 vals = [v]
+        if op != "erase" and hasattr(self.local, "_op_into_dn") and self.local._dn_ready(op, self.peer.capacity):
+            # sync-free: the shard op reads its batch length on the device
+            rkeys, rpay, status, ctx = self.peer.dispatch_dn(keys, vals[0] if vals else None)
+            self.local._op_into_dn(op, rkeys, [rpay] if rpay is not None else [], self.peer.ret, status)
+            out, msk = self.peer.combine_dn(ctx)
+            if not int(status[1].item()):  # the one host read: did a receive buffer overflow?
+                self.local._dn_done(op)
+                return PartitionedResult(out, msk, ctx[1])
+            # nothing was stored anywhere (every rank saw the same matrix):
+            # redo on the host-checked path, which grows the buffers
         rkeys, rpay, ctx = self.peer.dispatch(keys, vals[0] if vals else None)
         if op != "erase" and hasattr(self.local, "_op_into"):
             # the shard op writes its indices straight into the result buffer
