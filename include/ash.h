@@ -383,12 +383,13 @@ int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t
  * status[0] (0 when any owner's rows pass recv_capacity: ash_route_put_counts
  * then stores nothing on every rank, status[1] = 1, and the caller redoes
  * the op with grown buffers); ash_route_pull with this rank's row offsets
- * taken from the count matrix on the device. */
+ * taken from the count matrix on the device, a no-op when recv_status[1]
+ * reports the overflow. */
 int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t rank,
                           int64_t recv_capacity, int32_t* status, void* stream);
 int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world,
-                          int32_t rank, const int64_t* count_matrix, const void* const* peer_ret,
-                          int32_t* out, uint8_t* out_mask, void* stream);
+                          int32_t rank, const int64_t* count_matrix, const int32_t* recv_status,
+                          const void* const* peer_ret, int32_t* out, uint8_t* out_mask, void* stream);
 
 #ifdef __cplusplus
 }

@@ -100,7 +100,7 @@ _SIGNATURES = {
                                  c_void_p]),
     "ash_route_recv_status": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_void_p, c_void_p]),
     "ash_route_pull_counts": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
-                                        c_void_p, c_void_p]),
+                                        c_void_p, c_void_p, c_void_p]),
     "ash_gather_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ash_scatter_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
 }

@@ -112,11 +112,13 @@ def _allocate_fused(gm: HashMap, n: int, launch):
         if wflags & _lib.FLAG_RANGE:
             raise ValueError("block coordinates exceed int32 range")
         gm._size_known = False
-        if gflags & (_lib.FLAG_CAPACITY | _lib.FLAG_TABLE_FULL):
-            # nothing committed: undo the claims, then the host-checked
-            # activate (doubling growth, hashmap.py:389-396)
-            call("ash_insert_rollback", gm._ptr(), rows, gi.data_ptr(), stream)
-            gm._tombs_ub += rows
+        if gflags & (_lib.FLAG_CAPACITY | _lib.FLAG_TABLE_FULL) or rows < count:
+            # not committed on the device (more distinct blocks than the
+            # capacity, or the guard fired): undo any claims, then the
+            # host-checked activate (doubling growth, hashmap.py:389-396)
+            if rows:
+                call("ash_insert_rollback", gm._ptr(), rows, gi.data_ptr(), stream)
+                gm._tombs_ub += rows
             blocks = out[:count].clone()
             return blocks, gm._insert_like(blocks, None, association=True).indices
         gm._top_ub = min(gm._capacity, gm._top_ub + winners)

@@ -797,28 +797,16 @@ __device__ __forceinline__ void claim_chunk(const Table& t, const int32_t* __res
   if (lane == 0 && tomb_total) atomicSub(&counters[ASH_CTR_TOMBS], tomb_total);
 }
 
+// d_n: a device-sized batch (ash_insert_dn): blocks past min(n, *d_n) exit
 template <int A, int B = kBlock>
 __global__ void __launch_bounds__(B) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                             int32_t* counters, int32_t* tile_cnt) {
-  __shared__ uint32_t stage[kClaimRounds][B * 3];
-  claim_chunk<A, B>(t, keys, n, blockIdx.x * static_cast<int64_t>(B * kClaimRounds), tmp, mask, counters, tile_cnt,
-                    stage);
-}
-
-// device-sized batch (ash_insert_dn): a grid sized for n_max would be mostly
-// empty blocks, so a bounded grid strides over the chunks of min(n, *d_n)
-template <int A, int B = kBlock>
-__global__ void __launch_bounds__(B) k_claim_dn(Table t, const int32_t* __restrict__ keys, int64_t n,
-                                                int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                                int32_t* counters, int32_t* tile_cnt, const int32_t* d_n) {
+                                             int32_t* counters, int32_t* tile_cnt, const int32_t* d_n) {
   __shared__ uint32_t stage[kClaimRounds][B * 3];
   n = dev_len(n, d_n);
-  for (int64_t blk = blockIdx.x * static_cast<int64_t>(B * kClaimRounds); blk < n;
-       blk += static_cast<int64_t>(gridDim.x) * B * kClaimRounds) {
-    claim_chunk<A, B>(t, keys, n, blk, tmp, mask, counters, tile_cnt, stage);
-    __syncwarp();  // the warp's stage rows are rewritten by the next chunk
-  }
+  const int64_t blk = blockIdx.x * static_cast<int64_t>(B * kClaimRounds);
+  if (blk >= n) return;
+  claim_chunk<A, B>(t, keys, n, blk, tmp, mask, counters, tile_cnt, stage);
 }
 
 // ---------------------------------------------------------------------------
@@ -1994,16 +1982,17 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kBlock)
     k_dd_words(int64_t n, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
                int32_t* __restrict__ word_pre, const int32_t* blk_pre, const int32_t* ws_counters,
-               int32_t* status) {
+               int32_t* status, int64_t rows_max) {
   __shared__ int32_t s_warp[kWarps];
   __shared__ int32_t s_prefix;
   const int64_t n_words = (n + 31) / 32;
   if (status && blockIdx.x == 0 && threadIdx.x == 0) {
     // ash_allocate_*: status[0] = rows the global activate takes (0 when the
     // dedup overflowed its workspace prefix or met an out-of-range block),
-    // [1] = distinct rows, [2] = workspace flags
+    // [1] = distinct rows, [2] = workspace flags; more rows than rows_max
+    // (the map's capacity) cannot all be new: the host path takes them
     const int32_t count = ws_counters[ASH_CTR_COUNT], flags = ws_counters[ASH_CTR_FLAGS];
-    status[0] = (flags & (ASH_FLAG_TABLE_FULL | ASH_FLAG_RANGE)) ? 0 : count;
+    status[0] = (flags & (ASH_FLAG_TABLE_FULL | ASH_FLAG_RANGE)) || count > rows_max ? 0 : count;
     status[1] = count;
     status[2] = flags;
   }
@@ -2257,7 +2246,8 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
 // scratch_idx: the word prefixes (ceil(n / 32) words)
 template <typename Src>
 void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
-                      int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s, int32_t* status = nullptr) {
+                      int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s, int32_t* status = nullptr,
+                      int64_t status_rows_max = 0) {
   const int64_t words = (n + 31) / 32;
   uint32_t* cand = reinterpret_cast<uint32_t*>(scratch_mask);
   uint32_t* dem = cand + words;
@@ -2269,7 +2259,8 @@ void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, 
   note_launch();
   k_tile_scan<<<1, kScanBlock, 0, s>>>(ws->tile_counts, wg, ws->counters, -1, ASH_CTR_COUNT, nullptr, nullptr);
   note_launch();
-  k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts, ws->counters, status);
+  k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts, ws->counters, status,
+                                   status_rows_max);
   note_launch();
   k_dd_emit<<<grid_for(t.n_buckets, kBlock), kBlock, 0, s>>>(t.slots, t.n_buckets, cand, dem, scratch_idx, out_coords,
                                                               out_sel);
@@ -2303,20 +2294,14 @@ int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t wid
   return check_batch(*n);
 }
 
-// status[0] = rows the global activate takes (0 when the dedup overflowed
-// its workspace prefix or met an out-of-range block), [1] = distinct rows, [2] = workspace flags; after
-// the activate [3] = global flags, [4] = new blocks.
+// ash_allocate_*: status[3] = global flags, [4] = new blocks after the
+// activate (written by the table sweep kernel; this kernel when the sweep
+// is switched off)
 __global__ void k_alloc_status(const int32_t* ws_counters, const int32_t* g_counters, int32_t* status, int phase) {
-  if (phase == 0) {
-    const int32_t count = ws_counters[ASH_CTR_COUNT], flags = ws_counters[ASH_CTR_FLAGS];
-    // an overflowed workspace or an out-of-range block leaves the map untouched
-    status[0] = (flags & (ASH_FLAG_TABLE_FULL | ASH_FLAG_RANGE)) ? 0 : count;
-    status[1] = count;
-    status[2] = flags;
-  } else {
-    status[3] = g_counters[ASH_CTR_FLAGS];
-    status[4] = g_counters[ASH_CTR_WINNERS];
-  }
+  (void)ws_counters;
+  (void)phase;
+  status[3] = g_counters[ASH_CTR_FLAGS];
+  status[4] = g_counters[ASH_CTR_WINNERS];
 }
 
 // The per-frame sequence is ~15 small launches (~75 us of host launch cost
@@ -2466,8 +2451,11 @@ static int allocate_sequence(ash_map_t* global, ash_map_t* ws, const Src& src, i
                              int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
                              int32_t* status, cudaStream_t s) {
   cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
-  run_dedup_select(make_table(ws), ws, src, n, out_blocks, nullptr, scratch_idx, scratch_mask, s, status);
-  if (int rc = insert_dn_impl(global, out_blocks, n, status, nullptr, 1, out_gi, out_gmask, s, status, true))
+  // at most capacity new blocks can commit: more distinct rows than that
+  // skip the device activate (status[0] = 0) and take the host path (growth)
+  const int64_t cap_rows = n < global->capacity ? n : global->capacity;
+  run_dedup_select(make_table(ws), ws, src, n, out_blocks, nullptr, scratch_idx, scratch_mask, s, status, cap_rows);
+  if (int rc = insert_dn_impl(global, out_blocks, cap_rows, status, nullptr, 1, out_gi, out_gmask, s, status, true))
     return rc;
   return check_launch("ash_allocate_blocks");
 }
@@ -2580,14 +2568,8 @@ static int claim_impl(ash_map_t* m, const int32_t* keys, int64_t n, const int32_
   cudaMemsetAsync(out_mask, 0, n, s);
   // 128-thread blocks: 0.302 ms against 0.310 at 256 and 0.330 at 512 (C2,
   // r01m A/B; 64 ties with 128): finer block turnover over the ~66 waves
-  if (d_n) {
-    const unsigned g = grid_for(n, kClaimBlock * kClaimRounds), cap = static_cast<unsigned>(device_sms()) * 16;
-    ASH_DISPATCH_ARITY(m->arity, (k_claim_dn<A, kClaimBlock><<<g < cap ? g : cap, kClaimBlock, 0, s>>>(
-                                     t, keys, n, out_idx, out_mask, m->counters, m->tile_counts, d_n)));
-  } else {
-    ASH_DISPATCH_ARITY(m->arity, (k_claim<A, kClaimBlock><<<grid_for(n, kClaimBlock * kClaimRounds), kClaimBlock, 0, s>>>(
-                                     t, keys, n, out_idx, out_mask, m->counters, m->tile_counts)));
-  }
+  ASH_DISPATCH_ARITY(m->arity, (k_claim<A, kClaimBlock><<<grid_for(n, kClaimBlock * kClaimRounds), kClaimBlock, 0, s>>>(
+                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts, d_n)));
   return check_launch("ash_insert_claim");
 }
 

@@ -400,8 +400,11 @@ __global__ void __launch_bounds__(kBlock) k_route_pull(const uint8_t* __restrict
                                                        const int32_t* __restrict__ jdx, int64_t n, PeerArgs pa,
                                                        uint32_t world, int32_t* __restrict__ out,
                                                        uint8_t* __restrict__ out_mask,
-                                                       const int64_t* __restrict__ cmat, uint32_t rank) {
+                                                       const int64_t* __restrict__ cmat, uint32_t rank,
+                                                       const int32_t* recv_status) {
   __shared__ const int32_t* s_base[kMaxWorld];
+  // an overflowed exchange stored nothing (and left jdx unwritten): no results
+  if (recv_status && recv_status[1]) return;
   for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
     int64_t off = pa.row_off[o];
     if (cmat) {  // this rank's first row at owner o: rows of the sources before it
@@ -612,7 +615,7 @@ int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t
     pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
   }
   k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, 0); note_launch();
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, 0, nullptr); note_launch();
   return rcheck("ash_route_pull");
 }
 
@@ -628,8 +631,8 @@ int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t ra
 }
 
 int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world, int32_t rank,
-                          const int64_t* count_matrix, const void* const* peer_ret, int32_t* out,
-                          uint8_t* out_mask, void* stream) {
+                          const int64_t* count_matrix, const int32_t* recv_status, const void* const* peer_ret,
+                          int32_t* out, uint8_t* out_mask, void* stream) {
   if (n < 0 || world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return rfail("bad routing arguments");
   if (n == 0) return ASH_OK;
   if (!owners || !jdx || !count_matrix || !peer_ret || !out) return rfail("null routing buffer");
@@ -640,7 +643,8 @@ int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, 
     pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
   }
   k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank));
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank),
+      recv_status);
   note_launch();
   return rcheck("ash_route_pull_counts");
 }

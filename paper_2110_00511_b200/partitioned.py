@@ -31,6 +31,10 @@ import torch.distributed as dist
 
 __all__ = ["PartitionedHashMap", "PartitionedResult", "CudaRouter"]
 
+# sync-free peer ops (device-sized shard op); ASH_PEER_DN=0 keeps the host
+# read of the count matrix inside each op
+_PEER_DN = __import__("os").environ.get("ASH_PEER_DN", "1") == "1"
+
 
 @dataclass
 class PartitionedResult:
@@ -287,13 +291,14 @@ class PeerExchange:
             rpay = self.recv_pay[:cap * self.pay_rb].view(dt).view(cap, *shape)
         return rkeys, rpay, status, (n, owners, jdx, mat)
 
-    def combine_dn(self, ctx):
+    def combine_dn(self, ctx, status):
         n, owners, jdx, mat = ctx
         self._barrier()  # every owner's results are in place
         out = torch.empty(n, dtype=torch.int32, device=self.device)
         msk = torch.empty(n, dtype=torch.uint8, device=self.device)
         self._lib.call("ash_route_pull_counts", owners.data_ptr(), jdx.data_ptr(), n, self.world, self.rank,
-                       mat.data_ptr(), self._p_ret, out.data_ptr(), msk.data_ptr(), self._stream())
+                       mat.data_ptr(), status.data_ptr(), self._p_ret, out.data_ptr(), msk.data_ptr(),
+                       self._stream())
         self._barrier()  # all pulls done: buffers reusable
         return out, msk.view(torch.bool)
 
@@ -414,11 +419,12 @@ class PartitionedHashMap:
                     raise ValueError(f"value batch has shape {tuple(vals[0].shape)}, expected "
                                      f"({keys.shape[0]}, {', '.join(map(str, specs[0].shape))})")
                 vals = [v]
-        if op != "erase" and hasattr(self.local, "_op_into_dn") and self.local._dn_ready(op, self.peer.capacity):
+        if (op != "erase" and _PEER_DN and hasattr(self.local, "_op_into_dn")
+                and self.local._dn_ready(op, self.peer.capacity)):
             # sync-free: the shard op reads its batch length on the device
             rkeys, rpay, status, ctx = self.peer.dispatch_dn(keys, vals[0] if vals else None)
             self.local._op_into_dn(op, rkeys, [rpay] if rpay is not None else [], self.peer.ret, status)
-            out, msk = self.peer.combine_dn(ctx)
+            out, msk = self.peer.combine_dn(ctx, status)
             if not int(status[1].item()):  # the one host read: did a receive buffer overflow?
                 self.local._dn_done(op)
                 return PartitionedResult(out, msk, ctx[1])
