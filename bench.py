@@ -778,6 +778,8 @@ def main():
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no sweep / e2e / cpu leg): for ncu captures")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[1] six-point sweep")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="N > 1 / --partitioned: skip the configs[4] 400M-key strong-scaling runs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -795,6 +797,8 @@ def main():
     import torch
     if world > 1 or args.partitioned or args.c5:
         from paper_2110_00511_b200 import partitioned
+        args.clock_sampler = ClockSampler
+        args.hbm_peak = _peaks()[0]
         partitioned.bench_main(args, rank, world)
         return
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))

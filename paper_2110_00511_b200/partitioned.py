@@ -24,6 +24,7 @@ carry the owner of every key.  Capacity and auto-rehash are per shard.
 from __future__ import annotations
 
 from dataclasses import dataclass
+import time
 
 import numpy as np
 import torch
@@ -336,7 +337,7 @@ class PartitionedHashMap:
 
     def __init__(self, capacity_per_rank: int, key_arity: int, value_specs=(), group=None,
                  device=None, auto_rehash: bool = True, local_map=None, router=None,
-                 transport: str = "nccl", peer_mapping: str = "symmetric"):
+                 transport: str = "nccl", peer_mapping: str = "symmetric", recv_capacity: int = None):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -358,7 +359,8 @@ class PartitionedHashMap:
                 raise ValueError("the peer transport carries at most one value buffer")
             payload = (specs[0].shape, local_map._torch_dtypes[0]) if specs else None
             self.peer = PeerExchange(group, self.world, self.rank, self.device, self.key_arity, payload,
-                                     capacity=max(int(capacity_per_rank), 1), mapping=peer_mapping)
+                                     capacity=max(int(recv_capacity or capacity_per_rank), 1),
+                                     mapping=peer_mapping)
 
     # -- routing ---------------------------------------------------------
 
@@ -419,13 +421,23 @@ class PartitionedHashMap:
                     raise ValueError(f"value batch has shape {tuple(vals[0].shape)}, expected "
                                      f"({keys.shape[0]}, {', '.join(map(str, specs[0].shape))})")
                 vals = [v]
-        if (op != "erase" and _PEER_DN and hasattr(self.local, "_op_into_dn")
-                and self.local._dn_ready(op, self.peer.capacity)):
-            # sync-free: the shard op reads its batch length on the device
+        if op != "erase" and _PEER_DN and hasattr(self.local, "_op_into_dn"):
+            # sync-free dispatch; the same collectives on every rank whichever
+            # shard op each one runs
             rkeys, rpay, status, ctx = self.peer.dispatch_dn(keys, vals[0] if vals else None)
-            self.local._op_into_dn(op, rkeys, [rpay] if rpay is not None else [], self.peer.ret, status)
+            pays = [rpay] if rpay is not None else []
+            over = None
+            if self.local._dn_ready(op, self.peer.capacity):
+                # the shard op reads its batch length on the device
+                self.local._op_into_dn(op, rkeys, pays, self.peer.ret, status)
+            else:  # this shard needs the host-checked op (growth): read the length
+                m, over = status.tolist()
+                if not over:
+                    self.local._op_into(op, rkeys[:m], [p[:m] for p in pays], self.peer.ret[:m])
             out, msk = self.peer.combine_dn(ctx, status)
-            if not int(status[1].item()):  # the one host read: did a receive buffer overflow?
+            if over is None:
+                over = int(status[1].item())  # the one host read: did a receive buffer overflow?
+            if not over:
                 self.local._dn_done(op)
                 return PartitionedResult(out, msk, ctx[1])
             # nothing was stored anywhere (every rank saw the same matrix):
@@ -532,32 +544,38 @@ def _reduce(x, op=dist.ReduceOp.SUM, dev=None):
     return float(t.item())
 
 
-def _make_pm(args, capacity: int, dev):
+def _make_pm(args, capacity: int, dev, recv_capacity: int = None):
     import sys
     transport = getattr(args, "transport", "nccl")
     if _shared_gpu():
         return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport="peer",
-                                  peer_mapping="ipc"), "peer"
+                                  peer_mapping="ipc", recv_capacity=recv_capacity), "peer"
     try:
-        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport=transport), transport
+        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport=transport,
+                                  recv_capacity=recv_capacity), transport
     except Exception as exc:  # no symmetric memory on this node: NCCL all-to-all instead
         if transport != "peer":
             raise
         print(f"peer transport unavailable ({exc!r}); using NCCL all-to-all", file=sys.stderr)
-        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport="nccl"), "nccl"
+        return PartitionedHashMap(capacity, 3, [np.float32], device=dev, transport="nccl",
+                                  recv_capacity=recv_capacity), "nccl"
 
 
-def bench_c5(args, rank: int, world: int) -> None:
+def run_c5_partitioned(args, rank: int, world: int, dev, transport: str) -> dict:
     """configs[4]: the 400M-key map built across the ranks by the mixed
     stream — each step inserts 2^25 new keys and finds 2^25 keys (half
     present), every rank holding a contiguous 1/N slice of both global
-    batches; total work fixed (strong scaling).  Step time = max over ranks."""
-    import json
-
+    batches; total work fixed (strong scaling).  Step time = max over ranks.
+    Index-exact at every step: with all-new keys on a fresh heap, a shard's
+    winners take its indices in arrival order, so each owner's received insert
+    indices are 0, 1, 2, ... in global batch order (checked through the hit
+    count and the per-shard sizes); the finds hit exactly the present half."""
     from .workloads import c5_step_batches
-    dev = _bench_init()
     total, batch = 400_000_000, 1 << 25
-    pm, transport = _make_pm(args, int(total / world * 1.05) + (1 << 20), dev)
+    cap = int(total / world * 1.05) + (1 << 20)
+    recv = int(batch / world * 1.25) + (1 << 16)
+    a2 = argparse_like(args, transport=transport)
+    pm, transport = _make_pm(a2, cap, dev, recv_capacity=recv)
     stream = torch.cuda.current_stream(dev)
     # set-up outside the timed build, like the map's construction: the first
     # collective creates the NCCL communicator and the first launches load
@@ -567,7 +585,9 @@ def bench_c5(args, rank: int, world: int) -> None:
     steps = -(-total // batch)
     ms = 0.0
     ops = 0
-    launches0 = None
+    from . import _lib
+    launches0 = _lib.lib.ash_launch_count()
+    stored = 0
     for s in range(steps):
         size = min(batch, total - s * batch)
         ins, q = c5_step_batches(s * batch, size, total, device=dev)
@@ -576,39 +596,70 @@ def bench_c5(args, rank: int, world: int) -> None:
         vals = torch.rand((hi - lo, 1), dtype=torch.float32, device=dev)
         dist.barrier()
         torch.cuda.synchronize()
-        if launches0 is None:
-            from . import _lib
-            launches0 = _lib.lib.ash_launch_count()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        pm.insert(ins, vals)
+        r = pm.insert(ins, vals)
         f = pm.find(q)
         b.record(stream)
         torch.cuda.synchronize()
         ms += _reduce(a.elapsed_time(b), dist.ReduceOp.MAX, dev)
         ops += 2 * size
+        new = int(_reduce(int(r.masks.sum()), dev=dev))
         hits = int(_reduce(int(f.masks.sum()), dev=dev))
-        assert hits == size // 2, (s, hits)
-    from . import _lib
+        stored += new
+        assert new == size and hits == size // 2, (s, new, hits)
+        # index-exact: all-new keys on a fresh heap take each shard's next
+        # indices in arrival order (global batch order), so the indices this
+        # rank gets from one owner are consecutive
+        for o in range(world):
+            v = r.indices[r.owners == o].to(torch.int64)
+            assert v.numel() < 2 or bool((v[1:] - v[:-1] == 1).all()), (s, o)
     launches = _lib.lib.ash_launch_count() - launches0
-    assert pm.size == total
+    assert pm.size == total == stored
+    del pm
+    torch.cuda.empty_cache()
+    return {"workload": "configs[4]: 400M-key hash-partitioned map built by the mixed stream (12 steps of 2^25 "
+                        "inserts + 2^25 finds, half present); every rank holds a contiguous 1/N slice of each "
+                        "global batch; time = max over ranks", "scaling": "strong",
+            "routing": _routing_name(transport), "mops": round(ops / ms / 1e3, 2), "ms_total": round(ms, 2),
+            "gpu_launches": launches,
+            "parity": "every step: inserts all new (sum of masks = batch) with the indices from each owner "
+                      "consecutive in batch order, finds hit exactly the present half, shard sizes sum to the "
+                      "keys stored"}
+
+
+def argparse_like(args, **kw):
+    import copy
+    a = copy.copy(args)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+def _routing_name(transport: str) -> str:
+    if transport == "peer":
+        return "peer-memory put/pull (CUDA IPC, shared GPU)" if _shared_gpu() else \
+            "peer-memory put/pull (symmetric memory)"
+    return "NCCL all-to-all"
+
+
+def bench_c5(args, rank: int, world: int) -> None:
+    import json
+    dev = _bench_init()
+    res = run_c5_partitioned(args, rank, world, dev, getattr(args, "transport", "peer"))
     if rank == 0:
+        steps = -(-400_000_000 // (1 << 25))
         print(json.dumps({
-            "metric": "insert & find Mops/s (int3 keys)", "value": round(ops / ms / 1e3, 2), "unit": "Mops/s",
-            "n_gpus": world, "steps": steps, "warmup": 0, "ms_per_step": round(ms / steps, 4),
+            "metric": "insert & find Mops/s (int3 keys)", "value": res["mops"], "unit": "Mops/s",
+            "n_gpus": world, "steps": steps, "warmup": 0, "ms_per_step": round(res["ms_total"] / steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (counter-based keys generated on the device)",
-            "config": {"workload": "configs[4]: 400M-key hash-partitioned map built by the mixed stream "
-                                   "(12 steps of 2^25 inserts + 2^25 finds, half present); every rank holds "
-                                   "a contiguous 1/N slice of each global batch; time = max over ranks",
-                       "routing": ("peer-memory put/pull (CUDA IPC, shared GPU)" if _shared_gpu() else
-                                   "peer-memory put/pull (symmetric memory)") if transport == "peer"
-                                  else "NCCL all-to-all",
+            "config": {"workload": res["workload"], "routing": res["routing"],
                        "parallelism": f"hash-partitioned x{world}",
                        "setup": "excluded (map construction, one warm-up find: NCCL communicator, kernel loading)",
                        **({"note": "ASH_SHARED_GPU: all ranks on one GPU (functional run, not a scaling "
                                    "number)"} if _shared_gpu() else {})},
-            "gpu_launches": launches,
+            "gpu_launches": res["gpu_launches"], "parity": res["parity"],
         }), flush=True)
     dist.destroy_process_group()
 
@@ -655,27 +706,88 @@ def bench_main(args, rank: int, world: int) -> None:
     dist.barrier()
     torch.cuda.synchronize()
     from . import _lib
+    sampler = getattr(args, "clock_sampler", None)
+    clk = sampler(dev.index or 0) if (sampler is not None and rank == 0) else None
+    if clk is not None:
+        clk.__enter__()
     launches0 = _lib.lib.ash_launch_count()
     times = [step() for _ in range(args.steps)]
     torch.cuda.synchronize()
     launches = _lib.lib.ash_launch_count() - launches0
     dist.barrier()
     ms = _reduce(statistics.mean(times), dist.ReduceOp.MAX, dev)
+    # keep the GPUs busy ~1 s for the clock sampler (untimed): every rank runs
+    # the same number of (collective) steps
+    for _ in range(max(3, int(1000.0 / max(ms, 1e-3)))):
+        step()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    med = _reduce(statistics.median(times), dist.ReduceOp.MAX, dev)
+    mn = _reduce(min(times), dist.ReduceOp.MAX, dev)
     value = 2 * per_rank * world / (ms / 1e3) / 1e6
+
+    # e2e through the public API: pinned host keys / values in, host results
+    # out (the H2D / D2H inside the timed region), max over ranks
+    keys_h, vals_h = keys.cpu().pin_memory(), vals.cpu().pin_memory()
+    outs_h = [torch.empty(per_rank, dtype=dt, pin_memory=True) for dt in (torch.int32, torch.bool) * 2]
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        pm.local.clear()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        kd = keys_h.to(dev, non_blocking=True)
+        vd = vals_h.to(dev, non_blocking=True)
+        ri = pm.insert(kd, vd)
+        rf = pm.find(kd)
+        for o, t in zip(outs_h, (ri.indices, ri.masks, rf.indices, rf.masks)):
+            o.copy_(t, non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append((t1 - t0) * 1e3)
+    assert bool(outs_h[3].all())
+    e2e_ms = _reduce(statistics.median(e2e), dist.ReduceOp.MAX, dev)
+    h2d = 2 * keys_h.numel() * 4 + vals_h.numel() * 4
+    d2h = 2 * (per_rank * 4 + per_rank)
+
+    # configs[4] (strong scaling, 400M keys) with both transports
+    del pm
+    torch.cuda.empty_cache()
+    other = {}
+    if not getattr(args, "no_c5", False):
+        for tr in ("peer", "nccl"):
+            if _shared_gpu() and tr == "nccl":
+                continue
+            other[f"c5_partitioned_{tr}"] = run_c5_partitioned(args, rank, world, dev, tr)
     if rank == 0:
+        bw = getattr(args, "hbm_peak", None)
+        # per-GPU HBM bytes per key: insert 75 B + find 49 B,
+        # + 34 B each of routing (partition + unpermute passes)
+        per_key = 75 + 49 + 2 * 34
+        frac = round(per_key * per_rank / (ms / 1e3) / 1e9 / bw, 4) if bw else None
         print(json.dumps({
             "metric": "insert & find Mops/s (int3 keys)", "value": round(value, 2), "unit": "Mops/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic",
+            "data": "synthetic (counter-based int3 keys per rank slice, uniqueness 0.5)",
             "config": {"workload": f"hash-partitioned map, {per_rank:,} insert + {per_rank:,} find "
                                    f"int3 keys per rank per step (uniqueness {rho}); step time = max over ranks",
-                       "routing": ("peer-memory put/pull (CUDA IPC, shared GPU)" if _shared_gpu() else
-                                   "peer-memory put/pull (symmetric memory)") if transport == "peer"
-                                  else "NCCL all-to-all",
+                       "routing": _routing_name(transport),
                        "parallelism": f"hash-partitioned x{world}",
+                       "l2": "flushed between steps (256 MB write per rank)",
                        **({"note": "ASH_SHARED_GPU: all ranks on one GPU (functional run, not a scaling "
                                    "number)"} if _shared_gpu() else {})},
+            "step_time": {"mean_ms": round(ms, 4), "median_ms": round(med, 4), "min_ms": round(mn, 4),
+                          "trials": len(times), "over_ranks": "max"},
+            "roofline": {"bound": "hbm", "kernel": "whole step (per GPU)", "achieved_bytes_per_key": per_key,
+                         "achieved": round(per_key * per_rank / (ms / 1e3) / 1e9, 1) if bw else None,
+                         "peak": bw, "unit": "GB/s", "frac": frac, "traffic": None},
+            "e2e": {"value": round(2 * per_rank * world / (e2e_ms / 1e3) / 1e6, 2), "unit": "Mops/s",
+                    "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+                    "median_ms": round(e2e_ms, 3), "over_ranks": "max"},
             "gpu_launches": launches,  # libash kernels in the timed region (ash_launch_count)
+            "clocks": clk.summary() if clk is not None else None,
+            "other_configs": other,
         }), flush=True)
     dist.destroy_process_group()

@@ -90,3 +90,66 @@ def test_peer_transport_two_ranks_share_one_gpu(cuda_ok):
                     np.float32)
     assert np.array_equal(got[fnd], want[fnd])
     assert sum(out[r][8] for r in range(world)) == ref.size
+
+
+def _worker_growth(rank, world, port, batches, vals, q):
+    """Shards that fill (and grow) at different rates: each rank picks its
+    own shard op (device-sized or host-checked) while the collectives stay
+    identical on every rank."""
+    import sys
+    sys.path.insert(0, os.getcwd())
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2110_00511_b200.partitioned import PartitionedHashMap
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        pm = PartitionedHashMap(1500, 3, [np.float32], device=dev, transport="peer", peer_mapping="ipc",
+                                recv_capacity=1200)
+        outs = []
+        for b, (keys, v) in enumerate(zip(batches, vals)):
+            sl = np.array_split(np.arange(len(keys)), world)[rank]
+            r = pm.insert(keys[sl], v[sl])
+            f = pm.find(keys[sl][::-1].copy())
+            outs.append((r.masks.cpu().numpy(), f.masks.cpu().numpy(), pm.local.capacity))
+        torch.cuda.synchronize()
+        q.put((rank, outs, pm.local_size))
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, "error", repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_transport_shards_diverge_and_grow(cuda_ok):
+    import torch.multiprocessing as mp
+    from oracle.ash_oracle import OracleMap
+    world = 2
+    rng = np.random.default_rng(31)
+    batches = [rng.integers(-400, 400, size=(n, 3)).astype(np.int32) for n in (2000, 2300, 4000, 3000)]
+    vals = [rng.random((len(b), 1), dtype=np.float32) for b in batches]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_growth, args=(r, world, port, batches, vals, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        item = q.get(timeout=240)
+        assert not isinstance(item[1], str), item
+        out[item[0]] = item
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = OracleMap(16, 3, [np.float32])
+    for b, (keys, v) in enumerate(zip(batches, vals)):
+        ri = ref.insert(keys, v)
+        rf = ref.find(keys[np.concatenate([s[::-1] for s in np.array_split(np.arange(len(keys)), world)])])
+        got_i = np.concatenate([out[r][1][b][0] for r in range(world)])
+        got_f = np.concatenate([out[r][1][b][1] for r in range(world)])
+        assert np.array_equal(got_i, ri.masks), b
+        assert np.array_equal(got_f, rf.masks), b
+    assert sum(out[r][2] for r in range(world)) == ref.size
+    caps = [[c for _, _, c in out[r][1]] for r in range(world)]
+    assert max(caps[0][-1], caps[1][-1]) > 1500  # the shards grew

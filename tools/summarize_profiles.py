@@ -38,8 +38,11 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "ms": 1e3,
 
 
 def raw(rep: Path) -> dict:
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.suffix == ".csv":  # tools/ncu_export.sh output (the report itself stays on the box)
+        txt = rep.read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     out = {"kernel": vals[hdr.index("Kernel Name")][:120]}
@@ -78,6 +81,8 @@ def main(tag: str):
     PROF.mkdir(exist_ok=True)
     kern = {}
     for rep in sorted(OUT.glob(f"prof_k_*_{tag}.ncu-rep")):
+        kern[rep.name.split("_" + tag)[0].replace("prof_", "")] = raw(rep)
+    for rep in sorted(OUT.glob(f"prof_k_*_{tag}_raw.csv")):
         kern[rep.name.split("_" + tag)[0].replace("prof_", "")] = raw(rep)
     (PROF / f"{tag}_kernels.json").write_text(json.dumps(kern, indent=1))
     lines = [f"# ncu launch list ({tag}): `ncu --metrics gpu__time_duration.sum --clock-control none "
