@@ -248,6 +248,10 @@ def run_reference(args, rank: int, world: int):
     other = {"c1": cpu_c1(ref, settings)}
     if not args.no_sweep:
         other["sweep"] = cpu_sweep(ref, best, times)
+    other["c3_voxelize"] = {"workload": "configs[2]: voxel_downsample of the 20M unit-sphere cloud (float64) at 5 mm",
+                            **cpu_c3(ref)}
+    other["c4_allocate_blocks"] = {"workload": "configs[3]: allocate_blocks map calls, 640x480 plane frame",
+                                   **cpu_c4(ref)}
     sample = (f"per step: the identical configs[1] workload (gen_keys(10M, 0.5, seed 0), f32[1] values, fresh "
               f"capacity-10M map, insert + find), {where}, threads={best} (the faster of threads=1 and "
               f"threads={ncpu} over the warm-up steps)")
@@ -280,6 +284,41 @@ def cpu_c1(ref, settings, trials: int = 10):
                                "min_ms": round(min(ts) * 1e3, 2),
                                "mops_at_median": round(2 * len(keys) / statistics.median(ts) / 1e6, 3)}
     return out
+
+
+def cpu_c3(ref, n_sample: int = 2_000_000) -> dict:
+    """configs[2] on the CPU: the reference's voxel_downsample
+    (geometry.py:59-76) on the first n_sample points of the same 20M sphere
+    cloud (float64, 5 mm), points per second."""
+    pts = _workloads().sphere_points(20_000_000, seed=0)[:n_sample]
+    t0 = time.perf_counter()
+    ref.voxel_downsample(pts, 0.005)
+    dt = time.perf_counter() - t0
+    return {"mpts_per_s": round(n_sample / dt / 1e6, 3), "cores": 1,
+            "sample": f"first {n_sample:,} points of the configs[2] cloud"}
+
+
+def cpu_c4(ref) -> dict:
+    """configs[3] on the CPU: the map calls of VoxelBlockGrid.allocate_blocks
+    (tsdf/grid.py:136-150: local activate, global activate + find, local
+    value scatter) on one 640x480 plane frame's 1,536,000 candidates, with
+    the reference's HashMap; candidates per second."""
+    from oracle import ash_oracle as O  # the candidate list only (pinned by golden alloc_blocks)
+    cam = O.scaled_camera(640, 480)
+    coords = O.candidate_blocks(O.plane_depth(cam, 1.0), cam, np.eye(4), 0.0058 * 8, 0.04)
+    gm = ref.HashMap(100_000, 3, [((8, 8, 8, 2), np.float32)])
+    t0 = time.perf_counter()
+    local = ref.HashMap(len(coords), 3, [np.int32])
+    li, lmask = local.activate(coords)
+    li, lmask = np.asarray(li), np.asarray(lmask)
+    surv = coords[lmask]
+    gm.activate(surv)
+    gi, gmask = gm.find(surv)
+    local.value_buffer(0)[li[lmask], 0] = np.asarray(gi)
+    dt = time.perf_counter() - t0
+    assert bool(np.asarray(gmask).all())
+    return {"mcand_per_s": round(len(coords) / dt / 1e6, 3), "cores": 1,
+            "sample": "the first plane frame (1,536,000 candidates), map calls of grid.py:136-150"}
 
 
 def cpu_sweep(ref, threads, headline_times):
@@ -541,12 +580,9 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
     c3 = {"workload": "configs[2]: voxel_downsample of 20M unit-sphere points (float64) at 5 mm",
           "voxels": int(coords.shape[0]), "ms": round(ms, 3), "mpts_per_s": round(20e6 / ms / 1e3, 1),
           "note": "includes the count read-back (one 8-byte sync) that sizes the outputs"}
+    ref, ref_kind, _ = load_reference() if with_cpu else (None, None, None)
     if with_cpu:
-        smp = pts_np[:2_000_000]
-        t0 = time.perf_counter()
-        O.voxel_downsample(smp, 0.005)
-        c3["cpu_baseline"] = {"mpts_per_s": round(2.0 / (time.perf_counter() - t0), 3), "cores": 1,
-                              "kind": "port", "sample": "first 2M points of the same cloud"}
+        c3["cpu_baseline"] = {**cpu_c3(ref), "kind": ref_kind}
     out["c3_voxelize"] = c3
     cam = O.scaled_camera(640, 480)
     depth = O.plane_depth(cam, 1.0)
@@ -575,11 +611,7 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
           "mcand_per_s": round(len(frames[0]) / ms / 1e3, 1),
           "note": "includes the host syncs of the boolean-mask gathers in the reference call sequence"}
     if with_cpu:
-        og = O.OracleMap(100_000, 3, [((8, 8, 8, 2), np.float32)])
-        t0 = time.perf_counter()
-        O.allocate_blocks_map_calls(og, frames[0])
-        c4["cpu_baseline"] = {"mcand_per_s": round(len(frames[0]) / (time.perf_counter() - t0) / 1e6, 3),
-                              "cores": 1, "kind": "port", "sample": "first frame"}
+        c4["cpu_baseline"] = {**cpu_c4(ref), "kind": ref_kind}
     out["c4_allocate_blocks"] = c4
     # the same frames end to end from the depth image: fused candidate
     # generation + dedup on the device (§8(f) row 1), then the global activate

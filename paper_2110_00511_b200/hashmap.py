@@ -815,12 +815,32 @@ class HashMap:
             self._size_known = False
 
     def _dn_done(self, op: str) -> None:
-        """After the op's host read: a device-sized insert can only fail on a
-        probe chain past the device bound (load <= 0.75: not in practice);
-        fail loudly rather than return wrong indices."""
-        if op != "find" and int(self._counters[_lib.CTR_FLAGS].item()) & (_lib.FLAG_CAPACITY |
-                                                                           _lib.FLAG_TABLE_FULL):
-            raise RuntimeError("device-sized insert could not place every key (probe bound); rebuild the map")
+        """After a device-sized insert: it can only fail on a probe chain past
+        the device bound (load <= 0.75: not in practice).  The flags word is
+        copied to pinned memory behind the op and checked at the next call
+        (``_dn_check``), so the op itself never waits; a failure is raised
+        loudly rather than returning wrong indices silently."""
+        if op == "find":
+            return
+        if getattr(self, "_dn_flags_h", None) is None:
+            self._dn_flags_h = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            self._dn_flags_ev = torch.cuda.Event()
+        self._dn_check()  # the previous one's flags (long arrived: one op back)
+        self._dn_flags_h.copy_(self._counters[_lib.CTR_FLAGS:_lib.CTR_FLAGS + 1], non_blocking=True)
+        self._dn_flags_ev.record(torch.cuda.current_stream(self._device))
+        self._dn_pending = True
+
+    def _dn_check(self, wait: bool = True) -> None:
+        """Raise if a previous device-sized insert failed; wait=False only
+        looks when its flags have already arrived (never blocks)."""
+        if getattr(self, "_dn_pending", False):
+            if not wait and not self._dn_flags_ev.query():
+                return
+            self._dn_flags_ev.synchronize()
+            self._dn_pending = False
+            if int(self._dn_flags_h[0]) & (_lib.FLAG_CAPACITY | _lib.FLAG_TABLE_FULL):
+                raise RuntimeError("a device-sized insert could not place every key (probe bound); "
+                                   "rebuild the map")
 
     @on_device
     def find(self, keys) -> BatchResult:

@@ -146,11 +146,14 @@ class PeerExchange:
             self.pay_rb = int(np.prod(shape)) * torch.empty(0, dtype=dt).element_size()
         self._scratch = torch.empty(0, dtype=torch.int32, device=device)
         self._mat_h = self._mat_ev = None
+        self._flag_h = self._flag_ev = None
         self.capacity = 0
         self._alloc(capacity)
 
     def _alloc(self, cap: int) -> None:
         cap = max(int(cap), 1)
+        if getattr(self, "recv_keys", None) is not None:
+            self._barrier()  # peers may still read the old buffers (no trailing barrier per op)
         sizes = [(cap * self.arity, torch.int32), (cap, torch.int32)]
         if self.pay_rb:
             sizes.append((cap * self.pay_rb, torch.uint8))
@@ -275,6 +278,13 @@ class PeerExchange:
         status = torch.empty(2, dtype=torch.int32, device=self.device)
         lib.call("ash_route_recv_status", mat.data_ptr(), self.world, self.rank, self.capacity,
                  status.data_ptr(), self._stream())
+        # the overflow flag reaches the host early in the op (its first
+        # kernels): the op's end waits for this event, not for the pull
+        if self._flag_h is None:
+            self._flag_h = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+            self._flag_ev = torch.cuda.Event()
+        self._flag_h.copy_(status, non_blocking=True)
+        self._flag_ev.record(torch.cuda.current_stream(self.device))
         jdx = torch.empty(n, dtype=torch.int32, device=self.device)
         rb = self.pay_rb if (payload is not None and n) else 0
         if rb:
@@ -300,7 +310,11 @@ class PeerExchange:
         self._lib.call("ash_route_pull_counts", owners.data_ptr(), jdx.data_ptr(), n, self.world, self.rank,
                        mat.data_ptr(), status.data_ptr(), self._p_ret, out.data_ptr(), msk.data_ptr(),
                        self._stream())
-        self._barrier()  # all pulls done: buffers reusable
+        # no trailing barrier: the next op's put writes only the receive
+        # buffers (read by this op's shard op, which every rank finished
+        # before the barrier above), and its shard op writes the result
+        # buffers only after its own post-put barrier, which no rank reaches
+        # before its pull here is done
         return out, msk.view(torch.bool)
 
     def combine(self, local_idx, ctx) -> torch.Tensor:
@@ -314,7 +328,11 @@ class PeerExchange:
         msk = torch.empty(n, dtype=torch.uint8, device=self.device)
         self._lib.call("ash_route_pull", owners.data_ptr(), jdx.data_ptr(), n, self.world, offs,
                        self._p_ret, out.data_ptr(), msk.data_ptr(), self._stream())
-        self._barrier()  # all pulls done: buffers reusable
+        # no trailing barrier: the next op's put writes only the receive
+        # buffers (read by this op's shard op, which every rank finished
+        # before the barrier above), and its shard op writes the result
+        # buffers only after its own post-put barrier, which no rank reaches
+        # before its pull here is done
         return out, msk.view(torch.bool)
 
 
@@ -421,6 +439,8 @@ class PartitionedHashMap:
                     raise ValueError(f"value batch has shape {tuple(vals[0].shape)}, expected "
                                      f"({keys.shape[0]}, {', '.join(map(str, specs[0].shape))})")
                 vals = [v]
+        if hasattr(self.local, "_dn_check"):
+            self.local._dn_check(wait=False)  # a previous device-sized insert's flags, if arrived
         if op != "erase" and _PEER_DN and hasattr(self.local, "_op_into_dn"):
             # sync-free dispatch; the same collectives on every rank whichever
             # shard op each one runs
@@ -435,8 +455,9 @@ class PartitionedHashMap:
                 if not over:
                     self.local._op_into(op, rkeys[:m], [p[:m] for p in pays], self.peer.ret[:m])
             out, msk = self.peer.combine_dn(ctx, status)
-            if over is None:
-                over = int(status[1].item())  # the one host read: did a receive buffer overflow?
+            if over is None:  # the one host read: did a receive buffer overflow?
+                self.peer._flag_ev.synchronize()
+                over = int(self.peer._flag_h[1])
             if not over:
                 self.local._dn_done(op)
                 return PartitionedResult(out, msk, ctx[1])
@@ -498,6 +519,8 @@ class PartitionedHashMap:
 
     @property
     def local_size(self) -> int:
+        if hasattr(self.local, "_dn_check"):
+            self.local._dn_check()
         return int(self.local.size)
 
     @property
