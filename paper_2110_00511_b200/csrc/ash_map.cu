@@ -1775,13 +1775,16 @@ struct FrameSrc {
   int per_pixel;  // n_steps (ray) or 27 (neighbor)
   int neighbor;
   double fx, fy, cx, cy, dmin, dmax, trunc, two_trunc, step, block;
+  double rblock;  // RN(1 / block), for quantize_fast
   double R[9], tr[3];
-  __device__ __forceinline__ bool key(int64_t p, Key<3>& k, bool* bad) const {
-    const int64_t pix = p / per_pixel;
-    const int s = static_cast<int>(p - pix * per_pixel);
+  __device__ __forceinline__ bool key(int64_t p64, Key<3>& k, bool* bad) const {
+    // positions < 2^30 (check_batch): 32-bit divisions
+    const uint32_t p = static_cast<uint32_t>(p64);
+    const uint32_t pix = p / static_cast<uint32_t>(per_pixel);
+    const int s = static_cast<int>(p - pix * static_cast<uint32_t>(per_pixel));
     const double z = __ldg(depth + pix);
     if (!(z > 0.0 && z >= dmin && z <= dmax)) return false;  // Frame.valid_mask (types.py:67-69)
-    const int64_t v = pix / width, u = pix - v * width;
+    const uint32_t v = pix / static_cast<uint32_t>(width), u = pix - v * static_cast<uint32_t>(width);
     const double x = __ddiv_rn(__dsub_rn(static_cast<double>(u), cx), fx);
     const double y = __ddiv_rn(__dsub_rn(static_cast<double>(v), cy), fy);
     double d = z;
@@ -1794,7 +1797,7 @@ struct FrameSrc {
     for (int i = 0; i < 3; ++i) {
       const double wi = __dadd_rn(__fma_rn(p2, R[3 * i + 2], __fma_rn(p1, R[3 * i + 1], __dmul_rn(p0, R[3 * i]))),
                                   tr[i]);
-      k.w[i] = static_cast<uint32_t>(quantize_one<double>(wi, block, bad));
+      k.w[i] = static_cast<uint32_t>(quantize_fast<double>(wi, block, rblock, bad));  // floor(wi / block), exact
     }
     if (neighbor) {  // lattice_offsets(1)[s], lexicographic; int32 wrap
       k.w[0] += static_cast<uint32_t>(s / 9 - 1);
@@ -2330,6 +2333,7 @@ int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t wid
   f->two_trunc = 2 * trunc;
   f->step = block_size / 2;
   f->block = block_size;
+  f->rblock = 1.0 / block_size;
   // n_steps = int(ceil(2 * trunc / step)) + 1 (tsdf/grid.py:117)
   const double ns = ceil((2 * trunc) / f->step) + 1;
   if (!(ns >= 1 && ns <= 4096)) return fail(ASH_ERR_INVALID, "too many ray samples per pixel");

@@ -151,3 +151,28 @@ def test_fused_allocate_workspace_overflow_leaves_map_untouched(ash):
     G.eq(gi, gi_ref, "gi")
     assert gm.size == og.size
     gm.validate()
+
+
+def test_graph_replay_alternating_sequences(ash):
+    """Two frames of different sizes alternate (each sequence is captured on
+    its second occurrence and replayed after that, with the claim re-pointed
+    at the frame's rows): every call equals the oracle's map calls."""
+    from oracle import ash_oracle as O
+    cams = [O.scaled_camera(160, 120), O.scaled_camera(200, 150)]
+    frames = []
+    for i, cam in enumerate(cams):
+        depth = O.sphere_depth(cam) if i else O.plane_depth(cam, 1.0)
+        for f in range(3):
+            pose = np.eye(4)
+            pose[0, 3] = 0.03 * f
+            frames.append(O.candidate_blocks(depth, cam, pose, BLOCK, TRUNC))
+    order = [0, 3, 1, 4, 2, 5, 0, 3, 1, 4, 2, 5]
+    gm = ash.HashMap(20_000, 3, [((8, 8, 8, 2), np.float32)], device="cuda")
+    og = O.OracleMap(20_000, 3, [((8, 8, 8, 2), np.float32)])
+    for i in order:
+        gi, _ = ash.allocate_blocks(gm, frames[i])
+        gi_ref, _, _, _ = O.allocate_blocks_map_calls(og, frames[i])
+        G.eq(gi, gi_ref, f"frame {i}")
+    assert gm.size == og.size
+    G.bytes_eq(gm.key_buffer, og.key_buffer, "keys")
+    gm.validate()
