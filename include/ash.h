@@ -312,10 +312,14 @@ int ash_insert_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_
  * flags, [3] global flags (ASH_FLAG_CAPACITY / TABLE_FULL: roll back
  * [0] claims and redo the activate on the host path), [4] new blocks.
  * out_blocks: n x 3, out_gi / out_gmask: n entries; scratch as for
- * ash_unique_rows; global tile workspace for n positions. */
+ * ash_unique_rows; global tile workspace for n positions.  small_activate:
+ * run the activate in one block (up to 8192 distinct rows; more leave
+ * status[0] = 0 and nothing claimed, for the host path): the caller's
+ * choice from the previous frame's count. */
 int ash_allocate_blocks(ash_map_t* global, ash_map_t* ws, const int32_t* coords, int64_t n,
                         int32_t* out_blocks, int32_t* out_gi, uint8_t* out_gmask,
-                        int32_t* scratch_idx, uint8_t* scratch_mask, int32_t* status, void* stream);
+                        int32_t* scratch_idx, uint8_t* scratch_mask, int32_t* status,
+                        int32_t small_activate, void* stream);
 
 /* Copy rows [0, min(*d_count, cap)) of two arrays (row sizes multiples of 4
  * bytes) in one launch: the caller's own copies of a fused allocate's
@@ -330,7 +334,7 @@ int ash_allocate_frame(ash_map_t* global, ash_map_t* ws, const double* depth, in
                        int64_t width, const double* cam, const double* pose, double block_size,
                        double trunc, int32_t neighbor, int32_t* out_blocks, int32_t* out_gi,
                        uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
-                       int32_t* status, void* stream);
+                       int32_t* status, int32_t small_activate, void* stream);
 
 /* Delegate-backend insert commit (hashmap.py:369-387), after
  * ash_insert_claim + ash_insert_count: position p owns heap[top + p]; every

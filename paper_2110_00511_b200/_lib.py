@@ -62,10 +62,10 @@ _SIGNATURES = {
     "ash_copy_prefix2": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                                    c_void_p]),
     "ash_allocate_blocks": (c_int32, [_M, _M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                      c_void_p, c_void_p]),
+                                      c_void_p, c_int32, c_void_p]),
     "ash_allocate_frame": (c_int32, [_M, _M, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_double, c_double,
                                      c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                     c_void_p]),
+                                     c_int32, c_void_p]),
     "ash_insert_commit_delegate": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                              c_void_p, c_void_p]),
     "ash_heap_put_losers": (c_int32, [_M, c_void_p, c_int64, c_void_p]),

@@ -61,11 +61,14 @@ def allocate_blocks(global_map: HashMap, coords, threads: int = 1):
         gi, _ = global_map.activate(survivors)
         return gi, LocalBlockMap(survivors, gi, n, global_map.device)
     blocks, gi = _allocate_fused(
-        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, stream: call(
+        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, small, stream: call(
             "ash_allocate_blocks", global_map._ptr(), ctypes.byref(ws.struct), coords.data_ptr(), n,
             out.data_ptr(), gi_.data_ptr(), gm_.data_ptr(), si.data_ptr(), sm.data_ptr(), st.data_ptr(),
-            stream))
+            small, stream))
     return gi, LocalBlockMap(blocks, gi, n, global_map.device)
+
+
+_SMALL_ACTIVATE = 8192  # k_activate_small's batch limit (ash_map.cu kSmallMax)
 
 
 def _fused_ok(gm: HashMap) -> bool:
@@ -94,7 +97,9 @@ def _allocate_fused(gm: HashMap, n: int, launch):
         stream = _stream_handle(dev)
         for slots, probe in ws.attempts():
             ws.use(slots, probe)
-            launch(ws, out, gi, gmask, scratch_idx, scratch_mask, status, stream)
+            # one-block activate when the previous frame had few distinct blocks
+            small = 1 if 2 * ws.estimate <= _SMALL_ACTIVATE else 0
+            launch(ws, out, gi, gmask, scratch_idx, scratch_mask, status, small, stream)
             # the caller's result copies go in before the count is known
             # (sized from the previous call): no launch after the host read
             cap = min(n, max(256, 2 * ws.estimate))
@@ -294,10 +299,10 @@ def allocate_frame(global_map: HashMap, depth, intrinsics, pose, block_size: flo
         gi = global_map.activate(blocks).indices if blocks.shape[0] else blocks[:0, 0]
     else:
         blocks, gi = _allocate_fused(
-        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, stream: call(
+        global_map, n, lambda ws, out, gi_, gm_, si, sm, st, small, stream: call(
             "ash_allocate_frame", global_map._ptr(), ctypes.byref(ws.struct), d.data_ptr(), h, w, cam, pose_c,
                 float(block_size), float(trunc), nb, out.data_ptr(), gi_.data_ptr(), gm_.data_ptr(),
-                si.data_ptr(), sm.data_ptr(), st.data_ptr(), stream))
+                si.data_ptr(), sm.data_ptr(), st.data_ptr(), small, stream))
     if blocks.shape[0] == 0:
         return torch.zeros(0, dtype=torch.int32, device=dev), None
     per_pixel = n // (h * w)

@@ -44,6 +44,10 @@ constexpr uint32_t CLAIMER = 0x40000000u;
 constexpr uint32_t SLOT_MASK = 0x3FFFFFFFu;
 constexpr uint8_t DEMOTED = 2;  // out_mask scratch: this position lost the slot
 
+// probe bound of device-sized inserts: a table the batch overfills flags
+// ASH_FLAG_TABLE_FULL after this many buckets instead of scanning it whole
+constexpr uint32_t kDnProbe = 4096;
+
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kItems = 8;
@@ -2107,6 +2111,214 @@ __global__ void __launch_bounds__(kBlock) k_copy_prefix2(const uint32_t* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// one-block kernels for the per-frame sequence (ash_allocate_*): a frame has
+// ~2K new blocks, where every extra kernel boundary costs more than the work
+
+// zero up to four byte ranges in one launch (the sequence's memsets)
+struct ZeroRanges {
+  uint8_t* p[4];
+  int64_t bytes[4];
+};
+
+__global__ void __launch_bounds__(kBlock) k_zero_ranges(ZeroRanges z) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kBlock;
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(kBlock) + threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    uint8_t* p = z.p[r];
+    const int64_t nb = z.bytes[r];
+    if (!p || nb <= 0) continue;
+    const int64_t words = (reinterpret_cast<uintptr_t>(p) & 15) ? 0 : nb / 16;
+    for (int64_t i = i0; i < words; i += stride) reinterpret_cast<uint4*>(p)[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = words * 16 + i0; i < nb; i += stride) p[i] = 0;
+  }
+}
+
+// count + scan + word prefixes of a small dedup (n <= kSmallWords * 32) in
+// one block: winners per 32-position word, exclusive word prefixes, the
+// distinct count and the status gate (see k_dd_words)
+constexpr int kRankThreads = 1024;
+constexpr int kSmallWords = 4 * kRankThreads;  // 128K positions: at most 4 dependent loads per thread
+
+__global__ void __launch_bounds__(kRankThreads)
+    k_dd_rank_small(int64_t n, const uint32_t* __restrict__ cand, const uint32_t* __restrict__ dem,
+                    int32_t* __restrict__ word_pre, int32_t* ws_counters, int32_t* status, int64_t rows_max) {
+  __shared__ int32_t s_warp[kRankThreads / 32];
+  const int64_t n_words = (n + 31) / 32;
+  const int per = static_cast<int>((n_words + kRankThreads - 1) / kRankThreads);  // words per thread
+  const int64_t w0 = static_cast<int64_t>(threadIdx.x) * per;
+  int32_t cnt = 0;
+  for (int i = 0; i < per; ++i)
+    if (w0 + i < n_words) cnt += __popc(__ldg(cand + w0 + i) & ~__ldg(dem + w0 + i));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int32_t v = s_warp[lane];
+    int32_t vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, vi, o);
+      if (lane >= o) vi += y;
+    }
+    s_warp[lane] = vi - v;
+    if (lane == 31) {
+      const int32_t count = vi, flags = ws_counters[ASH_CTR_FLAGS];
+      ws_counters[ASH_CTR_COUNT] = count;
+      if (status) {
+        status[0] = (flags & (ASH_FLAG_TABLE_FULL | ASH_FLAG_RANGE)) || count > rows_max ? 0 : count;
+        status[1] = count;
+        status[2] = flags;
+      }
+    }
+  }
+  __syncthreads();
+  int32_t run = s_warp[warp] + incl - cnt;
+  for (int i = 0; i < per; ++i) {
+    if (w0 + i >= n_words) break;
+    word_pre[w0 + i] = run;
+    run += __popc(__ldg(cand + w0 + i) & ~__ldg(dem + w0 + i));
+  }
+}
+
+// Device-sized activate (association: found keys return their index) of at
+// most kSmallMax int3 keys in ONE block: claim, rank and commit separated by
+// block barriers instead of kernel boundaries, and each winner writes its
+// slot's final state itself (the batch's ranks are known inside the block:
+// no table sweep).  Same results as ash_insert_dn.  A longer batch is left
+// to the caller (status[0] = 0, nothing claimed); a batch that does not fit
+// the capacity commits nothing (ASH_FLAG_CAPACITY, out_idx keeps the claim
+// scratch for ash_insert_rollback).
+constexpr int kSmallThreads = 1024, kSmallItems = 8, kSmallMax = kSmallThreads * kSmallItems;
+
+__global__ void __launch_bounds__(kSmallThreads)
+    k_activate_small(Table t, const int32_t* __restrict__ keys, int64_t n_max, const int32_t* d_n,
+                     int32_t* __restrict__ out_idx, uint8_t* __restrict__ out_mask, const int32_t* __restrict__ heap,
+                     int64_t capacity, uint8_t* __restrict__ active, int32_t* __restrict__ key_buf, int32_t* counters,
+                     int32_t* status) {
+  constexpr int kW = kSmallThreads / 32;
+  __shared__ int32_t s_tiles[kSmallMax / kTile + 1];
+  __shared__ int32_t s_cnt[kSmallItems * kW];  // winners per (item, warp), then their exclusive prefixes
+  __shared__ int32_t s_tombs;
+  __shared__ uint32_t s_top;
+  __shared__ int s_fits;
+  const int64_t n = dev_len(n_max, d_n);
+  if (n > kSmallMax) {
+    if (threadIdx.x == 0 && status) status[0] = 0;
+    return;
+  }
+  if (threadIdx.x < kSmallMax / kTile + 1) s_tiles[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_tombs = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // position of item i: i * kSmallThreads + tid (every thread busy for
+  // short batches; ranks from per-(item, warp) ballots)
+#pragma unroll
+  for (int i = 0; i < kSmallItems; ++i) {
+    const int64_t p = i * kSmallThreads + threadIdx.x;
+    if (p < n) out_mask[p] = 0;
+  }
+  __syncthreads();
+  uint32_t res[kSmallItems];
+  int tombs = 0;
+#pragma unroll
+  for (int i = 0; i < kSmallItems; ++i) {
+    res[i] = 0;
+    const int64_t p = i * kSmallThreads + threadIdx.x;
+    if (p >= n) continue;
+    Key<3> k = load_key<3>(keys, p, 3);
+    bool tomb = false, cand = false;
+    res[i] = probe_claim<3>(t, k, hash_key<3>(k, 3), static_cast<uint32_t>(p), keys, out_mask, counters, s_tiles,
+                            &tomb, &cand);
+    tombs += tomb;
+  }
+  if (tombs) atomicAdd(&s_tombs, tombs);
+  __syncthreads();  // every claim and every DEMOTED mark is in place
+  uint32_t bal[kSmallItems];
+#pragma unroll
+  for (int i = 0; i < kSmallItems; ++i) {
+    const int64_t p = i * kSmallThreads + threadIdx.x;
+    const bool w = p < n && (res[i] & PEND) && !(out_mask[p] & DEMOTED);
+    bal[i] = __ballot_sync(0xFFFFFFFFu, w);
+    if (lane == 0) s_cnt[i * kW + warp] = __popc(bal[i]);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the kSmallItems x kW counts, (item, warp) order
+    constexpr int kPer = kSmallItems * kW / 32;
+    int32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      v[j] = s_cnt[lane * kPer + j];
+      sum += v[j];
+    }
+    int32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int32_t run = incl - sum;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      s_cnt[lane * kPer + j] = run;
+      run += v[j];
+    }
+    if (lane == 31) {
+      const int32_t total = incl;
+      const uint32_t top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP));
+      s_top = top;
+      s_fits = static_cast<int64_t>(top) + total <= capacity;
+      counters[ASH_CTR_WINNERS] = total;
+      counters[ASH_CTR_TOP_BASE] = static_cast<int32_t>(top);
+      if (s_fits) counters[ASH_CTR_TOP] = static_cast<int32_t>(top) + total;
+      else atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_CAPACITY);
+      if (s_tombs) atomicSub(&counters[ASH_CTR_TOMBS], s_tombs);
+      if (status) {
+        status[3] = ld_volatile_i32(counters + ASH_CTR_FLAGS);
+        status[4] = total;
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_fits) {  // nothing committed: leave the claim scratch for ash_insert_rollback
+#pragma unroll
+    for (int i = 0; i < kSmallItems; ++i) {
+      const int64_t p = i * kSmallThreads + threadIdx.x;
+      if (p < n) out_idx[p] = static_cast<int32_t>(res[i]);
+    }
+    return;
+  }
+  const uint32_t top = s_top;
+#pragma unroll
+  for (int i = 0; i < kSmallItems; ++i) {
+    const int64_t p = i * kSmallThreads + threadIdx.x;
+    if (p >= n) continue;
+    if ((bal[i] >> lane) & 1) {  // winner
+      const uint32_t rank = s_cnt[i * kW + warp] + __popc(bal[i] & lanemask_lt());
+      const int32_t idx = __ldg(heap + top + rank);
+      t.slots[res[i] & SLOT_MASK].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+      int32_t* dr = key_buf + static_cast<int64_t>(idx) * 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) dr[d] = __ldg(keys + p * 3 + d);
+      active[idx] = 1;
+      out_idx[p] = idx;
+      out_mask[p] = 1;
+    } else if (res[i] < PEND) {  // present before the batch
+      out_idx[p] = static_cast<int32_t>(res[i]);
+      out_mask[p] = 1;
+    } else {  // a repeat of a new key (or a key that found no slot)
+      out_idx[p] = -1;
+      out_mask[p] = 0;
+    }
+  }
+}
+
 // Every candidate of a frame in virtual-position order (parity tests and the
 // reference's _candidate_blocks API); valid = 0 where the pixel is invalid.
 __global__ void k_frame_candidates(FrameSrc src, int64_t n, int32_t* __restrict__ out, uint8_t* __restrict__ valid,
@@ -2292,11 +2504,11 @@ int launch_commit_bulk(const Table& t, const int32_t* keys, int64_t n, const Val
 template <typename Src>
 void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_coords, int64_t* out_sel,
                       int32_t* scratch_idx, uint8_t* scratch_mask, cudaStream_t s, int32_t* status = nullptr,
-                      int64_t status_rows_max = 0) {
+                      int64_t status_rows_max = 0, bool zeroed = false) {
   const int64_t words = (n + 31) / 32;
   uint32_t* cand = reinterpret_cast<uint32_t*>(scratch_mask);
   uint32_t* dem = cand + words;
-  cudaMemsetAsync(cand, 0, sizeof(uint32_t) * 2 * words, s);
+  if (!zeroed) cudaMemsetAsync(cand, 0, sizeof(uint32_t) * 2 * words, s);
   if constexpr (Src::kStaged) {  // aligned clouds: the specialised claim
     k_dd_claim_cloud<typename Src::Scalar, 128><<<grid_for(n, 128), 128, 0, s>>>(
         t.slots, t.n_buckets, t.max_scan, src.pts, static_cast<uint32_t>(n), src.cell, src.rcell, ws->counters,
@@ -2306,13 +2518,18 @@ void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, 
   }
   note_launch();
   const unsigned wg = grid_for(words, kBlock);
-  k_dd_count<<<wg, kBlock, 0, s>>>(n, cand, dem, ws->tile_counts);
-  note_launch();
-  k_tile_scan<<<1, kScanBlock, 0, s>>>(ws->tile_counts, wg, ws->counters, -1, ASH_CTR_COUNT, nullptr, nullptr);
-  note_launch();
-  k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts, ws->counters, status,
-                                   status_rows_max);
-  note_launch();
+  if (words <= kSmallWords) {  // small batches: one block instead of three kernels
+    k_dd_rank_small<<<1, kRankThreads, 0, s>>>(n, cand, dem, scratch_idx, ws->counters, status, status_rows_max);
+    note_launch();
+  } else {
+    k_dd_count<<<wg, kBlock, 0, s>>>(n, cand, dem, ws->tile_counts);
+    note_launch();
+    k_tile_scan<<<1, kScanBlock, 0, s>>>(ws->tile_counts, wg, ws->counters, -1, ASH_CTR_COUNT, nullptr, nullptr);
+    note_launch();
+    k_dd_words<<<wg, kBlock, 0, s>>>(n, cand, dem, scratch_idx, ws->tile_counts, ws->counters, status,
+                                     status_rows_max);
+    note_launch();
+  }
   k_dd_emit<<<grid_for(t.n_buckets, kBlock), kBlock, 0, s>>>(t.slots, t.n_buckets, cand, dem, scratch_idx, out_coords,
                                                               out_sel);
   note_launch();
@@ -2388,12 +2605,12 @@ void key_put(std::vector<uint8_t>& k, const T& v) {
 template <typename Src>
 static int allocate_sequence(ash_map_t* global, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_blocks,
                              int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
-                             int32_t* status, cudaStream_t s);
+                             int32_t* status, bool small, cudaStream_t s);
 
 template <typename Src>
 static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_blocks,
                           int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
-                          int32_t* status, cudaStream_t s) {
+                          int32_t* status, bool small, cudaStream_t s) {
   if (int rc = check_map(global)) return rc;
   if (global->arity != 3) return fail(ASH_ERR_INVALID, "block coordinates need key arity 3");
   if (ws->n_slots < 64 || (ws->n_slots & 1)) return fail(ASH_ERR_INVALID, "workspace table too small");
@@ -2402,7 +2619,8 @@ static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int6
   if (!out_blocks || !out_gi || !out_gmask || !scratch_idx || !scratch_mask || !status)
     return fail(ASH_ERR_INVALID, "null output pointer");
   auto body = [&](cudaStream_t st) -> int {
-    return allocate_sequence(global, ws, src, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask, status, st);
+    return allocate_sequence(global, ws, src, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask, status,
+                             small, st);
   };
   static thread_local std::vector<GraphEntry> cache;
   static thread_local uint64_t tick = 0;
@@ -2419,6 +2637,7 @@ static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int6
   key_put(key, g_stream_hints);
   key_put(key, g_commit_bulk);
   key_put(key, g_sweep_div);
+  key_put(key, small);
   key_put(sb, src);
   ++tick;
   GraphEntry* e = nullptr;
@@ -2501,12 +2720,32 @@ static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int6
 template <typename Src>
 static int allocate_sequence(ash_map_t* global, ash_map_t* ws, const Src& src, int64_t n, int32_t* out_blocks,
                              int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
-                             int32_t* status, cudaStream_t s) {
-  cudaMemsetAsync(ws->counters, 0, sizeof(int32_t) * ASH_N_COUNTERS, s);
+                             int32_t* status, bool small, cudaStream_t s) {
+  // one kernel zeroes the workspace counters, the dedup bitmaps and the
+  // global flags (three memset nodes otherwise)
+  const int64_t words = (n + 31) / 32;
+  ZeroRanges z;
+  memset(&z, 0, sizeof(z));
+  z.p[0] = reinterpret_cast<uint8_t*>(ws->counters), z.bytes[0] = sizeof(int32_t) * ASH_N_COUNTERS;
+  z.p[1] = scratch_mask, z.bytes[1] = static_cast<int64_t>(sizeof(uint32_t)) * 2 * words;
+  z.p[2] = reinterpret_cast<uint8_t*>(global->counters + ASH_CTR_FLAGS), z.bytes[2] = sizeof(int32_t);
+  const unsigned zg = grid_for(z.bytes[1] / 16 + 1, kBlock), zc = static_cast<unsigned>(device_sms()) * 4;
+  k_zero_ranges<<<zg < zc ? zg : zc, kBlock, 0, s>>>(z);
+  note_launch();
   // at most capacity new blocks can commit: more distinct rows than that
   // skip the device activate (status[0] = 0) and take the host path (growth)
   const int64_t cap_rows = n < global->capacity ? n : global->capacity;
-  run_dedup_select(make_table(ws), ws, src, n, out_blocks, nullptr, scratch_idx, scratch_mask, s, status, cap_rows);
+  run_dedup_select(make_table(ws), ws, src, n, out_blocks, nullptr, scratch_idx, scratch_mask, s, status, cap_rows,
+                   true);
+  if (small) {  // the activate in one block (a frame's few new blocks)
+    ash_map_t b = *global;
+    if (b.max_probe == 0 || b.max_probe > kDnProbe) b.max_probe = kDnProbe;
+    k_activate_small<<<1, kSmallThreads, 0, s>>>(make_table(&b), out_blocks, cap_rows, status, out_gi, out_gmask,
+                                                 global->heap, global->capacity, global->active, global->key_buf,
+                                                 global->counters, status);
+    note_launch();
+    return check_launch("ash_allocate_blocks");
+  }
   if (int rc = insert_dn_impl(global, out_blocks, cap_rows, status, nullptr, 1, out_gi, out_gmask, s, status, true))
     return rc;
   return check_launch("ash_allocate_blocks");
@@ -2779,9 +3018,6 @@ int ash_insert_lazy(ash_map_t* m, const int32_t* keys, int64_t n, const void* co
   return ash_insert_commit_lazy(m, keys, n, values, association, out_idx, out_mask, stream);
 }
 
-// probe bound of device-sized inserts: a table the batch overfills flags
-// ASH_FLAG_TABLE_FULL after this many buckets instead of scanning it whole
-constexpr uint32_t kDnProbe = 4096;
 
 int ash_insert_dn(ash_map_t* m, const int32_t* keys, int64_t n_max, const int32_t* d_n, const void* const* values,
                   int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream) {
@@ -2955,26 +3191,26 @@ int ash_unique_rows(ash_map_t* ws, const int32_t* keys, int64_t n, int32_t* out_
 
 int ash_allocate_blocks(ash_map_t* global, ash_map_t* ws, const int32_t* coords, int64_t n, int32_t* out_blocks,
                         int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx, uint8_t* scratch_mask,
-                        int32_t* status, void* stream) {
+                        int32_t* status, int32_t small_activate, void* stream) {
   if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return fail(ASH_ERR_INVALID, "empty candidate batch");
   if (!coords) return fail(ASH_ERR_INVALID, "null batch pointer");
   return allocate_fused(global, ws, RowSrc{coords}, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask,
-                        status, as_stream(stream));
+                        status, small_activate != 0, as_stream(stream));
 }
 
 int ash_allocate_frame(ash_map_t* global, ash_map_t* ws, const double* depth, int64_t height, int64_t width,
                        const double* cam, const double* pose, double block_size, double trunc, int32_t neighbor,
                        int32_t* out_blocks, int32_t* out_gi, uint8_t* out_gmask, int32_t* scratch_idx,
-                       uint8_t* scratch_mask, int32_t* status, void* stream) {
+                       uint8_t* scratch_mask, int32_t* status, int32_t small_activate, void* stream) {
   if (!ws || !ws->slots || !ws->counters) return fail(ASH_ERR_INVALID, "null workspace");
   FrameSrc f;
   int64_t n = 0;
   if (int rc = make_frame_src(&f, depth, height, width, cam, pose, block_size, trunc, neighbor, &n)) return rc;
   if (n == 0) return fail(ASH_ERR_INVALID, "empty frame");
   return allocate_fused(global, ws, f, n, out_blocks, out_gi, out_gmask, scratch_idx, scratch_mask, status,
-                        as_stream(stream));
+                        small_activate != 0, as_stream(stream));
 }
 
 int ash_copy_prefix2(const void* src0, void* dst0, int64_t row_bytes0, const void* src1, void* dst1,

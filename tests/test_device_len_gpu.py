@@ -176,3 +176,23 @@ def test_graph_replay_alternating_sequences(ash):
     assert gm.size == og.size
     G.bytes_eq(gm.key_buffer, og.key_buffer, "keys")
     gm.validate()
+
+
+def test_one_block_activate_refuses_long_batches(ash):
+    """The fused sequence picks the one-block activate from the previous
+    call's count; a batch with more distinct blocks than it takes (8192) is
+    left untouched on the device and activated on the host path, exactly."""
+    from oracle import ash_oracle as O
+    from paper_2110_00511_b200.blocks import unique_rows
+    rng = np.random.default_rng(8)
+    unique_rows(torch.from_numpy(rng.integers(0, 3, size=(10_000, 3)).astype(np.int32)).cuda())  # estimate 27
+    gm = ash.HashMap(100_000, 3, device="cuda")
+    og = O.OracleMap(100_000, 3)
+    for size, span in ((30_000, 40), (30_000, 5), (200_000, 60)):
+        coords = rng.integers(-span, span, size=(size, 3)).astype(np.int32)
+        gi, _ = ash.allocate_blocks(gm, coords)
+        gi_ref, _, _, _ = O.allocate_blocks_map_calls(og, coords)
+        G.eq(gi, gi_ref, f"{size}/{span}")
+    assert gm.size == og.size
+    G.eq(gm.active_indices(), og.active_indices(), "active")
+    gm.validate()
