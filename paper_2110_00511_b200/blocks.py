@@ -5,6 +5,7 @@ survivors are activated in the persistent global map, and each local entry
 stores its block's global buffer index."""
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -49,12 +50,13 @@ def allocate_blocks(global_map: HashMap, coords, threads: int = 1):
     a single host read (libash ``ash_allocate_blocks``); the local map —
     needed only by frame-scoped queries (tsdf/raycast.py:32-35) — is built on
     first use with the reference's indices (``LocalBlockMap``)."""
-    coords = global_map._check_keys(coords)
+    if not (isinstance(coords, torch.Tensor) and coords.dtype == torch.int32 and coords.dim() == 2
+            and coords.shape[1] == 3 and coords.device == global_map.device and coords.is_contiguous()):
+        coords = global_map._check_keys(coords).contiguous()  # (a device int3 batch needs no checks)
     if coords.shape[0] == 0:
         return torch.zeros(0, dtype=torch.int32, device=global_map.device), None
     if global_map.key_arity != 3:
         raise ValueError("block coordinates must have key arity 3")
-    coords = coords.contiguous()
     n = coords.shape[0]
     if not _fused_ok(global_map):  # delegate semantics: the host-planned activate
         survivors = unique_rows(coords)
@@ -84,7 +86,9 @@ def _allocate_fused(gm: HashMap, n: int, launch):
     from .geometry import _VoxelWorkspace
     dev = gm.device
     ws = _VoxelWorkspace.get(dev)
-    with _VoxelWorkspace._lock, torch.cuda.device(dev), gm._guard.writing():
+    same_dev = dev.index == torch.cuda.current_device()
+    with _VoxelWorkspace._lock, (contextlib.nullcontext() if same_dev else torch.cuda.device(dev)), \
+            gm._guard.writing():
         gm._settle()
         ws.reserve(n)
         gm._ensure_scan(n)
@@ -103,8 +107,8 @@ def _allocate_fused(gm: HashMap, n: int, launch):
             # the caller's result copies go in before the count is known
             # (sized from the previous call): no launch after the host read
             cap = min(n, max(256, 2 * ws.estimate))
-            blocks_c = torch.empty((cap, 3), dtype=torch.int32, device=dev)
-            gi_c = torch.empty(cap, dtype=torch.int32, device=dev)
+            res = torch.empty(4 * cap, dtype=torch.int32, device=dev)  # one allocation for both
+            blocks_c, gi_c = res[:3 * cap].view(cap, 3), res[3 * cap:]
             call("ash_copy_prefix2", out.data_ptr(), blocks_c.data_ptr(), 12, gi.data_ptr(), gi_c.data_ptr(), 4,
                  status.data_ptr() + 4, cap, stream)
             rows, count, wflags, gflags, winners = status.tolist()  # the one host read
