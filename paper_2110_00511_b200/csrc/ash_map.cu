@@ -2912,6 +2912,19 @@ int ash_settle(ash_map_t* m, void* stream) {
   return check_launch("ash_settle");
 }
 
+// The table sweep runs only when the winners reach sweep_min (decided on the
+// device), so a batch shorter than that cannot need it: no launch (the
+// fused allocate's status words then come from a one-thread kernel)
+static void sweep_or_status(const Table& t, const int32_t* out_idx, const int32_t* rank_words, const ash_map_t* m,
+                            int64_t sweep_min, int64_t n, cudaStream_t s, int32_t* status) {
+  if (n >= sweep_min) {
+    launch_sweep(t, out_idx, rank_words, m, sweep_min, s, status);
+  } else if (status) {
+    k_alloc_status<<<1, 1, 0, s>>>(nullptr, m->counters, status, 1);
+    note_launch();
+  }
+}
+
 static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values,
                          int32_t association, int32_t* out_idx, uint8_t* out_mask, void* stream, bool lazy,
                          const int32_t* d_n, int32_t* status, bool plain) {
@@ -2936,6 +2949,9 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
   // deferred: the table keeps PENDING|pos for this batch's winners until
   // ash_settle (finds resolve them through the rank words meanwhile)
   const bool defer = lazy && rank_words;
+  // a batch of a few tiles starts faster with one block per tile than with
+  // the TMA-staged persistent commit (configs[3]'s ~2K new blocks: 8 -> 7 us)
+  if (tiles_for(n) < 16) plain = true;
   if (!plain && pre && vw >= 0 && m->arity <= 3 && g_commit_bulk && aligned16(keys) && aligned16(out_idx) &&
       aligned16(out_mask) && aligned16(m->heap) && (vw == 0 || aligned16(va.src[0]))) {
     int rc = ASH_OK;
@@ -2955,7 +2971,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
     }
 #undef ASH_BULK
     if (rc) return rc;
-    if (!defer) launch_sweep(t, out_idx, rank_words, m, sweep_min, s, status);
+    if (!defer) sweep_or_status(t, out_idx, rank_words, m, sweep_min, n, s, status);
     return check_launch("ash_insert_commit");
   }
   int32_t* tile_pre = pre ? pre : m->tile_counts;
@@ -2973,7 +2989,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
     default: ASH_COMMIT(-1); break;
   }
 #undef ASH_COMMIT
-  if (!defer) launch_sweep(t, out_idx, rank_words, m, sweep_min, s, status);
+  if (!defer) sweep_or_status(t, out_idx, rank_words, m, sweep_min, n, s, status);
   return check_launch("ash_insert_commit");
 }
 
