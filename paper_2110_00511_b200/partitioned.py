@@ -594,7 +594,10 @@ def run_c5_partitioned(args, rank: int, world: int, dev, transport: str) -> dict
     indices are 0, 1, 2, ... in global batch order (checked through the hit
     count and the per-shard sizes); the finds hit exactly the present half."""
     from .workloads import c5_step_batches
-    total, batch = 400_000_000, 1 << 25
+    import os
+    # configs[4]: 400M keys in steps of 2^25; ASH_C5_TOTAL shrinks it for tests
+    total = int(os.environ.get("ASH_C5_TOTAL", 400_000_000))
+    batch = min(1 << 25, max(1 << 16, total // 8))
     cap = int(total / world * 1.05) + (1 << 20)
     recv = int(batch / world * 1.25) + (1 << 16)
     a2 = argparse_like(args, transport=transport)
@@ -641,9 +644,10 @@ def run_c5_partitioned(args, rank: int, world: int, dev, transport: str) -> dict
     assert pm.size == total == stored
     del pm
     torch.cuda.empty_cache()
-    return {"workload": "configs[4]: 400M-key hash-partitioned map built by the mixed stream (12 steps of 2^25 "
-                        "inserts + 2^25 finds, half present); every rank holds a contiguous 1/N slice of each "
-                        "global batch; time = max over ranks", "scaling": "strong",
+    return {"workload": f"configs[4]: {total:,}-key hash-partitioned map built by the mixed stream ({steps} steps "
+                        f"of {batch:,} inserts + {batch:,} finds, half present); every rank holds a contiguous 1/N "
+                        "slice of each global batch; time = max over ranks", "scaling": "strong",
+            "keys": total, "steps": steps,
             "routing": _routing_name(transport), "mops": round(ops / ms / 1e3, 2), "ms_total": round(ms, 2),
             "gpu_launches": launches,
             "parity": "every step: inserts all new (sum of masks = batch) with the indices from each owner "
@@ -671,7 +675,7 @@ def bench_c5(args, rank: int, world: int) -> None:
     dev = _bench_init()
     res = run_c5_partitioned(args, rank, world, dev, getattr(args, "transport", "peer"))
     if rank == 0:
-        steps = -(-400_000_000 // (1 << 25))
+        steps = res["steps"]
         print(json.dumps({
             "metric": "insert & find Mops/s (int3 keys)", "value": res["mops"], "unit": "Mops/s",
             "n_gpus": world, "steps": steps, "warmup": 0, "ms_per_step": round(res["ms_total"] / steps, 4),

@@ -73,3 +73,19 @@ def test_package_import_does_not_load_libash():
             "from pathlib import Path; print('libash.so' in Path('/proc/self/maps').read_text())")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
     assert out.stdout.strip() == "False", out.stderr
+
+
+def test_self_launch_runs_torchrun_on_localhost(monkeypatch):
+    """`python bench.py --gpus N` without torchrun launches its own N ranks
+    the way the driver does (torch.distributed.run, 127.0.0.1)."""
+    import subprocess
+    import sys
+    import bench
+    seen = {}
+    monkeypatch.setattr(subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    assert bench.self_launch(4) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "3"][-3:] and cmd[-5].endswith("bench.py")
