@@ -147,3 +147,25 @@ def test_unique_rows_and_workspace_overflow_retry(ash):
     G.eq(got, _first_occurrence_rows(big), "big after small (retried)")
     got = unique_rows(small)
     G.eq(got, _first_occurrence_rows(small.cpu().numpy()), "small again")
+
+
+def test_general_rotations_match_reference_digests(ash):
+    """General rotations against the reference itself: digests of
+    VoxelBlockGrid._candidate_blocks written by the reference in the build
+    container (oracle/make_rotation_golden.py), where numpy's OpenBLAS
+    evaluates the pose product as the kernel does (an FMA chain): bit-exact,
+    independent of the GPU box's own BLAS."""
+    import hashlib
+    import json
+    from pathlib import Path
+    from oracle import ash_oracle as O
+    g = json.loads((Path(__file__).parent / "golden" / "frame_rotation_sha.json").read_text())
+    cam = O.scaled_camera(320, 240)
+    block = g["voxel"] * g["block_resolution"]
+    for case in g["cases"]:
+        depth = O.plane_depth(cam, 1.2) if case["shape"] == "plane" else O.sphere_depth(cam)
+        pose = np.array(case["pose"])
+        got = np.ascontiguousarray(G.to_np(ash.frame_candidates(depth, cam, pose, block, g["trunc"],
+                                                                device="cuda")), dtype=np.int32)
+        assert len(got) == case["count"], case["quaternion"]
+        assert hashlib.sha256(got.tobytes()).hexdigest() == case["sha256"], case["quaternion"]
