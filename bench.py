@@ -583,6 +583,15 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
     ref, ref_kind, _ = load_reference() if with_cpu else (None, None, None)
     if with_cpu:
         c3["cpu_baseline"] = {**cpu_c3(ref), "kind": ref_kind}
+    # voxelize B = P + S + rho_new (K + S + 12 + 8), P = 24
+    # (float64 rows), rho_new = distinct / points; the workspace probes hit
+    # the L2 (an upper bound on DRAM bytes)
+    rho3 = int(coords.shape[0]) / 20e6
+    b3 = 24 + 32 + rho3 * (12 + 32 + 12 + 8)
+    bw = _peaks()[0]
+    c3["roofline"] = {"bytes_per_point": round(b3, 2), "achieved": round(b3 * 20e6 / (ms / 1e3) / 1e9, 1),
+                      "peak": bw, "unit": "GB/s", "frac": round(b3 * 20e6 / (ms / 1e3) / 1e9 / bw, 4),
+                      "bound": "issue / L2 latency (claim: 68% issue, 52% long-scoreboard, ncu r02y)"}
     out["c3_voxelize"] = c3
     cam = O.scaled_camera(640, 480)
     depth = O.plane_depth(cam, 1.0)
@@ -612,6 +621,13 @@ def run_other_configs(torch, dev, ash, flush, with_cpu: bool):
           "note": "includes the host syncs of the boolean-mask gathers in the reference call sequence"}
     if with_cpu:
         c4["cpu_baseline"] = {**cpu_c4(ref), "kind": ref_kind}
+    # activate B = K + 5 + S + rho_new (K + S) per candidate
+    rho4 = gm.size / len(frames[0]) / len(frames)  # new blocks per candidate over the frames
+    b4 = 12 + 5 + 32 + rho4 * (12 + 32)
+    c4["roofline"] = {"bytes_per_candidate": round(b4, 2),
+                      "achieved": round(b4 * len(frames[0]) / (ms / 1e3) / 1e9, 1), "peak": bw, "unit": "GB/s",
+                      "frac": round(b4 * len(frames[0]) / (ms / 1e3) / 1e9 / bw, 4),
+                      "bound": "L2 / launch latency (~2K hot blocks; ~10 kernels per frame in one CUDA graph)"}
     out["c4_allocate_blocks"] = c4
     # the same frames end to end from the depth image: fused candidate
     # generation + dedup on the device (§8(f) row 1), then the global activate
