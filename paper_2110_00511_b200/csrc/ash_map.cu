@@ -1959,6 +1959,31 @@ __global__ void __launch_bounds__(B, 2048 / B) k_dd_claim(Table t, Src src, int6
 // a narrow parameter list (claim 204 -> 182 us at configs[2] with the lean
 // probe).  Same semantics as k_dd_claim<CloudSrc<T>>.
 
+// the claim of one warp of points, FULL = all 32 lanes in the batch
+// (compile-time full masks: no runtime convergence checks on the warp ops)
+template <typename T, bool FULL>
+__device__ __forceinline__ void cloud_claim_warp(uint4* __restrict__ slots, uint32_t n_buckets, uint32_t max_scan,
+                                                 T x0, T x1, T x2, uint32_t p, uint32_t lane, unsigned live,
+                                                 double cell, double rcell, int32_t* counters,
+                                                 uint32_t* __restrict__ cand, uint32_t* __restrict__ dem) {
+  const unsigned lm = FULL ? 0xFFFFFFFFu : live;
+  bool bad = false;
+  const uint32_t k0 = static_cast<uint32_t>(quantize_fast<T>(x0, cell, rcell, &bad));
+  const uint32_t k1 = static_cast<uint32_t>(quantize_fast<T>(x1, cell, rcell, &bad));
+  const uint32_t k2 = static_cast<uint32_t>(quantize_fast<T>(x2, cell, rcell, &bad));
+  if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
+  // a point in the same voxel as the (valid) previous lane's skips the table
+  const unsigned vmask = __ballot_sync(lm, !bad);
+  const uint32_t u0 = __shfl_up_sync(lm, k0, 1), u1 = __shfl_up_sync(lm, k1, 1), u2 = __shfl_up_sync(lm, k2, 1);
+  const bool dup = lane > 0 && ((vmask >> (lane - 1)) & 1) && u0 == k0 && u1 == k1 && u2 == k2;
+  Key<3> k;
+  k.w[0] = k0, k.w[1] = k1, k.w[2] = k2;
+  const bool ev = !bad && !dup &&
+                  dd_probe_lean(slots, n_buckets, max_scan, k0, k1, k2, dd_hash(k), PEND | p, counters, dem);
+  const unsigned cb = __ballot_sync(lm, ev);
+  if (cb && lane == 0) atomicOr(&cand[p >> 5], cb);  // lane 0 is live: warps start at multiples of 32
+}
+
 template <typename T, int B = 128>
 __global__ void __launch_bounds__(B, 2048 / B)
     k_dd_claim_cloud(uint4* __restrict__ slots, uint32_t n_buckets, uint32_t max_scan, const T* __restrict__ pts,
@@ -1968,8 +1993,6 @@ __global__ void __launch_bounds__(B, 2048 / B)
   __shared__ uint4 stage[B / 32][kV];
   const uint32_t lane = threadIdx.x & 31, wb = threadIdx.x >> 5;
   const uint32_t base = blockIdx.x * B + wb * 32, p = base + lane;
-  uint32_t live = 0xFFFFFFFFu;
-  T x0, x1, x2;
   const uint64_t pol = stream_policy(1);
   if (base + 32 <= n) {
     const uint4* src = reinterpret_cast<const uint4*>(pts + 3 * static_cast<size_t>(base));
@@ -1977,32 +2000,18 @@ __global__ void __launch_bounds__(B, 2048 / B)
     for (int c = lane; c < kV; c += 32) stage[wb][c] = ld_stream_v4(src + c, pol);
     __syncwarp();
     const T* row = reinterpret_cast<const T*>(stage[wb]) + 3 * lane;
-    x0 = row[0], x1 = row[1], x2 = row[2];
-  } else {
-    if (base >= n) return;
-    live = __ballot_sync(0xFFFFFFFFu, p < n);
-    if (p >= n) return;
-    x0 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p), pol);
-    x1 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p) + 1, pol);
-    x2 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p) + 2, pol);
+    cloud_claim_warp<T, true>(slots, n_buckets, max_scan, row[0], row[1], row[2], p, lane, 0xFFFFFFFFu, cell, rcell,
+                              counters, cand, dem);
+    return;
   }
-  bool bad = false;
-  const uint32_t k0 = static_cast<uint32_t>(quantize_fast<T>(x0, cell, rcell, &bad));
-  const uint32_t k1 = static_cast<uint32_t>(quantize_fast<T>(x1, cell, rcell, &bad));
-  const uint32_t k2 = static_cast<uint32_t>(quantize_fast<T>(x2, cell, rcell, &bad));
-  if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
-  // a point in the same voxel as the (valid) previous lane's skips the table
-  const unsigned vmask = __ballot_sync(live, !bad);
-  const uint32_t u0 = __shfl_up_sync(live, k0, 1), u1 = __shfl_up_sync(live, k1, 1),
-                 u2 = __shfl_up_sync(live, k2, 1);
-  const bool dup = lane > 0 && ((vmask >> (lane - 1)) & 1) && u0 == k0 && u1 == k1 && u2 == k2;
-  Key<3> k;
-  k.w[0] = k0, k.w[1] = k1, k.w[2] = k2;
-  const bool ev = !bad && !dup &&
-                  dd_probe_lean(slots, n_buckets, max_scan, k0, k1, k2, dd_hash(k), PEND | p, counters, dem);
-  __syncwarp(live);
-  const unsigned cb = __ballot_sync(live, ev);
-  if (cb && lane == __ffs(live) - 1) atomicOr(&cand[p >> 5], cb);
+  if (base >= n) return;
+  const unsigned live = __ballot_sync(0xFFFFFFFFu, p < n);
+  if (p >= n) return;
+  const T x0 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p), pol);
+  const T x1 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p) + 1, pol);
+  const T x2 = ld_stream_t<T>(pts + 3 * static_cast<size_t>(p) + 2, pol);
+  cloud_claim_warp<T, false>(slots, n_buckets, max_scan, x0, x1, x2, p, lane, live, cell, rcell, counters, cand,
+                             dem);
 }
 
 // winners per 256 bitmap words (8192 positions: one k_dd_words block) ->
