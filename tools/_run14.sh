@@ -1,5 +1,5 @@
 set -u
 O=gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q > $O/r02zj_gputests.log 2>&1; echo "pytest rc=$?"; tail -3 $O/r02zj_gputests.log
-timeout 900 python bench.py > $O/r02zj_bench.json 2> $O/r02zj_bench.err; echo "bench rc=$?"; tail -3 $O/r02zj_bench.err
-timeout 900 python bench.py --impl reference > $O/r02zj_reference_arm.json 2> $O/r02zj_reference_arm.err; echo "ref rc=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/r02zo_gputests.log 2>&1; echo "pytest rc=$?"; tail -3 $O/r02zo_gputests.log
+timeout 900 python bench.py > $O/r02zo_bench.json 2> $O/r02zo_bench.err; echo "bench rc=$?"; tail -3 $O/r02zo_bench.err
+timeout 900 python bench.py --impl reference > $O/r02zo_reference_arm.json 2> $O/r02zo_reference_arm.err; echo "ref rc=$?"
