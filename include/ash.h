@@ -50,6 +50,7 @@ extern "C" {
 #define ASH_FLAG_TABLE_FULL 1  /* a claim probe wrapped the table (or hit max_probe) */
 #define ASH_FLAG_RANGE 2       /* quantized coordinate outside int32 */
 #define ASH_FLAG_CAPACITY 4    /* a device-sized insert did not fit: nothing committed */
+#define ASH_FLAG_SPEC 8        /* state, not an error: the last claim used top + pos pending states */
 
 /*
  * Map state.  Table slots are 16 bytes {w0, w1, w2, state}: the first three

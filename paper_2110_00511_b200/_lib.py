@@ -16,7 +16,7 @@ MAX_VALUE_BUFFERS = 8
 CTR_TOP, CTR_TOMBS, CTR_WINNERS, CTR_ERASED, CTR_FLAGS, CTR_COUNT, CTR_TOP_BASE = 0, 1, 2, 3, 4, 5, 6
 CTR_HEAP_DIRTY = 7
 N_COUNTERS = 8
-FLAG_TABLE_FULL, FLAG_RANGE, FLAG_CAPACITY = 1, 2, 4
+FLAG_TABLE_FULL, FLAG_RANGE, FLAG_CAPACITY, FLAG_SPEC = 1, 2, 4, 8
 TILE = 2048  # positions per scan tile (csrc kTile)
 
 

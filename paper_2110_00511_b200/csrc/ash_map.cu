@@ -380,10 +380,16 @@ struct Table {
   uint32_t max_scan;     // claim probe limit in buckets (n_buckets, or ash_map_t.max_probe)
   const int32_t* key_buf;
   int arity;
+  // speculative claim (set by k_claim for its batch): pending states are
+  // spec_base + position instead of PENDING | position (see k_claim)
+  uint32_t spec;
+  uint32_t spec_base;
 };
 
 Table make_table(const ash_map_t* m) {
   Table t;
+  t.spec = 0;
+  t.spec_base = 0;
   t.slots = static_cast<uint4*>(m->slots);
   t.n_buckets = static_cast<uint32_t>(m->n_slots / 2);
   t.n_slots = static_cast<uint32_t>(m->n_slots);
@@ -500,7 +506,8 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
                                                 uint32_t j, const int32_t* batch, uint8_t* mask,
                                                 int32_t* counters, int32_t* tile_cnt, bool* claimed_tomb,
                                                 bool* candidate) {
-  const uint32_t me = PEND | j;
+  const uint32_t me = t.spec ? t.spec_base + j : PEND | j;
+  const uint32_t committed_lim = t.spec ? t.spec_base : PEND;  // states below: committed indices
   uint32_t b = home_bucket(h, t.n_buckets);
   int first = 0;
   uint32_t free_slot = EMPTY;
@@ -521,7 +528,7 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
         }
         if (st == EMPTY) goto claim;
       } else if (slot_matches<A>(w + 4 * s, st, k, t, batch)) {
-        if (st < PEND) return st;  // already present
+        if (st < committed_lim) return st;  // already present
         if (st < me) {  // a lower position already holds it: certain loser, no atomic
           mask[j] = DEMOTED;
           return PEND | slot;
@@ -530,8 +537,9 @@ __device__ __forceinline__ uint32_t probe_claim(const Table& t, const Key<A>& k,
         if (old < me) {
           mask[j] = DEMOTED;  // a lower position holds the key
         } else {
-          mask[old & ~PEND] = DEMOTED;  // we displaced a higher position
-          atomicSub(&tile_cnt[(old & ~PEND) / kTile], 1);
+          const uint32_t q = t.spec ? old - t.spec_base : old & ~PEND;
+          mask[q] = DEMOTED;  // we displaced a higher position
+          atomicSub(&tile_cnt[q / kTile], 1);
           *candidate = true;
         }
         return PEND | slot;
@@ -648,7 +656,8 @@ __device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint3
                                           const uint32_t (&w)[8], const int32_t* batch, uint8_t* mask,
                                           int32_t* tile_cnt, uint32_t* res, bool* candidate, uint32_t* cas_slot,
                                           uint4* cas_expect) {
-  const uint32_t me = PEND | j;
+  const uint32_t me = t.spec ? t.spec_base + j : PEND | j;
+  const uint32_t committed_lim = t.spec ? t.spec_base : PEND;  // states below: committed indices
   const uint32_t b = home_bucket(h, t.n_buckets);
   bool have_free = false;
 #pragma unroll
@@ -664,7 +673,7 @@ __device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint3
     } else if (slot_matches<A>(w + 4 * s, st, k, t, batch)) {
       const uint32_t slot = 2 * b + s;
       *res = PEND | slot;
-      if (st < PEND) {
+      if (st < committed_lim) {
         *res = st;
       } else if (st < me) {
         mask[j] = DEMOTED;
@@ -673,8 +682,9 @@ __device__ __forceinline__ int claim_fast(const Table& t, const Key<A>& k, uint3
         if (old < me) {
           mask[j] = DEMOTED;
         } else {
-          mask[old & ~PEND] = DEMOTED;
-          atomicSub(&tile_cnt[(old & ~PEND) / kTile], 1);
+          const uint32_t q = t.spec ? old - t.spec_base : old & ~PEND;
+          mask[q] = DEMOTED;
+          atomicSub(&tile_cnt[q / kTile], 1);
           *candidate = true;
         }
       }
@@ -760,7 +770,8 @@ __device__ __forceinline__ void claim_chunk(const Table& t, const int32_t* __res
     cas_ok[r] = false;
     if (state[r] == kFastCas) {
       const uint32_t j = static_cast<uint32_t>(blk + r * B + threadIdx.x);
-      cas_ok[r] = cas128(t.slots + cas_slot[r], cas_expect[r], slot_value<A>(k[r], PEND | j));
+      cas_ok[r] = cas128(t.slots + cas_slot[r], cas_expect[r],
+                         slot_value<A>(k[r], t.spec ? t.spec_base + j : PEND | j));
     }
   }
   // stage 4: resolve; anything unusual takes the full probe loop
@@ -801,13 +812,37 @@ __device__ __forceinline__ void claim_chunk(const Table& t, const int32_t* __res
   if (lane == 0 && tomb_total) atomicSub(&counters[ASH_CTR_TOMBS], tomb_total);
 }
 
-// d_n: a device-sized batch (ash_insert_dn): blocks past min(n, *d_n) exit
+// d_n: a device-sized batch (ash_insert_dn): blocks past min(n, *d_n) exit.
+//
+// Speculative pending states (allow_spec, arity <= 3): while the heap is the
+// identity above its top T0 (no frees there), every committed index is below
+// T0, so a pending claim can carry T0 + position instead of PENDING |
+// position -- the same order for the atomicMin -- and when every position of
+// the batch wins (all keys new and distinct: configs[4]'s insert stream) that
+// state already IS the final index T0 + rank: the commit writes no slot state
+// and the table sweep is skipped.  ASH_FLAG_SPEC tells the batch's commit and
+// sweep which encoding the table holds.
 template <int A, int B = kBlock>
 __global__ void __launch_bounds__(B) k_claim(Table t, const int32_t* __restrict__ keys, int64_t n,
                                              int32_t* __restrict__ tmp, uint8_t* __restrict__ mask,
-                                             int32_t* counters, int32_t* tile_cnt, const int32_t* d_n) {
+                                             int32_t* counters, int32_t* tile_cnt, const int32_t* d_n,
+                                             int allow_spec) {
   __shared__ uint32_t stage[kClaimRounds][B * 3];
   n = dev_len(n, d_n);
+  if (A != 0 && allow_spec) {
+    // read-only path: the per-SM cache serves the block's warps (a volatile
+    // load per warp queues ~10^5 requests on one L2 slice: +70 us at rho 0.1)
+    const uint32_t top = static_cast<uint32_t>(__ldg(counters + ASH_CTR_TOP));
+    if (__ldg(counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(top) &&
+        static_cast<uint64_t>(top) + static_cast<uint64_t>(n) < PEND) {
+      t.spec = 1;
+      t.spec_base = top;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the only writer of the bit
+    if (t.spec) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_SPEC);
+    else atomicAnd(&counters[ASH_CTR_FLAGS], ~ASH_FLAG_SPEC);
+  }
   const int64_t blk = blockIdx.x * static_cast<int64_t>(B * kClaimRounds);
   if (blk >= n) return;
   claim_chunk<A, B>(t, keys, n, blk, tmp, mask, counters, tile_cnt, stage);
@@ -1070,7 +1105,10 @@ __global__ void __launch_bounds__(kBlock)
   const uint64_t pol = stream_policy(t.hints);
   // large batches leave the slot states to k_commit_sweep (see there); the
   // winners' indices in tmp must then stay L2-resident for it
-  const bool defer = ld_volatile_i32(counters + ASH_CTR_WINNERS) >= sweep_min;
+  const int32_t winners = ld_volatile_i32(counters + ASH_CTR_WINNERS);
+  const bool defer = winners >= sweep_min;
+  // a speculative claim where every position won: the states are final
+  const bool states_final = (ld_volatile_i32(counters + ASH_CTR_FLAGS) & ASH_FLAG_SPEC) && winners == n;
   const uint64_t tpol = defer && !rank_words ? stream_policy(0) : pol;
   int32_t v[kItems];
   uint8_t mk[kItems];
@@ -1120,7 +1158,7 @@ __global__ void __launch_bounds__(kBlock)
     if (win[it]) {
       const int32_t idx = hidx[it];
       const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
-      if (!defer) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+      if (!defer && !states_final) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
       int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
@@ -1272,7 +1310,10 @@ __global__ void __launch_bounds__(kCommitThreads)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = stream_policy(t.hints);
-  const bool defer = ld_volatile_i32(counters + ASH_CTR_WINNERS) >= sweep_min;  // see k_commit_sweep
+  const int32_t winners = ld_volatile_i32(counters + ASH_CTR_WINNERS);
+  const bool defer = winners >= sweep_min;  // see k_commit_sweep
+  // a speculative claim where every position won: the states are final
+  const bool states_final = (ld_volatile_i32(counters + ASH_CTR_FLAGS) & ASH_FLAG_SPEC) && winners == n;
   const uint64_t tpol = defer && !rank_words ? stream_policy(0) : pol;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kCommitStages; ++s) {
@@ -1388,7 +1429,7 @@ __global__ void __launch_bounds__(kCommitThreads)
         const uint32_t rank = sm.pre[it * kCW + warp] + __popc(bal[it] & lanemask_lt());
         const int32_t idx = s_heap[heap_off + rank];
         const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
-        if (!defer) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
+        if (!defer && !states_final) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
         int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
 #pragma unroll
         for (int d = 0; d < A; ++d) st_stream(dr + d, s_keys[r * A + d], pol);
@@ -1436,18 +1477,28 @@ __global__ void __launch_bounds__(kCommitThreads)
 // touched the heap above top), the rank from the per-32-position winner bits
 // and prefixes the commit wrote to rank_words (2.5 MB at 10M positions, L2
 // resident); without rank_words, the index the commit wrote to tmp[pos].
+// After a speculative claim the pending states are top + pos (see k_claim).
+// mode: 0 = an insert's eager sweep; 1 = after a deferred commit: runs only
+// for a speculative claim (its states cannot be left for the finds to
+// resolve); 2 = ash_settle: runs only for PENDING | pos states.
 template <int U>  // buckets per thread per round; all loads of a round issued together
 __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t* __restrict__ tmp,
                                                          const int32_t* __restrict__ rank_words,
                                                          const int32_t* __restrict__ heap,
                                                          const int32_t* counters, int64_t sweep_min,
-                                                         int32_t* status) {
+                                                         int32_t* status, int64_t n, const int32_t* d_n,
+                                                         int mode) {
   if (status && blockIdx.x == 0 && threadIdx.x == 0) {  // ash_allocate_*: [3] flags, [4] new keys
     status[3] = ld_volatile_i32(counters + ASH_CTR_FLAGS);
     status[4] = ld_volatile_i32(counters + ASH_CTR_WINNERS);
   }
-  if (ld_volatile_i32(counters + ASH_CTR_WINNERS) < sweep_min) return;
-  if (ld_volatile_i32(counters + ASH_CTR_FLAGS) & ASH_FLAG_CAPACITY) return;  // nothing was committed
+  const int32_t winners = ld_volatile_i32(counters + ASH_CTR_WINNERS);
+  const int32_t flags = ld_volatile_i32(counters + ASH_CTR_FLAGS);
+  if (winners < sweep_min) return;
+  if (flags & ASH_FLAG_CAPACITY) return;  // nothing was committed
+  const bool spec = flags & ASH_FLAG_SPEC;
+  if ((mode == 1 && !spec) || (mode == 2 && spec)) return;
+  if (spec && winners == dev_len(n, d_n)) return;  // every position won: the states are final
   const uint32_t stride = gridDim.x * kBlock;
   const uint32_t top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
   // fresh heap region (no frees at or above top): index = top + rank
@@ -1466,8 +1517,10 @@ __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t*
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t st = w[u][4 * s + 3];
-        if ((st & 0xC0000000u) != PEND) continue;  // not PENDING (EMPTY / TOMB have both top bits)
-        const uint32_t j = st & ~PEND;
+        // pending?  EMPTY / TOMB have both top bits; committed indices are
+        // below top after a speculative claim
+        if (spec ? (st < top || st >= TOMB) : ((st & 0xC0000000u) != PEND)) continue;
+        const uint32_t j = spec ? st - top : st & ~PEND;
         if (rank_words) {
           const uint2 rw = __ldg(reinterpret_cast<const uint2*>(rank_words) + (j >> 5));
           idx[u][s] = rw.y + __popc(rw.x & ((1u << (j & 31)) - 1u));  // rank
@@ -1480,7 +1533,7 @@ __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t*
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t st = w[u][4 * s + 3];
-        if ((st & 0xC0000000u) != PEND) continue;
+        if (spec ? (st < top || st >= TOMB) : ((st & 0xC0000000u) != PEND)) continue;
         uint32_t v = idx[u][s];
         if (rank_words) v = ident ? top + v : static_cast<uint32_t>(__ldg(heap + top + v));
         t.slots[2 * static_cast<size_t>(b0 + u * stride) + s].w = v;
@@ -2455,7 +2508,8 @@ int device_sms() {
 __global__ void k_alloc_status(const int32_t* ws_counters, const int32_t* g_counters, int32_t* status, int phase);
 
 void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words, const ash_map_t* m, int64_t sweep_min,
-                  cudaStream_t s, int32_t* status = nullptr) {
+                  cudaStream_t s, int32_t* status = nullptr, int64_t n = 0, const int32_t* d_n = nullptr,
+                  int mode = 0) {
   if (sweep_min == INT64_MAX) {
     if (status) {
       k_alloc_status<<<1, 1, 0, s>>>(nullptr, m->counters, status, 1);
@@ -2470,7 +2524,7 @@ void launch_sweep(const Table& t, const int32_t* tmp, const int32_t* rank_words,
   // (bench A/B in r01l: the DRAM read/write mix, not load latency, bounds it)
   // 8 CTAs per SM (4 and 16 measured 5% slower, r01m)
   k_commit_sweep<1><<<g < cap ? g : cap, kBlock, 0, s>>>(t, tmp, rank_words, m->heap, m->counters, sweep_min,
-                                                         status);
+                                                         status, n, d_n, mode);
   note_launch();
 }
 
@@ -2857,7 +2911,7 @@ int ash_find_lattice(ash_map_t* m, const int32_t* coords, int64_t n, int32_t r, 
 }
 
 static int claim_impl(ash_map_t* m, const int32_t* keys, int64_t n, const int32_t* d_n, int32_t* out_idx,
-                      uint8_t* out_mask, void* stream) {
+                      uint8_t* out_mask, void* stream, int allow_spec = 1) {
   if (int rc = check_map(m)) return rc;
   if (int rc = check_batch(n)) return rc;
   if (n == 0) return ASH_OK;
@@ -2866,10 +2920,11 @@ static int claim_impl(ash_map_t* m, const int32_t* keys, int64_t n, const int32_
   cudaStream_t s = as_stream(stream);
   if (int rc = check_tiles(m, n)) return rc;
   cudaMemsetAsync(out_mask, 0, n, s);
+  if (const char* e = getenv("ASH_SPEC")) allow_spec = allow_spec && e[0] != '0';  // A/B switch
   // 128-thread blocks: 0.302 ms against 0.310 at 256 and 0.330 at 512 (C2,
   // r01m A/B; 64 ties with 128): finer block turnover over the ~66 waves
   ASH_DISPATCH_ARITY(m->arity, (k_claim<A, kClaimBlock><<<grid_for(n, kClaimBlock * kClaimRounds), kClaimBlock, 0, s>>>(
-                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts, d_n)));
+                                   t, keys, n, out_idx, out_mask, m->counters, m->tile_counts, d_n, allow_spec)));
   return check_launch("ash_insert_claim");
 }
 
@@ -2917,7 +2972,7 @@ int ash_settle(ash_map_t* m, void* stream) {
   if (!m->rank_words) return ASH_OK;
   Table t = make_table(m);
   const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
-  launch_sweep(t, nullptr, m->rank_words, m, sweep_min, as_stream(stream));
+  launch_sweep(t, nullptr, m->rank_words, m, sweep_min, as_stream(stream), nullptr, 0, nullptr, 2);
   return check_launch("ash_settle");
 }
 
@@ -2925,9 +2980,10 @@ int ash_settle(ash_map_t* m, void* stream) {
 // device), so a batch shorter than that cannot need it: no launch (the
 // fused allocate's status words then come from a one-thread kernel)
 static void sweep_or_status(const Table& t, const int32_t* out_idx, const int32_t* rank_words, const ash_map_t* m,
+                            const int32_t* d_n, int mode,
                             int64_t sweep_min, int64_t n, cudaStream_t s, int32_t* status) {
   if (n >= sweep_min) {
-    launch_sweep(t, out_idx, rank_words, m, sweep_min, s, status);
+    launch_sweep(t, out_idx, rank_words, m, sweep_min, s, status, n, d_n, mode);
   } else if (status) {
     k_alloc_status<<<1, 1, 0, s>>>(nullptr, m->counters, status, 1);
     note_launch();
@@ -2956,7 +3012,8 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
   const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
   int32_t* rank_words = (m->rank_words && m->rank_words_len >= 2 * ((n + 31) / 32)) ? m->rank_words : nullptr;
   // deferred: the table keeps PENDING|pos for this batch's winners until
-  // ash_settle (finds resolve them through the rank words meanwhile)
+  // ash_settle (finds resolve them through the rank words meanwhile); the
+  // sweep then runs only if the claim was speculative (mode 1, k_commit_sweep)
   const bool defer = lazy && rank_words;
   // a batch of a few tiles starts faster with one block per tile than with
   // the TMA-staged persistent commit (configs[3]'s ~2K new blocks: 8 -> 7 us)
@@ -2980,7 +3037,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
     }
 #undef ASH_BULK
     if (rc) return rc;
-    if (!defer) sweep_or_status(t, out_idx, rank_words, m, sweep_min, n, s, status);
+    sweep_or_status(t, out_idx, rank_words, m, d_n, defer ? 1 : 0, sweep_min, n, s, status);
     return check_launch("ash_insert_commit");
   }
   int32_t* tile_pre = pre ? pre : m->tile_counts;
@@ -2998,7 +3055,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
     default: ASH_COMMIT(-1); break;
   }
 #undef ASH_COMMIT
-  if (!defer) sweep_or_status(t, out_idx, rank_words, m, sweep_min, n, s, status);
+  sweep_or_status(t, out_idx, rank_words, m, d_n, defer ? 1 : 0, sweep_min, n, s, status);
   return check_launch("ash_insert_commit");
 }
 
@@ -3038,7 +3095,9 @@ int ash_insert(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* 
 
 int ash_insert_lazy(ash_map_t* m, const int32_t* keys, int64_t n, const void* const* values, int32_t association,
                     int32_t* out_idx, uint8_t* out_mask, void* stream) {
-  if (int rc = ash_insert_claim(m, keys, n, out_idx, out_mask, stream)) return rc;
+  // PENDING | pos states, which the finds resolve until ash_settle (a
+  // speculative claim would have to be swept at once)
+  if (int rc = claim_impl(m, keys, n, nullptr, out_idx, out_mask, stream, 0)) return rc;
   if (int rc = ash_insert_count(m, n, out_idx, out_mask, stream)) return rc;
   return ash_insert_commit_lazy(m, keys, n, values, association, out_idx, out_mask, stream);
 }
