@@ -395,6 +395,18 @@ int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t ra
 int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world,
                           int32_t rank, const int64_t* count_matrix, const int32_t* recv_status,
                           const void* const* peer_ret, int32_t* out, uint8_t* out_mask, void* stream);
+/* Count-matrix exchange over peer memory, replacing the all-gather of the
+ * per-owner counts and ash_route_recv_status in one kernel.  peer_xchg[r]:
+ * rank r's exchange buffer (int64, world * world + world entries, mapped
+ * here; its flag tail zeroed before the first op).  Stores this rank's
+ * counts into row `rank` of every peer's matrix and release-stores `epoch`
+ * (> 0, +1 per op, the same on every rank) into its flag; waits (device
+ * side) for every source's flag of this epoch, then writes the matrix to
+ * count_matrix (device, world x world) and status as ash_route_recv_status,
+ * with status[1] = 2 when some source stayed silent for timeout_ns. */
+int ash_route_exchange(const int64_t* counts, int32_t world, int32_t rank, void* const* peer_xchg,
+                       uint64_t epoch, int64_t recv_capacity, int64_t* count_matrix, int32_t* status,
+                       uint64_t timeout_ns, void* stream);
 
 #ifdef __cplusplus
 }

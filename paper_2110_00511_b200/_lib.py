@@ -101,12 +101,14 @@ _SIGNATURES = {
     "ash_route_recv_status": (c_int32, [c_void_p, c_int32, c_int32, c_int64, c_void_p, c_void_p]),
     "ash_route_pull_counts": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p]),
+    "ash_route_exchange": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, ctypes.c_uint64, c_int64, c_void_p,
+                                     c_void_p, ctypes.c_uint64, c_void_p]),
     "ash_gather_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ash_scatter_rows": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
 }
 _ROUTE_FUNCS = ("ash_route_owner", "ash_route_partition", "ash_gather_rows", "ash_scatter_rows",
                 "ash_route_count", "ash_route_put", "ash_route_put_counts", "ash_route_pull",
-                "ash_route_recv_status", "ash_route_pull_counts")
+                "ash_route_recv_status", "ash_route_pull_counts", "ash_route_exchange")
 
 EXPORTED = tuple(_SIGNATURES)
 

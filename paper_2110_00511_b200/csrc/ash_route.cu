@@ -462,6 +462,85 @@ __global__ void k_route_recv_status(const int64_t* __restrict__ cmat, uint32_t w
   }
 }
 
+// Count-matrix exchange over peer memory (replaces the all-gather of the
+// per-owner counts and ash_route_recv_status): every rank's exchange buffer
+// holds the world x world matrix followed by one epoch flag per source rank.
+// Thread t stores this rank's count row into peer t's matrix (row `rank`),
+// fences at system scope and release-stores the op's epoch into peer t's
+// flag[rank]; then it acquire-spins on its own flag[t] until source t's row
+// of this epoch has landed.  The matrix is copied out (the next op's rows may
+// overwrite the exchange buffer only after this rank passed the op's
+// post-put barrier, i.e. after this copy), and the receive status computed
+// as k_route_recv_status does.  A source silent for timeout_ns sets
+// status[1] = 2 (the put then stores nothing, the pull is a no-op).
+struct XchgArgs {
+  int64_t* x[kMaxWorld];
+};
+
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t ld_relaxed_sys_i64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kMaxWorld) k_route_exchange(const int64_t* __restrict__ counts, uint32_t world,
+                                                              uint32_t rank, XchgArgs xa, uint64_t epoch,
+                                                              int64_t cap, int64_t* __restrict__ mat,
+                                                              int32_t* status, uint64_t timeout_ns) {
+  __shared__ int s_over, s_late;
+  const uint32_t t = threadIdx.x;
+  if (t == 0) s_over = s_late = 0;
+  const uint32_t ww = world * world;
+  if (t < world) {
+    int64_t* px = xa.x[t];
+    for (uint32_t j = 0; j < world; ++j) px[rank * world + j] = counts[j];
+    __threadfence_system();
+    st_release_sys_u64(reinterpret_cast<uint64_t*>(px + ww + rank), epoch);
+  }
+  __syncthreads();
+  const int64_t* lx = xa.x[rank];
+  if (t < world) {
+    const uint64_t* f = reinterpret_cast<const uint64_t*>(lx + ww + t);
+    const uint64_t t0 = global_ns();
+    while (static_cast<int64_t>(ld_acquire_sys_u64(f) - epoch) < 0) {
+      if (global_ns() - t0 > timeout_ns) {
+        s_late = 1;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < ww; i += blockDim.x) mat[i] = ld_relaxed_sys_i64(lx + i);
+  __syncthreads();
+  for (uint32_t o = t; o < world; o += blockDim.x) {
+    int64_t tot = 0;
+    for (uint32_t src = 0; src < world; ++src) tot += mat[src * world + o];
+    if (tot > cap) s_over = 1;
+  }
+  __syncthreads();
+  if (t == 0) {
+    int64_t m = 0;
+    for (uint32_t src = 0; src < world; ++src) m += mat[src * world + rank];
+    const int bad = s_late ? 2 : s_over;
+    status[0] = bad ? 0 : static_cast<int32_t>(m);
+    status[1] = bad;
+  }
+}
+
 // dst[i] = src[idx[i]] (gather) / dst[idx[i]] = src[i] (scatter): thread per row
 __global__ void k_gather_rows(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                               int64_t rb, uint8_t* __restrict__ dst) {
@@ -628,6 +707,25 @@ int ash_route_recv_status(const int64_t* count_matrix, int32_t world, int32_t ra
                                                                       static_cast<uint32_t>(rank), recv_capacity,
                                                                       status); note_launch();
   return rcheck("ash_route_recv_status");
+}
+
+int ash_route_exchange(const int64_t* counts, int32_t world, int32_t rank, void* const* peer_xchg, uint64_t epoch,
+                       int64_t recv_capacity, int64_t* count_matrix, int32_t* status, uint64_t timeout_ns,
+                       void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || recv_capacity < 0 || epoch == 0)
+    return rfail("bad routing arguments");
+  if (!counts || !peer_xchg || !count_matrix || !status) return rfail("null routing buffer");
+  XchgArgs xa;
+  memset(&xa, 0, sizeof(xa));
+  for (int o = 0; o < world; ++o) {
+    if (!peer_xchg[o]) return rfail("null peer exchange buffer");
+    xa.x[o] = static_cast<int64_t*>(peer_xchg[o]);
+  }
+  k_route_exchange<<<1, kMaxWorld, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, static_cast<uint32_t>(world), static_cast<uint32_t>(rank), xa, epoch, recv_capacity, count_matrix,
+      status, timeout_ns);
+  note_launch();
+  return rcheck("ash_route_exchange");
 }
 
 int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t world, int32_t rank,

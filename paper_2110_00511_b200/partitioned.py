@@ -35,6 +35,15 @@ __all__ = ["PartitionedHashMap", "PartitionedResult", "CudaRouter"]
 # sync-free peer ops (device-sized shard op); ASH_PEER_DN=0 keeps the host
 # read of the count matrix inside each op
 _PEER_DN = __import__("os").environ.get("ASH_PEER_DN", "1") == "1"
+# count matrix exchanged through peer memory by one kernel (ash_route_exchange)
+# instead of an all-gather + ash_route_recv_status; ASH_PEER_XCHG=0 for A/B
+_PEER_XCHG = __import__("os").environ.get("ASH_PEER_XCHG", "1") == "1"
+_XCHG_TIMEOUT_NS = 30 * 10 ** 9  # a peer silent this long fails the op instead of hanging the GPU
+
+
+def _exchange_ok(over: int) -> None:
+    if over == 2:
+        raise RuntimeError("peer count exchange timed out: a rank did not reach the collective op")
 
 
 @dataclass
@@ -149,6 +158,16 @@ class PeerExchange:
         self._flag_h = self._flag_ev = None
         self.capacity = 0
         self._alloc(capacity)
+        # count-matrix exchange buffer (ash_route_exchange): symmetric memory
+        # only (ranks sharing a GPU exchange the counts through gloo)
+        self._p_xchg = None
+        self._epoch = 0
+        if mapping == "symmetric" and _PEER_XCHG:
+            self._xchg = self._symm.empty(world * world + world, dtype=torch.int64, device=device)
+            self._xchg.zero_()
+            self._xchg_handle = self._symm.rendezvous(self._xchg, self.group_name)
+            self._p_xchg = (self._lib.c_void_p * world)(*self._xchg_handle.buffer_ptrs)
+            self._xchg_handle.barrier(channel=0)  # zeroed on every rank before the first exchange
 
     def _alloc(self, cap: int) -> None:
         cap = max(int(cap), 1)
@@ -268,16 +287,24 @@ class PeerExchange:
         owners = torch.empty(n, dtype=torch.uint8, device=self.device)
         lib.call("ash_route_count", keys.data_ptr(), n, self.arity, self.world, counts.data_ptr(),
                  owners.data_ptr(), self._scratch.data_ptr(), self._scratch.numel(), self._stream())
-        if dist.get_backend(self.group) == "gloo":  # CPU control plane (tests: ranks sharing a GPU)
-            parts = [torch.empty(self.world, dtype=torch.int64) for _ in range(self.world)]
-            dist.all_gather(parts, counts.cpu(), group=self.group)
-            mat = torch.stack(parts).to(self.device)
-        else:
-            mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
-            dist.all_gather_into_tensor(mat, counts, group=self.group)
         status = torch.empty(2, dtype=torch.int32, device=self.device)
-        lib.call("ash_route_recv_status", mat.data_ptr(), self.world, self.rank, self.capacity,
-                 status.data_ptr(), self._stream())
+        if self._p_xchg is not None:
+            # counts through peer memory, waited for on the device: no
+            # collective call, no host wait
+            mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
+            self._epoch += 1
+            lib.call("ash_route_exchange", counts.data_ptr(), self.world, self.rank, self._p_xchg, self._epoch,
+                     self.capacity, mat.data_ptr(), status.data_ptr(), _XCHG_TIMEOUT_NS, self._stream())
+        else:
+            if dist.get_backend(self.group) == "gloo":  # CPU control plane (tests: ranks sharing a GPU)
+                parts = [torch.empty(self.world, dtype=torch.int64) for _ in range(self.world)]
+                dist.all_gather(parts, counts.cpu(), group=self.group)
+                mat = torch.stack(parts).to(self.device)
+            else:
+                mat = torch.empty((self.world, self.world), dtype=torch.int64, device=self.device)
+                dist.all_gather_into_tensor(mat, counts, group=self.group)
+            lib.call("ash_route_recv_status", mat.data_ptr(), self.world, self.rank, self.capacity,
+                     status.data_ptr(), self._stream())
         # the overflow flag reaches the host early in the op (its first
         # kernels): the op's end waits for this event, not for the pull
         if self._flag_h is None:
@@ -452,12 +479,14 @@ class PartitionedHashMap:
                 self.local._op_into_dn(op, rkeys, pays, self.peer.ret, status)
             else:  # this shard needs the host-checked op (growth): read the length
                 m, over = status.tolist()
+                _exchange_ok(over)
                 if not over:
                     self.local._op_into(op, rkeys[:m], [p[:m] for p in pays], self.peer.ret[:m])
             out, msk = self.peer.combine_dn(ctx, status)
             if over is None:  # the one host read: did a receive buffer overflow?
                 self.peer._flag_ev.synchronize()
                 over = int(self.peer._flag_h[1])
+                _exchange_ok(over)
             if not over:
                 self.local._dn_done(op)
                 return PartitionedResult(out, msk, ctx[1])

@@ -198,3 +198,51 @@ def test_peer_put_with_device_count_matrix(cuda_ok, world, rank):
             a, b = int(before[o]), int(before[o] + cnt[o])
             assert np.array_equal(got[a:b], k[sel]) and np.array_equal(gp[a:b], pay[sel])
             assert np.all(got[:a] == -7) and np.all(got[b:] == -7)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_count_exchange_kernel(cuda_ok, world):
+    """ash_route_exchange: every rank's exchange kernel (one per stream, all
+    resident together) stores its count row into every peer's buffer and
+    waits for theirs; each gets the full matrix and the receive status of
+    ash_route_recv_status, over several epochs; an overflow gives status
+    [0, 1]."""
+    from paper_2110_00511_b200 import _lib
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(world)
+    xchg = [torch.zeros(world * world + world, dtype=torch.int64, device=dev) for _ in range(world)]
+    P = _lib.c_void_p * world
+    peers = P(*[x.data_ptr() for x in xchg])
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    torch.cuda.synchronize()
+    for epoch in range(1, 4):
+        C = rng.integers(0, 1000, size=(world, world)).astype(np.int64)
+        cap = int(C.sum(0).max()) - (1 if epoch == 3 else 0)
+        counts = [torch.from_numpy(C[r].copy()).to(dev) for r in range(world)]
+        mats = [torch.full((world, world), -1, dtype=torch.int64, device=dev) for _ in range(world)]
+        stats = [torch.full((2,), -9, dtype=torch.int32, device=dev) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            _lib.call("ash_route_exchange", counts[r].data_ptr(), world, r, peers, epoch, cap, mats[r].data_ptr(),
+                      stats[r].data_ptr(), 10 ** 10, streams[r].cuda_stream)
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert np.array_equal(mats[r].cpu().numpy(), C), (epoch, r)
+            over = epoch == 3
+            assert stats[r].tolist() == ([0, 1] if over else [int(C[:, r].sum()), 0])
+
+
+def test_count_exchange_timeout(cuda_ok):
+    """A source that never reaches the exchange: status [0, 2] after the
+    timeout instead of a hung kernel."""
+    from paper_2110_00511_b200 import _lib
+    dev = torch.device("cuda")
+    xchg = [torch.zeros(2 * 2 + 2, dtype=torch.int64, device=dev) for _ in range(2)]
+    peers = (_lib.c_void_p * 2)(*[x.data_ptr() for x in xchg])
+    counts = torch.tensor([3, 4], dtype=torch.int64, device=dev)
+    mat = torch.empty((2, 2), dtype=torch.int64, device=dev)
+    st = torch.full((2,), -9, dtype=torch.int32, device=dev)
+    _lib.call("ash_route_exchange", counts.data_ptr(), 2, 0, peers, 1, 100, mat.data_ptr(), st.data_ptr(),
+              5 * 10 ** 6, torch.cuda.current_stream().cuda_stream)
+    assert st.tolist() == [0, 2]
+    assert xchg[1][2 * 2 + 0].item() == 1 and xchg[1][0:2].tolist() == [3, 4]  # our row + flag reached rank 1
