@@ -742,9 +742,12 @@ def bench_main(args, rank: int, world: int) -> None:
     stream = torch.cuda.current_stream(dev)
 
     def step():
+        # ranks aligned first, then the L2 flush: as in the single-GPU step,
+        # the host issues the op while the flush runs, so the events time
+        # the device work of the op (not the host's launch prologue)
+        dist.barrier()
         pm.local.clear()
         flush.add_(1)
-        dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
