@@ -69,7 +69,7 @@ for rep in range(3):
             ws.use(slots, probe)
             _lib.call("ash_allocate_blocks", gm._ptr(), ctypes.byref(ws.struct), coords.data_ptr(), n,
                       out.data_ptr(), gi.data_ptr(), gmask.data_ptr(), si.data_ptr(), sm.data_ptr(), st.data_ptr(),
-                      stream)
+                      int(ws.estimate <= blocks._SMALL_ACTIVATE), stream)
             t = tick("launch (C call)", t)
             vals = st.tolist()
             t = tick("status read (sync)", t)
