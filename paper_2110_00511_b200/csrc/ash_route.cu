@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/ash.h"
@@ -28,6 +29,13 @@ constexpr int kTile = kBlock * kItems;
 constexpr int kMaxWorld = 64;
 
 thread_local char g_route_err[256] = "";
+
+// ASH_PUT_STAGED=0: the put stores each row straight to its owner instead of
+// staging the tile's rows per owner (A/B runs); read at load time
+int g_put_staged = [] {
+  const char* e = getenv("ASH_PUT_STAGED");
+  return e ? (e[0] != '0' ? 1 : 0) : 1;
+}();
 
 int rfail(const char* msg) {
   snprintf(g_route_err, sizeof(g_route_err), "%s", msg);
@@ -297,13 +305,24 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
                                                       const int32_t* __restrict__ off, int64_t n_tiles,
                                                       const uint8_t* __restrict__ pay, int64_t pay_rb, PeerArgs pa,
                                                       int32_t* __restrict__ jdx, const int64_t* __restrict__ cmat,
-                                                      uint32_t rank, int64_t cap) {
+                                                      uint32_t rank, int64_t cap, int staged) {
   constexpr int kW = kBlock / 32;
-  __shared__ int32_t s_pre[kItems][kW][kMaxWorld];
+  // per-(item, warp, owner) offsets first; the same memory then stages the
+  // tile's rows owner by owner (key words, then 4-byte payload words), each
+  // owner's run aligned like its destination
+  constexpr int kPreWords = kItems * kW * kMaxWorld;
+  constexpr int kStageKeyWords = kTile * 3 + 4 * kMaxWorld;
+  constexpr int kStageWords = kStageKeyWords + kTile + 4 * kMaxWorld;
+  static_assert(kStageKeyWords % 4 == 0, "payload stage 16-byte aligned");
+  __shared__ __align__(16) int32_t s_raw[kStageWords > kPreWords ? kStageWords : kPreWords];
+  auto s_pre = reinterpret_cast<int32_t(*)[kW][kMaxWorld]>(s_raw);
   __shared__ int64_t s_off[kMaxWorld];
+  __shared__ int32_t s_t0[kMaxWorld], s_tc[kMaxWorld], s_kb[kMaxWorld], s_pb[kMaxWorld];
+  __shared__ int32_t* s_run_dst[2 * kMaxWorld];  // staged runs: peer destination, stage offset, words
+  __shared__ int32_t s_run_src[2 * kMaxWorld], s_run_n[2 * kMaxWorld], s_run_ch[2 * kMaxWorld + 1], s_runs;
   __shared__ int s_skip;
   const int warp = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < kItems * kW * kMaxWorld; e += kBlock) (&s_pre[0][0][0])[e] = 0;
+  for (int e = threadIdx.x; e < kPreWords; e += kBlock) s_raw[e] = 0;
   if (threadIdx.x == 0) s_skip = 0;
   __syncthreads();
   // row offsets: given, or from the exchanged count matrix cmat[src][owner]
@@ -343,12 +362,14 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
   // segment start off[o * n_tiles]
   for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
     int32_t run = off[o * n_tiles + blockIdx.x] - off[o * n_tiles];
+    s_t0[o] = run;  // the tile's rows for owner o: [run, run + count) of this source's segment
     for (int it = 0; it < kItems; ++it)
       for (int w = 0; w < kW; ++w) {
         const int32_t c = s_pre[it][w][o];
         s_pre[it][w][o] = run;
         run += c;
       }
+    s_tc[o] = run - s_t0[o];
   }
   __syncthreads();
   if (arity == 3 && (pay_rb == 0 || (pay_rb == 4 && (reinterpret_cast<uintptr_t>(pay) & 3) == 0))) {
@@ -363,18 +384,110 @@ __global__ void __launch_bounds__(kBlock) k_route_put(const int32_t* __restrict_
       for (int d = 0; d < 3; ++d) kw[it][d] = static_cast<uint32_t>(__ldg(keys + p * 3 + d));
       if (pay_rb) pw[it] = __ldg(reinterpret_cast<const uint32_t*>(pay) + p);
     }
+    if (!staged) {  // direct stores (A/B: ASH_PUT_STAGED=0)
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int64_t p = base + it * kBlock + threadIdx.x;
+        if (p >= n) continue;
+        const uint32_t o = own[it];
+        const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
+        const int64_t row = s_off[o] + j;
+        jdx[p] = j;
+        int32_t* kd = pa.keys[o] + row * 3;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) kd[d] = static_cast<int32_t>(kw[it][d]);
+        if (pay_rb) reinterpret_cast<uint32_t*>(pa.pay[o])[row] = pw[it];
+      }
+      return;
+    }
+    // rows for this rank's own shard are local stores, coalesced by the L2;
+    // rows for a peer are staged per owner and leave as 16-byte vectors (a
+    // direct int3 row store from a warp whose rows spread over N owners
+    // moves ~4-byte pieces of many sectors across NVLink)
+    int32_t jr[kItems];
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const int64_t p = base + it * kBlock + threadIdx.x;
+      jr[it] = 0;
       if (p >= n) continue;
       const uint32_t o = own[it];
-      const int32_t j = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
-      const int64_t row = s_off[o] + j;
-      jdx[p] = j;
-      int32_t* kd = pa.keys[o] + row * 3;
+      jr[it] = s_pre[it][warp][o] + static_cast<int32_t>(rank_in_warp[it]);
+      jdx[p] = jr[it];
+      if (o == rank) {
+        const int64_t row = s_off[o] + jr[it];
+        int32_t* kd = pa.keys[o] + row * 3;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) kd[d] = static_cast<int32_t>(kw[it][d]);
-      if (pay_rb) reinterpret_cast<uint32_t*>(pa.pay[o])[row] = pw[it];
+        for (int d = 0; d < 3; ++d) kd[d] = static_cast<int32_t>(kw[it][d]);
+        if (pay_rb) reinterpret_cast<uint32_t*>(pa.pay[o])[row] = pw[it];
+      }
+    }
+    if (world == 1) return;
+    __syncthreads();  // s_pre is read: its memory becomes the stage
+    constexpr int kChunk = 128;  // 16-byte vectors per warp task
+    if (threadIdx.x == 0) {
+      uint32_t kb = 0, pb = 0;
+      int32_t runs = 0, chunks = 0;
+      for (uint32_t o = 0; o < world; ++o) {
+        const int32_t c = o == rank ? 0 : s_tc[o];
+        const int64_t row0 = s_off[o] + s_t0[o];
+        for (int part = 0; part < (pay_rb ? 2 : 1); ++part) {
+          int32_t* dst = part == 0 ? pa.keys[o] + row0 * 3 : reinterpret_cast<int32_t*>(pa.pay[o]) + row0;
+          const int32_t words = part == 0 ? 3 * c : c;
+          uint32_t& b = part == 0 ? kb : pb;
+          const uint32_t a = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(dst) >> 2) & 3);
+          b += (a - b) & 3u;  // the run starts congruent with its destination mod 16 bytes
+          if (part == 0) s_kb[o] = static_cast<int32_t>(b);
+          else s_pb[o] = static_cast<int32_t>(b);
+          if (words > 0) {
+            const int32_t head = min(words, static_cast<int32_t>((4 - a) & 3));
+            const int32_t nv = (words - head) >> 2;
+            s_run_dst[runs] = dst;
+            s_run_src[runs] = static_cast<int32_t>(b) + (part == 0 ? 0 : kStageKeyWords);
+            s_run_n[runs] = words;
+            s_run_ch[runs] = chunks;
+            chunks += nv > 0 ? (nv + kChunk - 1) / kChunk : 1;
+            ++runs;
+          }
+          b += static_cast<uint32_t>(words);
+        }
+      }
+      s_run_ch[runs] = chunks;
+      s_runs = runs;
+    }
+    __syncthreads();
+    int32_t* sk = s_raw;
+    int32_t* sp = s_raw + kStageKeyWords;
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t p = base + it * kBlock + threadIdx.x;
+      if (p >= n || own[it] == rank) continue;
+      const uint32_t o = own[it];
+      const int32_t l = jr[it] - s_t0[o];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) sk[s_kb[o] + 3 * l + d] = static_cast<int32_t>(kw[it][d]);
+      if (pay_rb) sp[s_pb[o] + l] = static_cast<int32_t>(pw[it]);
+    }
+    __syncthreads();
+    // warp tasks: chunk k of run r = vectors [k * kChunk, (k + 1) * kChunk),
+    // the first chunk adds the unaligned head words, the last the tail
+    const int lane = threadIdx.x & 31;
+    const int32_t runs = s_runs, total = s_run_ch[runs];
+    int r = 0;
+    for (int32_t c = warp; c < total; c += kW) {
+      while (s_run_ch[r + 1] <= c) ++r;
+      int32_t* dst = s_run_dst[r];
+      const int32_t* src = s_raw + s_run_src[r];
+      const int32_t words = s_run_n[r];
+      const int32_t head = min(words, static_cast<int32_t>((4 - ((reinterpret_cast<uintptr_t>(dst) >> 2) & 3)) & 3));
+      const int32_t nv = (words - head) >> 2;
+      const int32_t k = c - s_run_ch[r], last = s_run_ch[r + 1] - s_run_ch[r] - 1;
+      if (k == 0 && lane < head) dst[lane] = src[lane];
+      const int4* s4 = reinterpret_cast<const int4*>(src + head);
+      int4* d4 = reinterpret_cast<int4*>(dst + head);
+      const int32_t v1 = min(nv, (k + 1) * kChunk);
+      for (int32_t v = k * kChunk + lane; v < v1; v += 32) d4[v] = s4[v];
+      const int32_t t0 = head + 4 * nv;
+      if (k == last && lane < words - t0) dst[t0 + lane] = src[t0 + lane];
     }
     return;
   }
@@ -658,7 +771,7 @@ static int route_put(const int32_t* keys, int64_t n, int32_t arity, int32_t worl
   k_route_put<<<static_cast<unsigned>(n_tiles), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
       keys, n, arity, static_cast<uint32_t>(world), owners, scratch, n_tiles,
       static_cast<const uint8_t*>(payload), payload_row_bytes, pa, jdx, cmat, static_cast<uint32_t>(rank),
-      cap); note_launch();
+      cap, g_put_staged); note_launch();
   return rcheck("ash_route_put");
 }
 
