@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import call
-from .hashmap import HashMap, ValueSpec, _stream_handle
+from .hashmap import HashMap, ValueSpec, _get_device, _stream_handle
 
 __all__ = ["allocate_blocks", "BlockGrid", "frame_candidates", "frame_blocks", "allocate_frame",
            "LocalBlockMap", "unique_rows"]
@@ -86,7 +86,7 @@ def _allocate_fused(gm: HashMap, n: int, launch):
     from .geometry import _VoxelWorkspace
     dev = gm.device
     ws = _VoxelWorkspace.get(dev)
-    same_dev = dev.index == torch.cuda.current_device()
+    same_dev = _get_device is not None and torch.cuda.is_initialized() and dev.index == _get_device()
     with _VoxelWorkspace._lock, (contextlib.nullcontext() if same_dev else torch.cuda.device(dev)), \
             gm._guard.writing():
         gm._settle()

@@ -129,6 +129,7 @@ class _VoxelWorkspace:
         self.struct.counters = self.counters.data_ptr()
         self.estimate = 0  # distinct keys of the previous call
         self._seq_bufs = None
+        self._reserved = -1  # batch size of the last reserve()
 
     @classmethod
     def get(cls, device: torch.device) -> "_VoxelWorkspace":
@@ -143,6 +144,8 @@ class _VoxelWorkspace:
     PROBE_LIMIT = 64  # buckets, for the estimated-size attempt
 
     def reserve(self, n: int) -> None:
+        if n == self._reserved:  # the per-frame case: same batch size, nothing to size
+            return
         need = _table_slots(max(n, 1), 2.0)
         if need > self.n_slots:
             self.slots = torch.empty(need * 4, dtype=torch.int32, device=self.device)
@@ -158,6 +161,7 @@ class _VoxelWorkspace:
             self.tiles = torch.zeros(tiles, dtype=torch.int32, device=self.device)
             self.struct.tile_counts = self.tiles.data_ptr()
             self.struct.tile_counts_len = tiles
+        self._reserved = n
 
     def sequence_buffers(self, n: int):
         """(blocks, gi, gmask, scratch_idx, scratch_mask, status) for a fused

@@ -45,6 +45,8 @@ def test_scan_tiles_and_error_plumbing():
     assert _lib.scan_tiles(1) == 1
     assert _lib.scan_tiles(_lib.TILE) == 1
     assert _lib.scan_tiles(_lib.TILE + 1) == 2
+    for n in (0, 1, 2047, 2048, 2049, 10_000_000, 2 ** 31):
+        assert _lib.scan_tiles(n) == int(_lib.lib.ash_scan_tiles(n)), n
     # invalid arguments are rejected before any device work
     with pytest.raises(ValueError, match="null map"):
         _lib.call("ash_find", None, None, 0, None, None, None)
