@@ -197,7 +197,8 @@ class _VoxelWorkspace:
         for slots, probe in self.attempts():
             self.use(slots, probe)
             launch()
-            count, flags = self.counters[[_lib.CTR_COUNT, _lib.CTR_FLAGS]].tolist()
+            # FLAGS (4) and COUNT (5) are adjacent: a view, one 8-byte read (no gather kernel)
+            flags, count = self.counters[_lib.CTR_FLAGS:_lib.CTR_COUNT + 1].tolist()
             if probe and flags & _lib.FLAG_TABLE_FULL:
                 self.refill(slots)  # claimed slots stay claimed after an overflow
                 continue
