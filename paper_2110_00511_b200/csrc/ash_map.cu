@@ -1134,6 +1134,8 @@ __global__ void __launch_bounds__(kBlock)
     }
   }
   const int arity = A ? A : t.arity;
+  // no frees at or above top: heap[top + r] == top + r (no heap loads)
+  const bool ident = __ldg(counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(sm.base);
   // phase 1: every load of every winner (heap index, key words, value row)
   // before any store, so each thread keeps kItems x several loads in flight
   int32_t hidx[kItems];
@@ -1143,7 +1145,8 @@ __global__ void __launch_bounds__(kBlock)
   for (int it = 0; it < kItems; ++it) {
     if (!win[it]) continue;
     const int64_t p = base + it * kBlock + threadIdx.x;
-    hidx[it] = static_cast<int32_t>(ld_stream(heap + sm.base + item_rank(sm, bal, it), pol));
+    const uint32_t hpos = sm.base + item_rank(sm, bal, it);
+    hidx[it] = ident ? static_cast<int32_t>(hpos) : static_cast<int32_t>(ld_stream(heap + hpos, pol));
     const int32_t* kr = keys + p * arity;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -1307,6 +1310,7 @@ __global__ void __launch_bounds__(kCommitThreads)
   __shared__ CommitStageInfo info[kCommitStages];
   __shared__ ScanSmem sm;
   __shared__ uint32_t s_top;
+  __shared__ int s_ident;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = stream_policy(t.hints);
@@ -1322,9 +1326,12 @@ __global__ void __launch_bounds__(kCommitThreads)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_top = static_cast<uint32_t>(ld_volatile_i32(counters + ASH_CTR_TOP_BASE));
+    // no frees at or above top: heap[top + r] == top + r, nothing to stage
+    s_ident = ld_volatile_i32(counters + ASH_CTR_HEAP_DIRTY) <= static_cast<int32_t>(s_top);
   }
   __syncthreads();
   const uint32_t top = s_top;
+  const bool ident = s_ident;
 
   if (warp == kCommitConsumers / 32) {
     // ---------------- producer warp (lane 0 issues) ----------------
@@ -1348,7 +1355,7 @@ __global__ void __launch_bounds__(kCommitThreads)
         tx += stage_range(st + L::kMask, mask + base, rows, &full[s], pol);
         tx += stage_range(st + L::kKeys, keys + base * A, rows * A * 4, &full[s], pol);
         if (SV) tx += stage_range(st + L::kVals, va.src[0] + base * SV * 4, rows * SV * 4, &full[s], pol);
-        if (he > hs) tx += stage_range(st + L::kHeap, heap + hs_al, (he - hs_al) * 4, &full[s], pol);
+        if (!ident && he > hs) tx += stage_range(st + L::kHeap, heap + hs_al, (he - hs_al) * 4, &full[s], pol);
         mbar_arrive_expect_tx(&full[s], tx);
       }
     }
@@ -1427,7 +1434,7 @@ __global__ void __launch_bounds__(kCommitThreads)
       const int64_t p = base + r;
       if (win[it]) {
         const uint32_t rank = sm.pre[it * kCW + warp] + __popc(bal[it] & lanemask_lt());
-        const int32_t idx = s_heap[heap_off + rank];
+        const int32_t idx = ident ? static_cast<int32_t>(top + info[s].pre + rank) : s_heap[heap_off + rank];
         const uint32_t slot = static_cast<uint32_t>(v[it]) & SLOT_MASK;
         if (!defer && !states_final) t.slots[slot].w = static_cast<uint32_t>(idx);  // PENDING -> committed
         int32_t* dr = key_buf + static_cast<int64_t>(idx) * arity;
