@@ -7,7 +7,8 @@
 //   hashmap.py:431-456 erase + index_heap.py:38-47 sorted free        -> k_erase_* + k_free_compact
 //   hashmap.py:458-460 active_indices                                 -> k_active_compact
 //   hashmap.py:326-332 _rehash_into                                   -> k_rehash_build
-//   geometry.py:49-76 quantize / voxel_downsample                     -> k_quantize / k_voxel_*
+//   geometry.py:49-76 quantize / voxel_downsample                     -> k_quantize / k_dd_* (dedup-select)
+//   tsdf/grid.py:98-150 candidates + allocate_blocks map calls         -> k_dd_*<FrameSrc|RowSrc> + k_activate_small
 //
 // Table: open addressing over 16-byte slots {w0,w1,w2,state}, probed as
 // 32-byte buckets (two slots = one DRAM sector; one 256-bit load each).
