@@ -86,8 +86,20 @@ def _random_access(kms):
     ra = json.loads(files[-1].read_text())
     ceil = ra["probe_32B_gps"]
     find_gps = N_KEYS / (kms["find"] / 1e3) / 1e9
-    return {"probe_ceiling_gps": ceil, "source": files[-1].name,
-            "find_gprobes_per_s": round(find_gps, 1), "find_frac_of_ceiling": round(find_gps / ceil, 3)}
+    out = {"probe_ceiling_gps": ceil, "source": files[-1].name,
+           "find_gprobes_per_s": round(find_gps, 1), "find_frac_of_ceiling": round(find_gps / ceil, 3)}
+    rmw = ra.get("rmw_5M")
+    if rmw and "claim" in kms:
+        # the claim's measured floor on the same 240 MB table: every position
+        # loads its home bucket (probe ceiling), every winner adds a 16-byte
+        # CAS on the loaded line (tools/atomics.cu: load+CAS128 minus load,
+        # per 5M), winners = rho x N
+        floor = N_KEYS / ceil / 1e6 + (rmw["load_cas128_ms"] - rmw["load_ms"]) * (RHO * N_KEYS / 5e6)
+        out.update({"claim_floor_ms": round(floor, 4), "claim_ms": round(kms["claim"], 4),
+                    "claim_frac_of_floor": round(floor / kms["claim"], 3),
+                    "claim_floor_model": "N / probe ceiling + winners x (load+CAS128 - load) per op, "
+                                         "same table size"})
+    return out
 
 
 def _peaks():
