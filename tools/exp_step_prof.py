@@ -11,11 +11,11 @@ from torch.profiler import ProfilerActivity, profile
 import paper_2110_00511_b200 as ash
 from paper_2110_00511_b200.workloads import gen_keys
 
-N = 10_000_000
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000  # 100000: configs[0]
 dev = torch.device("cuda:0")
 keys = torch.from_numpy(gen_keys(N, 0.5, "int3", seed=0)).to(dev)
 vals = torch.from_numpy(np.random.default_rng(1).random((N, 1), dtype=np.float32)).to(dev)
-m = ash.HashMap(N, 3, [np.float32], device=dev)
+m = ash.HashMap(N if N >= 1_000_000 else 2 * N, 3, [np.float32], device=dev)  # configs[0]: capacity 2N
 flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
 
