@@ -44,6 +44,7 @@ _SIGNATURES = {
     "ash_set_stream_hints": (c_int32, [c_int32]),
     "ash_launch_count": (c_int64, []),
     "ash_set_commit_mode": (c_int32, [c_int32, c_int32]),
+    "ash_set_sweep_table_min": (c_int32, [c_int64]),
     "ash_scan_tiles": (c_int64, [c_int64]),
     "ash_map_reset": (c_int32, [_M, c_int32, c_void_p]),
     "ash_find": (c_int32, [_M, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
@@ -130,6 +131,7 @@ def _load():
 
 lib = _load()
 lib.ash_set_stream_hints(int(_os.environ.get("ASH_STREAM_HINTS", "1")))
+lib.ash_set_sweep_table_min(int(_os.environ.get("ASH_SWEEP_TABLE_MIN", "-1")))
 lib.ash_set_commit_mode(int(_os.environ.get("ASH_COMMIT_BULK", "1")),
                         int(_os.environ.get("ASH_SWEEP_DIV", "5")))
 

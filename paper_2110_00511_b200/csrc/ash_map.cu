@@ -2491,6 +2491,8 @@ int g_commit_bulk = -1;  // ASH_COMMIT_BULK=0 selects the plain commit (A/B runs
 
 int g_sweep_div = 5;     // table sweep when winners >= n_buckets / g_sweep_div (0: never)
 
+int64_t g_sweep_table_min = -1;  // tables of at most this many bytes never sweep (< 0: L2 / 4)
+
 constexpr int kMaxDevices = 64;
 
 int current_device() {
@@ -2511,6 +2513,27 @@ int device_sms() {
     cache[dev].store(v, std::memory_order_relaxed);
   }
   return v;
+}
+
+// winners at which an insert commits its slot states by the table sweep:
+// never for a table that stays L2-resident between claim and commit
+int64_t sweep_min_for(const Table& t) {
+  if (g_sweep_div <= 0) return INT64_MAX;
+  int64_t small = g_sweep_table_min;
+  if (small < 0) {
+    static std::atomic<int64_t> l2_cache[kMaxDevices];
+    const int dev = current_device();
+    int64_t l2 = l2_cache[dev].load(std::memory_order_relaxed);
+    if (!l2) {
+      int v = 0;
+      cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+      l2 = v > 0 ? v : 1;
+      l2_cache[dev].store(l2, std::memory_order_relaxed);
+    }
+    small = l2 / 4;
+  }
+  if (static_cast<int64_t>(t.n_buckets) * 32 <= small) return INT64_MAX;
+  return (t.n_buckets + g_sweep_div - 1) / g_sweep_div;
 }
 
 __global__ void k_alloc_status(const int32_t* ws_counters, const int32_t* g_counters, int32_t* status, int phase);
@@ -2708,6 +2731,7 @@ static int allocate_fused(ash_map_t* global, ash_map_t* ws, const Src& src, int6
   key_put(key, g_stream_hints);
   key_put(key, g_commit_bulk);
   key_put(key, g_sweep_div);
+  key_put(key, g_sweep_table_min);
   key_put(key, small);
   key_put(sb, src);
   ++tick;
@@ -2832,6 +2856,11 @@ extern "C" {
 int ash_abi_version(void) { return ASH_ABI_VERSION; }
 
 int64_t ash_launch_count(void) { return ash_launch_counter().load(std::memory_order_relaxed); }
+
+int ash_set_sweep_table_min(int64_t bytes) {
+  g_sweep_table_min = bytes;
+  return ASH_OK;
+}
 
 int ash_set_commit_mode(int32_t bulk, int32_t sweep_div) {
   if (sweep_div < 0) return fail(ASH_ERR_INVALID, "sweep divisor must be >= 0");
@@ -2979,8 +3008,7 @@ int ash_settle(ash_map_t* m, void* stream) {
   if (int rc = check_map(m)) return rc;
   if (!m->rank_words) return ASH_OK;
   Table t = make_table(m);
-  const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
-  launch_sweep(t, nullptr, m->rank_words, m, sweep_min, as_stream(stream), nullptr, 0, nullptr, 2);
+  launch_sweep(t, nullptr, m->rank_words, m, sweep_min_for(t), as_stream(stream), nullptr, 0, nullptr, 2);
   return check_launch("ash_settle");
 }
 
@@ -3017,7 +3045,7 @@ static int insert_commit(ash_map_t* m, const int32_t* keys, int64_t n, const voi
   }
   int32_t* pre = split_prefix(m, n);
   // winners at which the slot states are committed by the table sweep
-  const int64_t sweep_min = g_sweep_div > 0 ? (t.n_buckets + g_sweep_div - 1) / g_sweep_div : INT64_MAX;
+  const int64_t sweep_min = sweep_min_for(t);
   int32_t* rank_words = (m->rank_words && m->rank_words_len >= 2 * ((n + 31) / 32)) ? m->rank_words : nullptr;
   // deferred: the table keeps PENDING|pos for this batch's winners until
   // ash_settle (finds resolve them through the rank words meanwhile); the

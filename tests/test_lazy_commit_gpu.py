@@ -19,6 +19,16 @@ def ash(cuda_ok):
     return ash
 
 
+@pytest.fixture(scope="module", autouse=True)
+def sweep_small_tables(cuda_ok):
+    """These maps are small enough to stay in the L2, where inserts skip the
+    table sweep; the tests exercise the sweep, so allow it for every size."""
+    from paper_2110_00511_b200 import _lib
+    _lib.lib.ash_set_sweep_table_min(0)
+    yield
+    _lib.lib.ash_set_sweep_table_min(-1)
+
+
 @pytest.fixture(autouse=True)
 def lazy_default():
     """The deferred commit is opt-in (ASH_LAZY_COMMIT=1); these tests turn it on."""
