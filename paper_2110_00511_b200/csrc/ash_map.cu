@@ -997,50 +997,76 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int
                                                           int top_slot, int total_slot, int32_t* pre_out,
                                                           const int32_t* d_n) {
   if (d_n) n_tiles = (dev_len(n_tiles * kTile, d_n) + kTile - 1) / kTile;
-  __shared__ int32_t warp_tot[kScanBlock / 32];
-  __shared__ int32_t carry;
+  // 32 warps, each a contiguous segment of whole 32-entry chunks read
+  // coalesced with kU chunks in flight: segment sums, a scan of the 32 sums,
+  // then each warp rescans its segment from its offset (a 1024-wide loop
+  // with block barriers per chunk took 6.5-7.8 us at 4.9K tiles)
+  constexpr int kU = 8;
+  static_assert(kScanBlock == 1024, "one warp per segment, 32 segments");
+  __shared__ int32_t warp_off[32];
+  __shared__ int32_t s_total;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+  const int64_t chunks = (n_tiles + 31) / 32;
+  const int64_t per = (chunks + 31) / 32;
+  const int64_t c0 = warp * per, c1 = c0 + per < chunks ? c0 + per : chunks;
+  int32_t sum = 0;
+  for (int64_t c = c0; c < c1; c += kU) {
+    int32_t x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = (c + u) * 32 + lane;
+      x[u] = (c + u < c1 && i < n_tiles) ? tile_cnt[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) sum += x[u];
+  }
+  sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+  if (lane == 0) warp_off[warp] = sum;
   __syncthreads();
-  for (int64_t base = 0; base < n_tiles; base += kScanBlock) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t x = i < n_tiles ? tile_cnt[i] : 0;
-    int32_t incl = x;
+  if (warp == 0) {
+    const int32_t w = warp_off[lane];
+    int32_t wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += y;
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += y;
     }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int32_t w = warp_tot[lane];
-      int32_t wi = w;
+    warp_off[lane] = wi - w;  // exclusive segment offsets
+    if (lane == 31) s_total = wi;
+  }
+  __syncthreads();
+  int32_t carry = warp_off[warp];
+  for (int64_t c = c0; c < c1; c += kU) {
+    int32_t x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = (c + u) * 32 + lane;
+      x[u] = (c + u < c1 && i < n_tiles) ? tile_cnt[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      int32_t incl = x[u];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-        if (lane >= o) wi += y;
+        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
       }
-      warp_tot[lane] = wi - w;  // exclusive warp offsets
-    }
-    __syncthreads();
-    const int32_t c = carry;
-    if (i < n_tiles) {
-      if (pre_out) {
-        pre_out[i] = c + warp_tot[warp] + incl - x;
-        tile_cnt[i] = 0;
-      } else {
-        tile_cnt[i] = c + warp_tot[warp] + incl - x;
+      const int64_t i = (c + u) * 32 + lane;
+      if (c + u < c1 && i < n_tiles) {
+        if (pre_out) {
+          pre_out[i] = carry + incl - x[u];
+          tile_cnt[i] = 0;  // ready for the next batch
+        } else {
+          tile_cnt[i] = carry + incl - x[u];
+        }
       }
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
-    __syncthreads();
-    if (threadIdx.x == kScanBlock - 1) carry = c + warp_tot[warp] + incl;
-    __syncthreads();
   }
   if (threadIdx.x == 0) {
     if (top_slot >= 0) counters[top_slot] = counters[ASH_CTR_TOP];
-    counters[total_slot] = carry;
-    if (pre_out) pre_out[n_tiles] = carry;
+    counters[total_slot] = s_total;
+    if (pre_out) pre_out[n_tiles] = s_total;
   }
 }
 
