@@ -1006,6 +1006,45 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(int32_t* tile_cnt, int
   __shared__ int32_t warp_off[32];
   __shared__ int32_t s_total;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (n_tiles <= kScanBlock) {  // one entry per thread: one load, one block scan
+    const int64_t i = threadIdx.x;
+    const int32_t x = i < n_tiles ? tile_cnt[i] : 0;
+    int32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_off[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int32_t w = warp_off[lane];
+      int32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_off[lane] = wi - w;
+      if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    if (i < n_tiles) {
+      const int32_t v = warp_off[warp] + incl - x;
+      if (pre_out) {
+        pre_out[i] = v;
+        tile_cnt[i] = 0;
+      } else {
+        tile_cnt[i] = v;
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (top_slot >= 0) counters[top_slot] = counters[ASH_CTR_TOP];
+      counters[total_slot] = s_total;
+      if (pre_out) pre_out[n_tiles] = s_total;
+    }
+    return;
+  }
   const int64_t chunks = (n_tiles + 31) / 32;
   const int64_t per = (chunks + 31) / 32;
   const int64_t c0 = warp * per, c1 = c0 + per < chunks ? c0 + per : chunks;
