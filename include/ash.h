@@ -111,7 +111,7 @@ int64_t ash_launch_count(void);
 int ash_set_commit_mode(int32_t bulk, int32_t sweep_div);
 /* Tables of at most `bytes` (slots x 16) never take the table sweep: their
  * lines stay in the L2 between the claim and the commit, so the commit's
- * state stores are L2 hits.  < 0: the default, a quarter of the device's L2;
+ * state stores are L2 hits.  < 0: the default, three quarters of the L2;
  * 0: every table may sweep (tests of the sweep on small maps). */
 int ash_set_sweep_table_min(int64_t bytes);
 
