@@ -625,10 +625,10 @@ class HashMap:
         return BatchResult(res.indices.cpu(), res.masks.cpu())
 
     def _pipelined(self, keys_h: torch.Tensor, vals_h, op: str) -> BatchResult:
-        if op == "insert":
-            self._settle()
         """Chunked H2D / kernels / D2H overlap for a host batch (op = insert
         or find).  Caller holds the guard and has checked capacity."""
+        if op == "insert":
+            self._settle()
         m = keys_h.shape[0]
         dev = self._device
         s = torch.cuda.current_stream(dev)
