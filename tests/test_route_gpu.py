@@ -200,6 +200,61 @@ def test_peer_put_with_device_count_matrix(cuda_ok, world, rank):
             assert np.all(got[:a] == -7) and np.all(got[b:] == -7)
 
 
+@pytest.mark.parametrize("world,rank", [(1, 0), (2, 0), (3, 1), (8, 7), (64, 5)])
+@pytest.mark.parametrize("n,shift", [(1, 0), (2047, 0), (2049, 1), (100_003, 0), (100_003, 3)])
+def test_peer_pull_with_device_count_matrix(cuda_ok, world, rank, n, shift):
+    """ash_route_pull_counts (world > 1: the staged pull, each block's owner
+    runs read as 16-byte vectors into shared memory): out[p] = owner o's
+    result at (rows of earlier sources at o) + jdx[p], mask = out >= 0; ragged
+    tails and unaligned outputs (shift) take the scalar path; an overflowed
+    exchange (recv_status[1]) leaves the outputs untouched."""
+    from paper_2110_00511_b200 import _lib
+    rng = np.random.default_rng(world * 1000 + rank + n + shift)
+    k = rng.integers(-2 ** 31, 2 ** 31, size=(n, 3)).astype(np.int32)
+    own = owner_of_np(k, world)
+    cnt = np.bincount(own, minlength=world)
+    C = rng.integers(0, 3000, size=(world, world)).astype(np.int64)
+    C[rank] = cnt
+    before = C[:rank].sum(0)
+    dev = torch.device("cuda")
+    kt = torch.from_numpy(k).to(dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    owners = torch.empty(n, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(int(_lib.lib.ash_route_scratch_len(n, world)), dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("ash_route_count", kt.data_ptr(), n, 3, world, counts.data_ptr(), owners.data_ptr(),
+              scratch.data_ptr(), scratch.numel(), st)
+    cap = int(C.sum(0).max())
+    P = _lib.c_void_p * world
+    mat = torch.from_numpy(C).to(dev)
+    bufk = [torch.empty((cap, 3), dtype=torch.int32, device=dev) for _ in range(world)]
+    jdx = torch.empty(n, dtype=torch.int32, device=dev)
+    _lib.call("ash_route_put_counts", kt.data_ptr(), n, 3, world, rank, owners.data_ptr(),
+              scratch.data_ptr(), scratch.numel(), mat.data_ptr(), cap,
+              P(*[b.data_ptr() for b in bufk]), 0, 0, P(*([None] * world)), jdx.data_ptr(), st)
+    # owner o's results: distinct per (owner, row), some negative (misses)
+    res = [torch.from_numpy(np.where(rng.random(cap) < 0.3, -1, np.arange(cap) * 64 + o).astype(np.int32)).to(dev)
+           for o in range(world)]
+    status = torch.zeros(2, dtype=torch.int32, device=dev)
+    out_all = torch.full((n + shift,), -99, dtype=torch.int32, device=dev)
+    msk_all = torch.full((n + shift,), 7, dtype=torch.uint8, device=dev)
+    out, msk = out_all[shift:], msk_all[shift:]
+    for over in (1, 0):
+        status[1] = over
+        _lib.call("ash_route_pull_counts", owners.data_ptr(), jdx.data_ptr(), n, world, rank, mat.data_ptr(),
+                  status.data_ptr(), P(*[r.data_ptr() for r in res]), out.data_ptr(), msk.data_ptr(), st)
+        if over:
+            assert torch.all(out == -99) and torch.all(msk == 7)
+    j = np.zeros(n, np.int64)
+    for o in range(world):
+        j[own == o] = np.arange(cnt[o])
+    resn = [r.cpu().numpy() for r in res]
+    expect = np.array([resn[o][before[o] + jj] for o, jj in zip(own, j)], dtype=np.int32)
+    assert np.array_equal(out.cpu().numpy(), expect)
+    assert np.array_equal(msk.cpu().numpy(), (expect >= 0).astype(np.uint8))
+    assert torch.all(out_all[:shift] == -99)
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_count_exchange_kernel(cuda_ok, world):
     """ash_route_exchange: every rank's exchange kernel (one per stream, all

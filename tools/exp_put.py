@@ -2,7 +2,9 @@
 into `world` owner buffers (all on this GPU: the store pattern, not NVLink),
 staged per-owner runs vs direct row stores (ASH_PUT_STAGED, read at load
 time: run once per setting).  Prints the median put time per world size and
-checks the rows landed where the direct put puts them."""
+checks the rows landed where the direct put puts them.  Then the pull of
+one int32 result per position back from the owner buffers (staged owner runs
+vs direct 4-byte gathers, ASH_PULL_STAGED; world 1 always gathers)."""
 import statistics
 import sys
 
@@ -49,3 +51,20 @@ for world in (1, 2, 8, 64):
         c = int(sel.sum())
         ok &= torch.equal(bk[o][:c], keys[sel]) and torch.equal(bp[o][:c], vals[sel])
     print(f"world {world:3d}: put median {statistics.median(ts) * 1e3:7.1f} us  rows ok={ok}", flush=True)
+    res = [torch.arange(cap, dtype=torch.int32, device=dev) * 64 + o for o in range(world)]
+    pr = P(*[r.data_ptr() for r in res])
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    msk = torch.empty(n, dtype=torch.uint8, device=dev)
+    ts = []
+    for rep in range(12):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.call("ash_route_pull_counts", owners.data_ptr(), jdx.data_ptr(), n, world, 0, C.data_ptr(), None,
+                  pr, out.data_ptr(), msk.data_ptr(), st)
+        b.record()
+        torch.cuda.synchronize()
+        if rep >= 2:
+            ts.append(a.elapsed_time(b))
+    own64 = owners.long()
+    ok = torch.equal(out, (jdx.long() * 64 + own64).int()) and bool(torch.all(msk == 1))
+    print(f"world {world:3d}: pull median {statistics.median(ts) * 1e3:7.1f} us  results ok={ok}", flush=True)
