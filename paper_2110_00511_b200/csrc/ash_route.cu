@@ -37,13 +37,6 @@ int g_put_staged = [] {
   return e ? (e[0] != '0' ? 1 : 0) : 1;
 }();
 
-// ASH_PULL_STAGED=0: world > 1 pulls gather each result straight from its
-// owner (k_route_pull) instead of staging the owners' runs (A/B runs)
-int g_pull_staged = [] {
-  const char* e = getenv("ASH_PULL_STAGED");
-  return e ? (e[0] != '0' ? 1 : 0) : 1;
-}();
-
 int rfail(const char* msg) {
   snprintf(g_route_err, sizeof(g_route_err), "%s", msg);
   return ASH_ERR_INVALID;
@@ -586,145 +579,6 @@ __global__ void __launch_bounds__(kBlock) k_route_pull(const uint8_t* __restrict
   }
 }
 
-// The pull for world > 1, staged like the put.  Positions [base, base +
-// kTile) of one block have, for each owner, jdx values forming ONE contiguous
-// run (the put's partition is stable over the whole batch, so jdx grows with
-// the position inside each owner's segment).  The block finds each owner's
-// run from the lowest / highest jdx its lanes hold (positions grow with the
-// lane, so no reduction: the first / last lane of the match group), reads the
-// peer runs with 16-byte vector loads into shared memory (each run placed
-// congruent with its source mod 16 bytes) and resolves every position from
-// there; rows of this rank's own shard are read directly.  A warp's 4-byte
-// gathers from N owners would otherwise fetch partly used sectors over
-// NVLink, several times each.  rank = kNoRank: every owner is staged.
-constexpr uint32_t kNoRank = 0xFFFFFFFFu;
-
-__global__ void __launch_bounds__(kBlock) k_route_pull_staged(const uint8_t* __restrict__ owners,
-                                                              const int32_t* __restrict__ jdx, int64_t n,
-                                                              PeerArgs pa, uint32_t world,
-                                                              int32_t* __restrict__ out,
-                                                              uint8_t* __restrict__ out_mask,
-                                                              const int64_t* __restrict__ cmat, uint32_t rank,
-                                                              const int32_t* recv_status) {
-  constexpr int kW = kBlock / 32;
-  constexpr int kStage = kTile + 4 * kMaxWorld;
-  constexpr int kChunk = 128;  // 16-byte vectors per warp task
-  __shared__ __align__(16) int32_t s_stage[kStage];
-  __shared__ const int32_t* s_base[kMaxWorld];
-  __shared__ int32_t s_lo[kMaxWorld], s_hi[kMaxWorld], s_sb[kMaxWorld];
-  __shared__ int32_t s_run_o[kMaxWorld], s_run_ch[kMaxWorld + 1], s_runs;
-  if (recv_status && recv_status[1]) return;  // an overflowed exchange stored nothing
-  for (uint32_t o = threadIdx.x; o < world; o += kBlock) {
-    int64_t off = pa.row_off[o];
-    if (cmat) {
-      off = 0;
-      for (uint32_t src = 0; src < rank; ++src) off += cmat[src * world + o];
-    }
-    s_base[o] = pa.ret[o] + off;
-    s_lo[o] = INT32_MAX;
-    s_hi[o] = -1;
-  }
-  __syncthreads();
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kTile);
-  const int64_t p0 = base + static_cast<int64_t>(threadIdx.x) * kItems;  // the thread's 8 consecutive positions
-  const bool vec = p0 + kItems <= n && ((reinterpret_cast<uintptr_t>(owners) | reinterpret_cast<uintptr_t>(jdx) |
-                                          reinterpret_cast<uintptr_t>(out) |
-                                          reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0;
-  uint32_t own[kItems];
-  int32_t j[kItems];
-  if (vec) {
-    const uint2 ow = *reinterpret_cast<const uint2*>(owners + p0);
-    const int4 ja = *reinterpret_cast<const int4*>(jdx + p0), jb = *reinterpret_cast<const int4*>(jdx + p0 + 4);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) own[i] = (ow.x >> (8 * i)) & 0xFF, own[4 + i] = (ow.y >> (8 * i)) & 0xFF;
-    j[0] = ja.x, j[1] = ja.y, j[2] = ja.z, j[3] = ja.w, j[4] = jb.x, j[5] = jb.y, j[6] = jb.z, j[7] = jb.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const bool in = p0 + i < n;
-      own[i] = in ? owners[p0 + i] : kNoRank;
-      j[i] = in ? jdx[p0 + i] : 0;
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const unsigned same = __match_any_sync(0xFFFFFFFFu, own[i]);
-    if (own[i] == kNoRank || own[i] == rank) continue;
-    if (lane == __ffs(same) - 1) atomicMin(&s_lo[own[i]], j[i]);
-    if (lane == 31 - __clz(same)) atomicMax(&s_hi[own[i]], j[i]);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t b = 0;
-    int32_t runs = 0, chunks = 0;
-    for (uint32_t o = 0; o < world; ++o) {
-      if (s_hi[o] < 0) continue;
-      const int32_t words = s_hi[o] - s_lo[o] + 1;
-      const int32_t* src = s_base[o] + s_lo[o];
-      const uint32_t a = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) >> 2) & 3);
-      b += (a - b) & 3u;  // congruent with the source mod 16 bytes
-      s_sb[o] = static_cast<int32_t>(b);
-      const int32_t head = min(words, static_cast<int32_t>((4 - a) & 3));
-      const int32_t nv = (words - head) >> 2;
-      s_run_o[runs] = static_cast<int32_t>(o);
-      s_run_ch[runs] = chunks;
-      chunks += nv > 0 ? (nv + kChunk - 1) / kChunk : 1;
-      ++runs;
-      b += static_cast<uint32_t>(words);
-    }
-    s_run_ch[runs] = chunks;
-    s_runs = runs;
-  }
-  __syncthreads();
-  {
-    const int32_t runs = s_runs, total = s_run_ch[runs];
-    int r = 0;
-    for (int32_t c = warp; c < total; c += kW) {
-      while (s_run_ch[r + 1] <= c) ++r;
-      const uint32_t o = static_cast<uint32_t>(s_run_o[r]);
-      const int32_t* src = s_base[o] + s_lo[o];
-      int32_t* dst = s_stage + s_sb[o];
-      const int32_t words = s_hi[o] - s_lo[o] + 1;
-      const int32_t head = min(words, static_cast<int32_t>((4 - ((reinterpret_cast<uintptr_t>(src) >> 2) & 3)) & 3));
-      const int32_t nv = (words - head) >> 2;
-      const int32_t k = c - s_run_ch[r], last = s_run_ch[r + 1] - s_run_ch[r] - 1;
-      if (k == 0 && lane < head) dst[lane] = src[lane];
-      const int4* s4 = reinterpret_cast<const int4*>(src + head);
-      int4* d4 = reinterpret_cast<int4*>(dst + head);
-      const int32_t v1 = min(nv, (k + 1) * kChunk);
-      for (int32_t v = k * kChunk + lane; v < v1; v += 32) d4[v] = s4[v];
-      const int32_t t0 = head + 4 * nv;
-      if (k == last && lane < words - t0) dst[t0 + lane] = src[t0 + lane];
-    }
-  }
-  __syncthreads();
-  int32_t v[kItems];
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint32_t o = own[i];
-    v[i] = o == kNoRank ? 0 : o == rank ? s_base[o][j[i]] : s_stage[s_sb[o] + j[i] - s_lo[o]];
-  }
-  if (vec) {
-    *reinterpret_cast<int4*>(out + p0) = make_int4(v[0], v[1], v[2], v[3]);
-    *reinterpret_cast<int4*>(out + p0 + 4) = make_int4(v[4], v[5], v[6], v[7]);
-    if (out_mask) {
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) lo |= static_cast<uint32_t>(v[i] >= 0) << (8 * i),
-                                  hi |= static_cast<uint32_t>(v[4 + i] >= 0) << (8 * i);
-      *reinterpret_cast<uint2*>(out_mask + p0) = make_uint2(lo, hi);
-    }
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    if (p0 + i >= n) break;
-    out[p0 + i] = v[i];
-    if (out_mask) out_mask[p0 + i] = v[i] >= 0;
-  }
-}
-
 // The rows this rank receives (sum of its column of the exchanged count
 // matrix) into status[0] for the device-sized shard op, 0 when some owner's
 // rows pass the receive capacity (k_route_put then stores nothing, on every
@@ -979,13 +833,8 @@ int ash_route_pull(const uint8_t* owners, const int32_t* jdx, int64_t n, int32_t
     pa.row_off[o] = row_off[o];
     pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
   }
-  if (world > 1 && g_pull_staged)
-    k_route_pull_staged<<<blocks((n + kTile - 1) / kTile, 1), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-        owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, kNoRank, nullptr);
-  else
-    k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-        owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, 0, nullptr);
-  note_launch();
+  k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, nullptr, 0, nullptr); note_launch();
   return rcheck("ash_route_pull");
 }
 
@@ -1031,14 +880,9 @@ int ash_route_pull_counts(const uint8_t* owners, const int32_t* jdx, int64_t n, 
     if (!peer_ret[o]) return rfail("null peer result buffer");
     pa.ret[o] = static_cast<const int32_t*>(peer_ret[o]);
   }
-  if (world > 1 && g_pull_staged)
-    k_route_pull_staged<<<blocks((n + kTile - 1) / kTile, 1), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-        owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank),
-        recv_status);
-  else
-    k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
-        owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank),
-        recv_status);
+  k_route_pull<<<blocks((n + 3) / 4, kBlock), kBlock, 0, static_cast<cudaStream_t>(stream)>>>(
+      owners, jdx, n, pa, static_cast<uint32_t>(world), out, out_mask, count_matrix, static_cast<uint32_t>(rank),
+      recv_status);
   note_launch();
   return rcheck("ash_route_pull_counts");
 }

@@ -3,8 +3,8 @@ into `world` owner buffers (all on this GPU: the store pattern, not NVLink),
 staged per-owner runs vs direct row stores (ASH_PUT_STAGED, read at load
 time: run once per setting).  Prints the median put time per world size and
 checks the rows landed where the direct put puts them.  Then the pull of
-one int32 result per position back from the owner buffers (staged owner runs
-vs direct 4-byte gathers, ASH_PULL_STAGED; world 1 always gathers)."""
+one int32 result per position back from the owner buffers (the staged-run
+variant of commit 9a67e8a, ASH_PULL_STAGED, is no longer built)."""
 import statistics
 import sys
 
