@@ -3,7 +3,10 @@ gloo control plane, receive/result buffers mapped across the processes by
 CUDA IPC (torch symmetric memory refuses ranks on one device; the
 world-size-1 symmetric test is in test_route_gpu.py), the fused put / pull
 routing kernels and the device map as each rank's shard.  Masks and values
-equal one big map."""
+equal one big map.  The same two-process runs cover the
+NCCL transport's code path (CudaRouter partition kernels, device shard map,
+un-permute) with gloo carrying its all_to_all_single (gloo stages CUDA
+tensors through the host; NCCL refuses two ranks on one device)."""
 import os
 import socket
 
@@ -20,7 +23,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, keys_all, vals_all, find_all, q):
+def _transport_kw(transport):
+    return dict(transport="peer", peer_mapping="ipc") if transport == "peer" else dict(transport="nccl")
+
+
+def _worker(rank, world, port, keys_all, vals_all, find_all, q, transport="peer"):
     import sys
     sys.path.insert(0, os.getcwd())
     import torch.distributed as dist
@@ -30,8 +37,7 @@ def _worker(rank, world, port, keys_all, vals_all, find_all, q):
         from paper_2110_00511_b200.partitioned import PartitionedHashMap
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
-        pm = PartitionedHashMap(len(keys_all), 3, [np.float32], device=dev, transport="peer",
-                                peer_mapping="ipc")
+        pm = PartitionedHashMap(len(keys_all), 3, [np.float32], device=dev, **_transport_kw(transport))
         sl = np.array_split(np.arange(len(keys_all)), world)[rank]
         fl = np.array_split(np.arange(len(find_all)), world)[rank]
         r = pm.insert(keys_all[sl], vals_all[sl])
@@ -48,7 +54,8 @@ def _worker(rank, world, port, keys_all, vals_all, find_all, q):
         dist.destroy_process_group()
 
 
-def test_peer_transport_two_ranks_share_one_gpu(cuda_ok):
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_peer_transport_two_ranks_share_one_gpu(cuda_ok, transport):
     import torch.multiprocessing as mp
     from oracle.ash_oracle import OracleMap
     world = 2
@@ -62,7 +69,8 @@ def test_peer_transport_two_ranks_share_one_gpu(cuda_ok):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, vals, probe, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, vals, probe, q, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -92,7 +100,7 @@ def test_peer_transport_two_ranks_share_one_gpu(cuda_ok):
     assert sum(out[r][8] for r in range(world)) == ref.size
 
 
-def _worker_growth(rank, world, port, batches, vals, q):
+def _worker_growth(rank, world, port, batches, vals, q, transport="peer"):
     """Shards that fill (and grow) at different rates: each rank picks its
     own shard op (device-sized or host-checked) while the collectives stay
     identical on every rank."""
@@ -105,8 +113,10 @@ def _worker_growth(rank, world, port, batches, vals, q):
         from paper_2110_00511_b200.partitioned import PartitionedHashMap
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
-        pm = PartitionedHashMap(1500, 3, [np.float32], device=dev, transport="peer", peer_mapping="ipc",
-                                recv_capacity=1200)
+        kw = _transport_kw(transport)
+        if transport == "peer":
+            kw["recv_capacity"] = 1200
+        pm = PartitionedHashMap(1500, 3, [np.float32], device=dev, **kw)
         outs = []
         for b, (keys, v) in enumerate(zip(batches, vals)):
             sl = np.array_split(np.arange(len(keys)), world)[rank]
@@ -121,7 +131,8 @@ def _worker_growth(rank, world, port, batches, vals, q):
         dist.destroy_process_group()
 
 
-def test_peer_transport_shards_diverge_and_grow(cuda_ok):
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_peer_transport_shards_diverge_and_grow(cuda_ok, transport):
     import torch.multiprocessing as mp
     from oracle.ash_oracle import OracleMap
     world = 2
@@ -131,7 +142,8 @@ def test_peer_transport_shards_diverge_and_grow(cuda_ok):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_growth, args=(r, world, port, batches, vals, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_growth, args=(r, world, port, batches, vals, q, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = {}
