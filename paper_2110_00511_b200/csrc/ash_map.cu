@@ -1802,18 +1802,28 @@ __device__ __forceinline__ int32_t quantize_one(T x, double cell, bool* bad) {
   return static_cast<int32_t>(q);
 }
 
-// floor(x / cell) without the division where that is provably exact: q =
-// RN(x * RN(1 / cell)) is within 2 ulp(q) of x / cell (one rounding of the
-// reciprocal, one of the product), so when q's fractional part is farther
-// than 4 ulp(q) from an integer, floor(q) == floor(x / cell).  Anything
-// else (near an integer, |q| >= 2^31, NaN, inf) takes the exact path.
+// floor(x / cell) without the division where that is provably exact.
+// q = RN(x * RN(1 / cell)) is within |q| * 2^-52 (1 + 2^-51) of t = x / cell
+// (one rounding of the reciprocal, one of the product), and numpy's
+// RN(t) within |t| * 2^-53 of t.  With tol = RN(|q| * 2^-50 + 2^-1000),
+// lo = RN(q - tol) <= RN(t) <= hi = RN(q + tol) (rounding is monotone), so
+// floor(lo) == floor(hi) gives floor(RN(t)), numpy's result.  Anything else
+// (an integer within tol, q = 0 or subnormal, |q| >= 2^30, NaN, inf) takes
+// the exact division.  Two F2I.FLOOR and one integer compare instead of a
+// floor, a fraction and three comparisons.
+template <typename T>
+__device__ __forceinline__ bool quantize_try(T x, double rcell, int32_t* out) {
+  const double q = static_cast<double>(x) * rcell;
+  const double tol = fma(fabs(q), 0x1p-50, 0x1p-1000);
+  const int32_t lo = __double2int_rd(__dsub_rn(q, tol)), hi = __double2int_rd(__dadd_rn(q, tol));
+  *out = lo;
+  return fabs(q) < 0x1p30 && lo == hi;
+}
+
 template <typename T>
 __device__ __forceinline__ int32_t quantize_fast(T x, double cell, double rcell, bool* bad) {
-  const double q = static_cast<double>(x) * rcell;
-  const double fq = floor(q);
-  const double f = q - fq;                     // exact for |q| < 2^52
-  const double tol = fabs(q) * 0x1p-50 + 0x1p-1000;
-  if (fabs(q) < 2147483648.0 && f > tol && f < 1.0 - tol) return static_cast<int32_t>(fq);
+  int32_t r;
+  if (quantize_try<T>(x, rcell, &r)) return r;
   return quantize_one<T>(x, cell, bad);
 }
 
@@ -2094,9 +2104,17 @@ __device__ __forceinline__ void cloud_claim_warp(uint4* __restrict__ slots, uint
                                                  uint32_t* __restrict__ cand, uint32_t* __restrict__ dem) {
   const unsigned lm = FULL ? 0xFFFFFFFFu : live;
   bool bad = false;
-  const uint32_t k0 = static_cast<uint32_t>(quantize_fast<T>(x0, cell, rcell, &bad));
-  const uint32_t k1 = static_cast<uint32_t>(quantize_fast<T>(x1, cell, rcell, &bad));
-  const uint32_t k2 = static_cast<uint32_t>(quantize_fast<T>(x2, cell, rcell, &bad));
+  // all three fast quantizes, then one (rarely taken) branch to the exact
+  // division for the coordinates that need it
+  int32_t q0, q1, q2;
+  const bool f0 = quantize_try<T>(x0, rcell, &q0), f1 = quantize_try<T>(x1, rcell, &q1),
+             f2 = quantize_try<T>(x2, rcell, &q2);
+  if (!(f0 && f1 && f2)) {
+    if (!f0) q0 = quantize_one<T>(x0, cell, &bad);
+    if (!f1) q1 = quantize_one<T>(x1, cell, &bad);
+    if (!f2) q2 = quantize_one<T>(x2, cell, &bad);
+  }
+  const uint32_t k0 = static_cast<uint32_t>(q0), k1 = static_cast<uint32_t>(q1), k2 = static_cast<uint32_t>(q2);
   if (bad) atomicOr(&counters[ASH_CTR_FLAGS], ASH_FLAG_RANGE);
   // a point in the same voxel as the (valid) previous lane's skips the table
   const unsigned vmask = __ballot_sync(lm, !bad);
