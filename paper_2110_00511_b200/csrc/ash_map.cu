@@ -1917,14 +1917,18 @@ struct FrameSrc {
   double fx, fy, cx, cy, dmin, dmax, trunc, two_trunc, step, block;
   double rblock;  // RN(1 / block), for quantize_fast
   double R[9], tr[3];
+  // exact n / d for n < 2^31 as (n * m) >> k (make_frame_src: divmagic)
+  uint64_t m_pp, m_w;
+  uint32_t k_pp, k_w;
   __device__ __forceinline__ bool key(int64_t p64, Key<3>& k, bool* bad) const {
-    // positions < 2^30 (check_batch): 32-bit divisions
+    // positions < 2^30 (check_batch): multiply-shift divisions
     const uint32_t p = static_cast<uint32_t>(p64);
-    const uint32_t pix = p / static_cast<uint32_t>(per_pixel);
+    const uint32_t pix = static_cast<uint32_t>((static_cast<uint64_t>(p) * m_pp) >> k_pp);  // p / per_pixel
     const int s = static_cast<int>(p - pix * static_cast<uint32_t>(per_pixel));
     const double z = __ldg(depth + pix);
     if (!(z > 0.0 && z >= dmin && z <= dmax)) return false;  // Frame.valid_mask (types.py:67-69)
-    const uint32_t v = pix / static_cast<uint32_t>(width), u = pix - v * static_cast<uint32_t>(width);
+    const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(pix) * m_w) >> k_w);  // pix / width
+    const uint32_t u = pix - v * static_cast<uint32_t>(width);
     const double x = __ddiv_rn(__dsub_rn(static_cast<double>(u), cx), fx);
     const double y = __ddiv_rn(__dsub_rn(static_cast<double>(v), cy), fy);
     double d = z;
@@ -2715,6 +2719,16 @@ void run_dedup_select(const Table& t, ash_map_t* ws, const Src& src, int64_t n, 
   note_launch();
 }
 
+// floor(n / d) == (n * m) >> k for every n < 2^31 (1 <= d < 2^31): k = 31 +
+// ceil(log2 d), m = ceil(2^k / d), so 2^k <= m d < 2^k + 2^(k - 31)
+// (Granlund-Montgomery, Thm 4.2)
+void divmagic(uint32_t d, uint64_t* m, uint32_t* k) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  *k = 31 + l;
+  *m = ((1ull << *k) + d - 1) / d;
+}
+
 int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t width, const double* cam,
                    const double* pose, double block_size, double trunc, int32_t neighbor, int64_t* n) {
   if (!depth || !cam || !pose) return fail(ASH_ERR_INVALID, "null frame pointer");
@@ -2735,6 +2749,9 @@ int make_frame_src(FrameSrc* f, const double* depth, int64_t height, int64_t wid
   const double ns = ceil((2 * trunc) / f->step) + 1;
   if (!(ns >= 1 && ns <= 4096)) return fail(ASH_ERR_INVALID, "too many ray samples per pixel");
   f->per_pixel = neighbor ? 27 : static_cast<int>(ns);
+  if (width >= (1ll << 30)) return fail(ASH_ERR_INVALID, "image too wide");
+  divmagic(static_cast<uint32_t>(f->per_pixel), &f->m_pp, &f->k_pp);
+  divmagic(static_cast<uint32_t>(width), &f->m_w, &f->k_w);
   for (int i = 0; i < 3; ++i) {
     for (int j = 0; j < 3; ++j) f->R[3 * i + j] = pose[4 * i + j];
     f->tr[i] = pose[4 * i + 3];
