@@ -169,3 +169,24 @@ def test_general_rotations_match_reference_digests(ash):
                                                                 device="cuda")), dtype=np.int32)
         assert len(got) == case["count"], case["quaternion"]
         assert hashlib.sha256(got.tobytes()).hexdigest() == case["sha256"], case["quaternion"]
+
+
+@pytest.mark.parametrize("w,h", [(37, 23), (61, 7), (5, 3)])
+def test_ragged_frames_distinct_blocks_match_oracle(ash, w, h):
+    """Image sizes whose candidate counts end inside a claim block (the
+    per-block pixel-ray table of the frame claim over a partial block, a
+    block spanning two image rows): frame_blocks and allocate_frame equal the
+    first-occurrence rows of the oracle's candidates, translated pose."""
+    from oracle import ash_oracle as O
+    from paper_2110_00511_b200.blocks import allocate_frame
+    cam = O.Camera(fx=30.0, fy=31.0, cx=(w - 1) / 2, cy=(h - 1) / 2, width=w, height=h)
+    pose = np.eye(4)
+    pose[:3, 3] = [0.013, -0.021, 0.007]
+    for depth in (O.plane_depth(cam, 0.9), O.sphere_depth(cam, radius=0.5)):
+        coords = O.candidate_blocks(depth, cam, pose, BLOCK, TRUNC)
+        want = _first_occurrence_rows(coords) if len(coords) else coords.reshape(0, 3)
+        G.eq(ash.frame_blocks(depth, cam, pose, BLOCK, TRUNC, device="cuda"), want, f"{w}x{h} blocks")
+        gm = ash.HashMap(4096, 3, [np.float32], device="cuda")
+        gi, _ = allocate_frame(gm, depth, cam, pose, BLOCK, TRUNC)
+        assert gm.size == len(want)
+        G.eq(gi, G.to_np(gm.find(want).indices), f"{w}x{h} gi")
