@@ -74,6 +74,11 @@ int check_launch(const char* what) {
 // ---------------------------------------------------------------------------
 // memory helpers
 
+__device__ __forceinline__ void st256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+}
+
 __device__ __forceinline__ void ld256_nc(const void* p, uint32_t (&r)[8]) {
   asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -1602,15 +1607,23 @@ __global__ void __launch_bounds__(kBlock) k_commit_sweep(Table t, const int32_t*
         }
       }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u) {
+      bool any = false;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const uint32_t st = w[u][4 * s + 3];
         if (spec ? (st < top || st >= TOMB) : ((st & 0xC0000000u) != PEND)) continue;
         uint32_t v = idx[u][s];
         if (rank_words) v = ident ? top + v : static_cast<uint32_t>(__ldg(heap + top + v));
-        t.slots[2 * static_cast<size_t>(b0 + u * stride) + s].w = v;
+        w[u][4 * s + 3] = v;
+        any = true;
       }
+      // the whole 32-byte bucket back as one full-sector store instead of
+      // 4-byte state stores (nothing else writes the table during the sweep;
+      // the key words and the other slot are rewritten unchanged): commit
+      // 0.167 -> 0.163 ms at C2, r02zzg
+      if (any) st256(t.slots + 2 * static_cast<size_t>(b0 + u * stride), w[u]);
+    }
   }
 }
 
